@@ -1,0 +1,225 @@
+/* pft_capi.h -- C ABI of the B200-native Partial Fourier Transform (arXiv 2008.12559).
+ *
+ * The reference (/root/reference) defines the PFT as SPEC modules with a C++ type
+ * header (proj/include/pft/types.hpp) and no compiled entry points.  Every function
+ * below replaces one SPEC operation; the citation after each declaration names it.
+ * The C++ API in <pft/pft.hpp> (namespace pft, SPEC names, exceptions) is a thin
+ * header-only layer over these symbols, and INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - No C++ types and no exceptions cross this boundary; every call returns pft_status.
+ *   - Complex numbers are pft_c128 = {re, im} doubles, layout-identical to
+ *     std::complex<double> / cuDoubleComplex / numpy complex128.
+ *   - Host planning objects (pft_table_t, pft_hplan_t) are immutable once built and
+ *     may be shared across threads.
+ *   - Device plans (pft_dplan_t) are read-only after creation.  pft_execute is
+ *     asynchronous on the given cudaStream_t, does not allocate, is capturable in a
+ *     CUDA graph, and is re-entrant on distinct (stream, workspace) pairs
+ *     (SPEC.md:263-265).  There is no CPU fallback: device calls fail with
+ *     PFT_ERR_NO_DEVICE / PFT_ERR_CUDA when no sm_100 device is usable.
+ */
+#ifndef PFT_CAPI_H
+#define PFT_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFT_TABLE_VERSION 1u
+#define PFT_MAX_TERMS 25 /* r <= 25, "typically 1 <= r <= 25" */
+
+typedef struct pft_c128 { double re, im; } pft_c128;
+
+typedef enum pft_status {
+    PFT_OK = 0,
+    PFT_ERR_INVALID_ARGUMENT = 1,     /* generic precondition failure                       */
+    PFT_ERR_P_NOT_DIVISOR = 2,        /* build_plan: p does not divide N       */
+    PFT_ERR_M_TOO_LARGE = 3,          /* build_plan: M > N/2               */
+    PFT_ERR_EPSILON_NOT_IN_TABLE = 4, /* build_plan/min_terms: table missing eps*/
+    PFT_ERR_RATIO_OUT_OF_RANGE = 5,   /* min_terms: M/p above every tabulated scope (:160)   */
+    PFT_ERR_LENGTH_MISMATCH = 6,      /* execute: a.len != plan.N              */
+    PFT_ERR_NON_FINITE = 7,           /* execute: non-finite input entries     */
+    PFT_ERR_IO = 8,                   /* table file unreadable / corrupted      */
+    PFT_ERR_VERSION_MISMATCH = 9,     /* table file version != 1             */
+    PFT_ERR_NO_DEVICE = 10,           /* no usable CUDA device                               */
+    PFT_ERR_CUDA = 11,                /* CUDA runtime error                                  */
+    PFT_ERR_UNSUPPORTED = 12,         /* shape this build does not handle                    */
+    PFT_ERR_INTERNAL = 13,
+    PFT_ERR_BUFFER_TOO_SMALL = 14
+} pft_status;
+
+const char* pft_status_string(pft_status s);
+/* Last detailed error message of the calling thread ("" if none). */
+const char* pft_last_error(void);
+/* Build identification: "pft-b200 <git/desc> sm_100a". */
+const char* pft_version(void);
+
+/* ------------------------------------------------------------------ minimax
+ * SPEC.md:30-114.  Near-minimax polynomial P(x)=sum_j w_j x^j for e^{iux} on |x|<=xi:
+ * Chebyshev (first-kind) interpolation, monomial expansion, certification on a grid
+ * of 4096*r equispaced points plus 8r Chebyshev nodes.          */
+
+/* best_approx(r, xi, u) -> coeffs[r], achieved_error */
+pft_status pft_best_approx(int r, double xi, double u, pft_c128* coeffs, double* achieved_error);
+/* scope_xi(eps, r) -> xi, coeffs[r], achieved */
+pft_status pft_scope_xi(double epsilon, int r, double* xi, pft_c128* coeffs, double* achieved_error);
+/* translate_poly(P, u, mu): Q(x) = e^{iu mu} P(x - mu) */
+pft_status pft_translate_poly(const pft_c128* coeffs, int r, double u, double mu, pft_c128* out);
+
+typedef struct pft_table_s* pft_table_t;
+
+/* The table shipped with the library: eps in {1e-1..1e-13} x r in 1..25 (SPEC.md:103,
+ * extended to BASELINE's eps=1e-12).  Owned by the library; do not destroy. */
+pft_status pft_table_default(pft_table_t* out);
+/* cmd_gen_table core: deterministic, byte-identical on regeneration. */
+pft_status pft_table_generate(const double* epsilons, int n_eps, int r_max, pft_table_t* out);
+/* save_table / load_table, PFTT v1 little-endian format. */
+pft_status pft_table_save(pft_table_t t, const char* path);
+pft_status pft_table_load(const char* path, pft_table_t* out);
+pft_status pft_table_save_csv(pft_table_t t, const char* path);
+void pft_table_destroy(pft_table_t t);
+/* Entry access.  n_entries counts (eps, r) cells; entry i has r_i coefficients. */
+pft_status pft_table_size(pft_table_t t, size_t* n_entries);
+pft_status pft_table_entry(pft_table_t t, size_t i, double* eps, int* r, double* xi,
+                           pft_c128* coeffs /* >= PFT_MAX_TERMS */, double* achieved_error);
+pft_status pft_table_lookup(pft_table_t t, double eps, int r, double* xi, pft_c128* coeffs,
+                            double* achieved_error);
+
+/* ------------------------------------------------------------------ planner
+ * SPEC.md:116-195, Algorithm 1.                                */
+
+/* divisors(N) ascending; *count is set even when cap is too small. */
+pft_status pft_divisors(uint64_t N, uint64_t* out, size_t cap, size_t* count);
+/* min_terms(eps, M, p) */
+pft_status pft_min_terms(pft_table_t t, double epsilon, uint64_t M, uint64_t p, int* r);
+/* select_divisor(N, M, table, eps): argmin_p r(N + p log2 max(p,2) + M), ties -> smaller p
+ *                                                                   */
+pft_status pft_select_divisor(pft_table_t t, uint64_t N, uint64_t M, double epsilon,
+                              uint64_t* p, int* r, double* cost);
+
+typedef struct pft_hplan_s* pft_hplan_t;
+
+typedef struct pft_plan_info {
+    uint64_t N, M;
+    int64_t mu;
+    uint64_t p, q;
+    int32_t r;
+    int32_t reserved;
+    double epsilon;
+    double achieved_epsilon;
+    double xi;
+    double estimated_cost; /* SPEC cost model value for this (p, r) */
+    uint64_t plan_id;
+} pft_plan_info;
+
+/* build_plan(N, M, mu, p (0 = auto via select_divisor), eps, table) */
+pft_status pft_plan_build(pft_table_t t, uint64_t N, uint64_t M, int64_t mu, uint64_t p,
+                          double epsilon, pft_hplan_t* out);
+void pft_plan_destroy(pft_hplan_t plan);
+pft_status pft_plan_info_get(pft_hplan_t plan, pft_plan_info* info);
+/* Plan tables (host copies).  B: q*r row-major; w: r; phase: q (e^{-2 pi i mu (l-q/2)/N});
+ * tvals: q (1-2l/q); post_powers: (2M+1)*r row-major by slot; post_twiddles: 2M+1. */
+pft_status pft_plan_copy_B(pft_hplan_t plan, pft_c128* out);
+pft_status pft_plan_copy_w(pft_hplan_t plan, pft_c128* out);
+pft_status pft_plan_copy_phase(pft_hplan_t plan, pft_c128* out);
+pft_status pft_plan_copy_tvals(pft_hplan_t plan, double* out);
+pft_status pft_plan_copy_post_powers(pft_hplan_t plan, double* out);
+pft_status pft_plan_copy_post_twiddles(pft_hplan_t plan, pft_c128* out);
+/* Plan summary JSON into buf; *needed includes the terminating NUL. */
+pft_status pft_plan_json(pft_hplan_t plan, char* buf, size_t cap, size_t* needed);
+
+/* ------------------------------------------------------------------ device (sm_100a)
+ * transform.execute (Algorithm 2) as two kernels:
+ *   K1  contraction C = A x B fused with the first (row-residue) pass of the r length-p
+ *       FFTs, one CTA per residue class k = c (mod P2);
+ *   K2  remaining FFT pass, pruned to the 2M+1 needed bins, fused with the Eq. (7)
+ *       post-process.
+ * See DESIGN.md for the data layout.                                                */
+
+typedef struct pft_dplan_s* pft_dplan_t;
+
+typedef struct pft_dplan_opts {
+    int device;        /* CUDA ordinal                                              */
+    uint64_t p2;       /* residue classes for K1 (0 = auto); must divide p          */
+    int threads;       /* K1 block size (0 = auto)                                  */
+    int reserved[6];
+} pft_dplan_opts;
+
+/* Upload a host plan to the device.  opts may be NULL (defaults). */
+pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dplan_t* out);
+void pft_dplan_destroy(pft_dplan_t d);
+/* Chosen decomposition p = P1 * P2 (P1 = local FFT length per residue class). */
+pft_status pft_dplan_layout(pft_dplan_t d, uint64_t* p1, uint64_t* p2);
+/* Device workspace bytes for `batch` independent transforms. */
+pft_status pft_workspace_bytes(pft_dplan_t d, size_t batch, size_t* bytes);
+/* Bytes of one partial slab (the reducible intermediate, p*r complex128 per transform). */
+pft_status pft_partial_bytes(pft_dplan_t d, size_t batch, size_t* bytes);
+
+/* execute: d_in holds `batch` signals of N complex128, signal b at d_in + b*in_stride;
+ * d_out receives batch x (2M+1) values, signal b at d_out + b*(2M+1).
+ * d_ws: pft_workspace_bytes(batch) bytes of device memory, or NULL to use the plan's
+ * own workspace (then calls on the plan must be serialised).  stream: cudaStream_t. */
+pft_status pft_execute(pft_dplan_t d, const pft_c128* d_in, size_t batch, size_t in_stride,
+                       pft_c128* d_out, void* d_ws, void* stream);
+
+/* Sharded single transform (contraction-axis split, BASELINE.json configs[4]):
+ * each rank owns, for every row k in [p], the column slice [l0, l0 + lq) of A (its
+ * local buffer is p rows of row_stride >= lq elements); see pft_shard_columns.  execute_partial contracts the local slice
+ * and applies K1's FFT pass, writing a reducible partial slab (sum over ranks ==
+ * the unsharded slab); finalize turns the reduced slab into the 2M+1 outputs. */
+pft_status pft_execute_partial(pft_dplan_t d, const pft_c128* d_in_local, uint64_t l0,
+                               uint64_t lq, uint64_t row_stride, pft_c128* d_partial,
+                               void* stream);
+pft_status pft_finalize(pft_dplan_t d, const pft_c128* d_partial, size_t batch,
+                        pft_c128* d_out, void* stream);
+/* Column range [l0, l0+lq) of rank `rank` among `world` (contiguous, near-equal). */
+pft_status pft_shard_columns(uint64_t q, int world, int rank, uint64_t* l0, uint64_t* lq);
+
+/* Status word written by the kernels (non-finite output => non-finite input).
+ * Synchronises `stream`; *flags bit0 = non-finite seen since the last reset. */
+pft_status pft_status_query(pft_dplan_t d, void* stream, int* flags, int reset);
+
+/* End-to-end convenience used by the C++ API and the e2e benchmark: copies h_in
+ * (pinned or pageable) H2D, executes, copies the result D2H, synchronises and maps
+ * a non-finite flag to PFT_ERR_NON_FINITE.  d_in/d_out are device staging buffers of
+ * batch*N and batch*(2M+1) elements (NULL = allocate/free internally). */
+pft_status pft_execute_host(pft_dplan_t d, const pft_c128* h_in, size_t batch, pft_c128* h_out,
+                            pft_c128* d_in, pft_c128* d_out, void* stream);
+
+/* ------------------------------------------------------------------ synthetic inputs
+ * Seeded counter-based generators (BASELINE.json configs), identical bit-for-bit on
+ * host and device for the uniform kind.  kind: 0 = uniform[-1,1] re/im,
+ * 1 = complex normal CN(0,1) (re,im ~ N(0,1/2)), 2 = sparse spectrum (n_tones tones at
+ * integer frequencies freqs[] with amplitudes amps[] plus CN(0, sigma^2) noise). */
+typedef struct pft_signal_desc {
+    int kind;
+    uint64_t seed;
+    uint64_t N;
+    uint64_t index_offset; /* global element index of element 0 (batched signals)  */
+    int n_tones;
+    const int64_t* freqs;  /* host pointer, n_tones                                  */
+    const pft_c128* amps;  /* host pointer, n_tones                                  */
+    double sigma;
+} pft_signal_desc;
+
+pft_status pft_generate_host(const pft_signal_desc* desc, pft_c128* out, uint64_t count);
+pft_status pft_generate_device(const pft_signal_desc* desc, pft_c128* d_out, uint64_t count,
+                               void* stream);
+/* The tone set of BASELINE configs[1]: n distinct integer frequencies uniform in
+ * [lo, hi] and CN(0,1) amplitudes, drawn from `seed`. */
+pft_status pft_sparse_tones(uint64_t seed, int n, int64_t lo, int64_t hi, int64_t* freqs,
+                            pft_c128* amps);
+
+/* ------------------------------------------------------------------ device introspection */
+/* Number of kernel launches one pft_execute issues (for launch accounting). */
+pft_status pft_launches_per_execute(pft_dplan_t d, int* launches);
+pft_status pft_device_count(int* n);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* PFT_CAPI_H */

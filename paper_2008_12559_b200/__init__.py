@@ -1,0 +1,528 @@
+"""B200-native Partial Fourier Transform (arXiv 2008.12559) -- Python mirror of the API.
+
+The product is libpft_b200.so: a C++20 host library (minimax table, planner) and sm_100a
+CUDA kernels behind the C ABI in include/pft_capi.h.  This module mirrors the reference's
+plan-then-execute interface (SPEC.md modules minimax / planner / transform; type names of
+proj/include/pft/types.hpp) with the same argument meaning and error behaviour, so tests
+read like the reference's own acceptance tests.  Every call goes through the C ABI; the
+transform itself runs only on the GPU (no CPU fallback -- see oracle/ for the checker).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+from ._capi import c128
+
+__all__ = [
+    "PftError", "ApproxPoly", "ScopeTable", "CostEstimate", "TargetRange", "PartialSpectrum", "PftPlan",
+    "DevicePlan", "best_approx", "scope_xi", "translate_poly", "divisors", "min_terms", "select_divisor",
+    "build_plan", "execute", "mod_index", "l1_norm", "generate_signal", "sparse_tones", "shard_columns",
+    "device_count", "lib",
+]
+
+DEFAULT_EPSILON = 1e-12  # BASELINE.json configs
+
+
+def lib() -> C.CDLL:
+    return _capi.load()
+
+
+# ----------------------------------------------------------------------------- errors
+
+class PftError(Exception):
+    """A non-OK pft_status from the C ABI."""
+
+    def __init__(self, status: int, message: str):
+        self.status = status
+        self.name = _capi.STATUS_NAMES.get(status, f"status {status}")
+        super().__init__(f"{self.name}: {message}")
+
+
+class PftValueError(PftError, ValueError):
+    pass
+
+
+class PftIOError(PftError, OSError):
+    pass
+
+
+class PftDeviceError(PftError, RuntimeError):
+    pass
+
+
+_VALUE = {1, 2, 3, 4, 5, 6, 7, 12, 14}
+_IO = {8, 9}
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    msg = (lib().pft_last_error() or b"").decode() or lib().pft_status_string(status).decode()
+    cls = PftValueError if status in _VALUE else PftIOError if status in _IO else PftDeviceError
+    raise cls(status, msg)
+
+
+def _cbuf(n: int) -> np.ndarray:
+    return np.zeros(max(n, 1), dtype=np.complex128)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+# ----------------------------------------------------------------------------- types.hpp mirror
+
+def mod_index(m: int, n: int) -> int:
+    """Non-negative m mod n (types.hpp:15-20)."""
+    return m % n
+
+
+def l1_norm(v) -> float:
+    """sum |v_i| (types.hpp:92-96)."""
+    return float(np.sum(np.abs(np.asarray(v, dtype=np.complex128))))
+
+
+@dataclasses.dataclass(frozen=True)
+class TargetRange:
+    """R_{mu,M} = [mu - M, mu + M] (types.hpp:24-43)."""
+    mu: int = 0
+    half_width: int = 0
+
+    def count(self) -> int:
+        return 2 * self.half_width + 1
+
+    def first(self) -> int:
+        return self.mu - self.half_width
+
+    def last(self) -> int:
+        return self.mu + self.half_width
+
+    def contains(self, m: int) -> bool:
+        return self.first() <= m <= self.last()
+
+    def slot(self, m: int) -> int:
+        if not self.contains(m):
+            raise IndexError(f"TargetRange::slot: index {m} outside [{self.first()}, {self.last()}]")
+        return m - self.first()
+
+
+@dataclasses.dataclass
+class PartialSpectrum:
+    """values[slot(m)] estimates coefficient m (types.hpp:47-53)."""
+    range: TargetRange
+    values: np.ndarray
+    plan_id: int = 0
+
+    def at(self, m: int) -> complex:
+        return complex(self.values[self.range.slot(m)])
+
+
+# ----------------------------------------------------------------------------- minimax
+
+@dataclasses.dataclass
+class ApproxPoly:
+    """SPEC.md:35-41."""
+    coeffs: np.ndarray
+    base_frequency: float
+    scope: float
+    achieved_error: float
+
+    @property
+    def degree(self) -> int:
+        return len(self.coeffs) - 1
+
+    def __call__(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        acc = np.zeros(x.shape, dtype=np.complex128)
+        pw = np.ones(x.shape)
+        for c in self.coeffs:
+            acc = acc + c * pw
+            pw = pw * x
+        return acc
+
+
+def best_approx(r: int, xi: float, u: float) -> ApproxPoly:
+    """Near-minimax degree r-1 polynomial for e^{iux} on |x| <= xi."""
+    out = _cbuf(r)
+    ach = C.c_double()
+    _check(lib().pft_best_approx(int(r), float(xi), float(u), _ptr(out), C.byref(ach)))
+    return ApproxPoly(out[:r].copy(), float(u), abs(float(xi)), ach.value)
+
+
+def scope_xi(epsilon: float, r: int) -> tuple[float, ApproxPoly]:
+    """Largest certified xi with error <= epsilon, and its polynomial."""
+    out = _cbuf(r)
+    xi = C.c_double()
+    ach = C.c_double()
+    _check(lib().pft_scope_xi(float(epsilon), int(r), C.byref(xi), _ptr(out), C.byref(ach)))
+    return xi.value, ApproxPoly(out[:r].copy(), float(np.pi), xi.value, ach.value)
+
+
+def translate_poly(poly: ApproxPoly, u: float, mu: float) -> ApproxPoly:
+    """Q(x) = e^{iu mu} P(x - mu) (Lemma 1)."""
+    c = np.ascontiguousarray(poly.coeffs, dtype=np.complex128)
+    out = _cbuf(len(c))
+    _check(lib().pft_translate_poly(_ptr(c), len(c), float(u), float(mu), _ptr(out)))
+    return ApproxPoly(out[:len(c)].copy(), float(u), poly.scope, poly.achieved_error)
+
+
+@dataclasses.dataclass
+class TableEntry:
+    epsilon: float
+    r: int
+    xi: float
+    coeffs: np.ndarray
+    achieved_error: float
+
+
+class ScopeTable:
+    """Persisted map (eps, r) -> (xi, coeffs) (PFTT v1 SPEC.md:108)."""
+
+    version = 1
+
+    def __init__(self, handle, owned: bool):
+        self._h = handle
+        self._owned = owned
+
+    def __del__(self):
+        if getattr(self, "_owned", False) and self._h:
+            lib().pft_table_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @classmethod
+    def default(cls) -> "ScopeTable":
+        h = C.c_void_p()
+        _check(lib().pft_table_default(C.byref(h)))
+        return cls(h, owned=False)
+
+    @classmethod
+    def generate(cls, epsilons: Optional[Sequence[float]] = None, r_max: int = 25) -> "ScopeTable":
+        h = C.c_void_p()
+        if epsilons:
+            arr = np.ascontiguousarray(epsilons, dtype=np.float64)
+            _check(lib().pft_table_generate(_ptr(arr), len(arr), int(r_max), C.byref(h)))
+        else:
+            _check(lib().pft_table_generate(None, 0, int(r_max), C.byref(h)))
+        return cls(h, owned=True)
+
+    @classmethod
+    def load(cls, path) -> "ScopeTable":
+        h = C.c_void_p()
+        _check(lib().pft_table_load(str(path).encode(), C.byref(h)))
+        return cls(h, owned=True)
+
+    def save(self, path) -> None:
+        _check(lib().pft_table_save(self._h, str(path).encode()))
+
+    def save_csv(self, path) -> None:
+        _check(lib().pft_table_save_csv(self._h, str(path).encode()))
+
+    def __len__(self) -> int:
+        n = C.c_size_t()
+        _check(lib().pft_table_size(self._h, C.byref(n)))
+        return n.value
+
+    def entry(self, i: int) -> TableEntry:
+        eps, xi, ach = C.c_double(), C.c_double(), C.c_double()
+        r = C.c_int()
+        buf = _cbuf(25)
+        _check(lib().pft_table_entry(self._h, i, C.byref(eps), C.byref(r), C.byref(xi), _ptr(buf), C.byref(ach)))
+        return TableEntry(eps.value, r.value, xi.value, buf[:r.value].copy(), ach.value)
+
+    @property
+    def entries(self) -> list[TableEntry]:
+        return [self.entry(i) for i in range(len(self))]
+
+    def lookup(self, epsilon: float, r: int) -> TableEntry:
+        xi, ach = C.c_double(), C.c_double()
+        buf = _cbuf(25)
+        _check(lib().pft_table_lookup(self._h, float(epsilon), int(r), C.byref(xi), _ptr(buf), C.byref(ach)))
+        return TableEntry(float(epsilon), int(r), xi.value, buf[:r].copy(), ach.value)
+
+    @property
+    def epsilon_grid(self) -> list[float]:
+        seen: list[float] = []
+        for e in self.entries:
+            if not any(abs(e.epsilon - s) <= 1e-9 * s for s in seen):
+                seen.append(e.epsilon)
+        return seen
+
+    @property
+    def r_max(self) -> int:
+        return max(e.r for e in self.entries)
+
+
+# ----------------------------------------------------------------------------- planner
+
+@dataclasses.dataclass(frozen=True)
+class CostEstimate:
+    """SPEC.md:130-133."""
+    p: int
+    r: int
+    cost: float
+
+
+def _table(table: Optional[ScopeTable]) -> ScopeTable:
+    return table if table is not None else ScopeTable.default()
+
+
+def divisors(N: int) -> list[int]:
+    """All divisors of N, ascending."""
+    cnt = C.c_size_t()
+    st = lib().pft_divisors(int(N), None, 0, C.byref(cnt))
+    if st not in (0, 14):
+        _check(st)
+    arr = np.zeros(max(cnt.value, 1), dtype=np.uint64)
+    _check(lib().pft_divisors(int(N), _ptr(arr), cnt.value, C.byref(cnt)))
+    return [int(x) for x in arr[:cnt.value]]
+
+
+def min_terms(epsilon: float, M: int, p: int, table: Optional[ScopeTable] = None) -> int:
+    """min{r : xi(eps, r) >= M/p}."""
+    r = C.c_int()
+    _check(lib().pft_min_terms(_table(table).handle, float(epsilon), int(M), int(p), C.byref(r)))
+    return r.value
+
+
+def select_divisor(N: int, M: int, table: Optional[ScopeTable] = None,
+                   epsilon: float = DEFAULT_EPSILON) -> tuple[int, CostEstimate]:
+    """Cost-model choice of p."""
+    p = C.c_uint64()
+    r = C.c_int()
+    cost = C.c_double()
+    _check(lib().pft_select_divisor(_table(table).handle, int(N), int(M), float(epsilon), C.byref(p),
+                                    C.byref(r), C.byref(cost)))
+    return p.value, CostEstimate(p.value, r.value, cost.value)
+
+
+class PftPlan:
+    """Frozen configuration of Algorithm 1.  Arrays are host copies of the
+    plan tables the GPU consumes; the oracle consumes the same arrays."""
+
+    def __init__(self, handle):
+        self._h = handle
+        info = _capi.PlanInfo()
+        _check(lib().pft_plan_info_get(handle, C.byref(info)))
+        self.N, self.M, self.mu = int(info.N), int(info.M), int(info.mu)
+        self.p, self.q, self.r = int(info.p), int(info.q), int(info.r)
+        self.epsilon = float(info.epsilon)
+        self.achieved_epsilon = float(info.achieved_epsilon)
+        self.xi = float(info.xi)
+        self.estimated_cost = float(info.estimated_cost)
+        self.plan_id = int(info.plan_id)
+        self._cache: dict = {}
+        self._dplans: dict = {}
+
+    def __del__(self):
+        for d in getattr(self, "_dplans", {}).values():
+            d.close()
+        if getattr(self, "_h", None):
+            lib().pft_plan_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def range(self) -> TargetRange:
+        return TargetRange(self.mu, self.M)
+
+    def _get(self, name: str, n: int, dtype, fn):
+        if name not in self._cache:
+            arr = np.zeros(max(n, 1), dtype=dtype)
+            _check(fn(self._h, _ptr(arr)))
+            self._cache[name] = arr[:n]
+        return self._cache[name]
+
+    @property
+    def B(self) -> np.ndarray:
+        return self._get("B", self.q * self.r, np.complex128, lib().pft_plan_copy_B).reshape(self.q, self.r)
+
+    @property
+    def w(self) -> np.ndarray:
+        return self._get("w", self.r, np.complex128, lib().pft_plan_copy_w)
+
+    @property
+    def phase(self) -> np.ndarray:
+        return self._get("phase", self.q, np.complex128, lib().pft_plan_copy_phase)
+
+    @property
+    def tvals(self) -> np.ndarray:
+        return self._get("tvals", self.q, np.float64, lib().pft_plan_copy_tvals)
+
+    @property
+    def post_powers(self) -> np.ndarray:
+        W = 2 * self.M + 1
+        return self._get("pp", W * self.r, np.float64, lib().pft_plan_copy_post_powers).reshape(W, self.r)
+
+    @property
+    def post_twiddles(self) -> np.ndarray:
+        return self._get("pt", 2 * self.M + 1, np.complex128, lib().pft_plan_copy_post_twiddles)
+
+    def json(self) -> str:
+        need = C.c_size_t()
+        lib().pft_plan_json(self._h, None, 0, C.byref(need))
+        buf = C.create_string_buffer(need.value)
+        _check(lib().pft_plan_json(self._h, buf, need.value, C.byref(need)))
+        return buf.value.decode()
+
+    def device_plan(self, device: int = 0, p2: int = 0) -> "DevicePlan":
+        key = (device, p2)
+        if key not in self._dplans:
+            self._dplans[key] = DevicePlan(self, device=device, p2=p2)
+        return self._dplans[key]
+
+
+def build_plan(N: int, M: int, mu: int = 0, p: Optional[int] = None, epsilon: float = DEFAULT_EPSILON,
+               table: Optional[ScopeTable] = None) -> PftPlan:
+    """Algorithm 1.  p=None selects p with the SPEC cost model."""
+    h = C.c_void_p()
+    _check(lib().pft_plan_build(_table(table).handle, int(N), int(M), int(mu), int(p or 0), float(epsilon),
+                                C.byref(h)))
+    return PftPlan(h)
+
+
+# ----------------------------------------------------------------------------- transform (GPU)
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(lib().pft_device_count(C.byref(n)))
+    return n.value
+
+
+class DevicePlan:
+    """A plan uploaded to one B200 (pft_dplan_t).  Device buffers are passed as raw
+    pointers (e.g. torch.Tensor.data_ptr() of complex128 CUDA tensors)."""
+
+    def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0):
+        self.plan = plan
+        opts = _capi.DPlanOpts()
+        opts.device = device
+        opts.p2 = p2
+        h = C.c_void_p()
+        _check(lib().pft_dplan_create(plan.handle, C.byref(opts), C.byref(h)))
+        self._h = h
+        p1, pp2 = C.c_uint64(), C.c_uint64()
+        _check(lib().pft_dplan_layout(h, C.byref(p1), C.byref(pp2)))
+        self.P1, self.P2 = p1.value, pp2.value
+        self.device = device
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().pft_dplan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def workspace_bytes(self, batch: int = 1) -> int:
+        n = C.c_size_t()
+        _check(lib().pft_workspace_bytes(self._h, batch, C.byref(n)))
+        return n.value
+
+    def launches_per_execute(self) -> int:
+        n = C.c_int()
+        _check(lib().pft_launches_per_execute(self._h, C.byref(n)))
+        return n.value
+
+    def execute_ptr(self, d_in: int, d_out: int, batch: int = 1, in_stride: int = 0, d_ws: int = 0,
+                    stream: int = 0) -> None:
+        _check(lib().pft_execute(self._h, C.c_void_p(d_in), batch, in_stride, C.c_void_p(d_out),
+                                 C.c_void_p(d_ws or None), C.c_void_p(stream or None)))
+
+    def execute_partial_ptr(self, d_in_local: int, l0: int, lq: int, row_stride: int, d_partial: int,
+                            stream: int = 0) -> None:
+        _check(lib().pft_execute_partial(self._h, C.c_void_p(d_in_local), l0, lq, row_stride,
+                                         C.c_void_p(d_partial), C.c_void_p(stream or None)))
+
+    def finalize_ptr(self, d_partial: int, d_out: int, batch: int = 1, stream: int = 0) -> None:
+        _check(lib().pft_finalize(self._h, C.c_void_p(d_partial), batch, C.c_void_p(d_out),
+                                  C.c_void_p(stream or None)))
+
+    def status(self, stream: int = 0, reset: bool = True) -> int:
+        f = C.c_int()
+        _check(lib().pft_status_query(self._h, C.c_void_p(stream or None), C.byref(f), int(reset)))
+        return f.value
+
+    def execute_host(self, a: np.ndarray, batch: int = 1) -> np.ndarray:
+        """End-to-end: host input -> H2D -> kernels -> D2H (raises on non-finite input)."""
+        a = np.ascontiguousarray(a, dtype=np.complex128)
+        if a.size != self.plan.N * batch:
+            raise PftValueError(6, f"length mismatch: got {a.size}, plan N*batch = {self.plan.N * batch}")
+        out = np.zeros(batch * (2 * self.plan.M + 1), dtype=np.complex128)
+        _check(lib().pft_execute_host(self._h, _ptr(a), batch, _ptr(out), None, None, None))
+        return out
+
+
+def execute(plan: PftPlan, a, device: int = 0) -> PartialSpectrum:
+    """Algorithm 2 on the GPU: host vector in, PartialSpectrum out."""
+    a = np.ascontiguousarray(np.asarray(a), dtype=np.complex128).reshape(-1)
+    if a.size != plan.N:
+        raise PftValueError(6, f"execute: length mismatch (a.len={a.size}, plan.N={plan.N})")
+    vals = plan.device_plan(device).execute_host(a)
+    return PartialSpectrum(plan.range, vals, plan.plan_id)
+
+
+# ----------------------------------------------------------------------------- sharding + inputs
+
+def shard_columns(q: int, world: int, rank: int) -> tuple[int, int]:
+    """Contraction-axis slice [l0, l0+lq) owned by `rank` (C5 sharding)."""
+    l0, lq = C.c_uint64(), C.c_uint64()
+    _check(lib().pft_shard_columns(int(q), int(world), int(rank), C.byref(l0), C.byref(lq)))
+    return l0.value, lq.value
+
+
+def sparse_tones(seed: int, n: int, lo: int, hi: int) -> tuple[np.ndarray, np.ndarray]:
+    f = np.zeros(max(n, 1), dtype=np.int64)
+    a = _cbuf(n)
+    _check(lib().pft_sparse_tones(int(seed), int(n), int(lo), int(hi), _ptr(f), _ptr(a)))
+    return f[:n].copy(), a[:n].copy()
+
+
+KIND_UNIFORM, KIND_NORMAL, KIND_SPARSE = 0, 1, 2
+
+
+def _desc(kind: int, seed: int, N: int, offset: int, freqs=None, amps=None, sigma: float = 0.0):
+    d = _capi.SignalDesc()
+    d.kind, d.seed, d.N, d.index_offset = kind, seed, N, offset
+    keep = []
+    if kind == KIND_SPARSE:
+        f = np.ascontiguousarray(freqs, dtype=np.int64)
+        a = np.ascontiguousarray(amps, dtype=np.complex128)
+        keep = [f, a]
+        d.n_tones = len(f)
+        d.freqs = f.ctypes.data_as(C.POINTER(C.c_int64))
+        d.amps = a.ctypes.data_as(C.POINTER(c128))
+        d.sigma = sigma
+    return d, keep
+
+
+def generate_signal(kind: int, seed: int, count: int, N: int = 0, offset: int = 0, freqs=None, amps=None,
+                    sigma: float = 0.0) -> np.ndarray:
+    """Seeded synthetic input on the host (bit-identical to the device generator for kind 0)."""
+    d, keep = _desc(kind, seed, N, offset, freqs, amps, sigma)
+    out = np.zeros(max(count, 1), dtype=np.complex128)
+    _check(lib().pft_generate_host(C.byref(d), _ptr(out), count))
+    del keep
+    return out[:count]
+
+
+def generate_signal_device(d_out: int, kind: int, seed: int, count: int, N: int = 0, offset: int = 0,
+                           freqs=None, amps=None, sigma: float = 0.0, stream: int = 0) -> None:
+    d, keep = _desc(kind, seed, N, offset, freqs, amps, sigma)
+    _check(lib().pft_generate_device(C.byref(d), C.c_void_p(d_out), count, C.c_void_p(stream or None)))
+    del keep

@@ -1,0 +1,122 @@
+"""Build libpft_b200.so in-tree (host C++20 + sm_100a CUDA), with incremental rebuilds.
+
+    python -m paper_2008_12559_b200.build [--force] [--verbose]
+
+Host sources (csrc/host/*.cpp) are compiled with g++ and OpenMP; device sources
+(csrc/device/*.cu) with nvcc for sm_100a only (-gencode arch=compute_100a,code=sm_100a)
+and -lineinfo so ncu's source page maps to the kernels.  The CUDA runtime is linked
+statically so the library loads on a machine without a GPU (planning works, device
+calls return PFT_ERR_NO_DEVICE).
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+BUILD = PKG / "build"
+LIB = PKG / "libpft_b200.so"
+TABLE = PKG / "data" / "scope_table_v1.pftt"
+INCLUDE = ROOT / "include"
+
+NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
+# /usr/bin/g++ first: the image's /opt/gcc wrapper cannot locate libgomp when linking
+CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else os.environ.get("CXX", "g++")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# x86-64-v3 (AVX2/FMA): the library is built here and executed on the GPU box's host.
+HOST_FLAGS = ["-std=c++20", "-O3", "-march=x86-64-v3", "-fPIC", "-fopenmp", "-Wall", "-Wextra",
+              "-Wno-unused-parameter"]
+NVCC_FLAGS = ["-std=c++20", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-fopenmp",
+              "-Xptxas", "-O3", "--expt-relaxed-constexpr"]
+
+
+def _run(cmd: list[str], verbose: bool) -> None:
+    if verbose:
+        print(" ".join(map(str, cmd)), flush=True)
+    res = subprocess.run([str(c) for c in cmd], capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"build step failed: {' '.join(map(str, cmd[:3]))} ...")
+    if verbose and (res.stdout.strip() or res.stderr.strip()):
+        print(res.stdout + res.stderr, flush=True)
+
+
+def _write_table_blob() -> Path | None:
+    gen = BUILD / "gen"
+    gen.mkdir(parents=True, exist_ok=True)
+    inc = gen / "table_blob.inc"
+    if not TABLE.exists():
+        if inc.exists():
+            inc.unlink()
+        return None
+    data = TABLE.read_bytes()
+    lines = ["// generated from data/scope_table_v1.pftt by build.py -- do not edit",
+             "static const unsigned char kPftTableBlob[] = {"]
+    for i in range(0, len(data), 20):
+        lines.append("    " + ", ".join(str(b) for b in data[i:i + 20]) + ",")
+    lines.append("};")
+    text = "\n".join(lines) + "\n"
+    if not inc.exists() or inc.read_text() != text:
+        inc.write_text(text)
+    return inc
+
+
+def _deps_hash(src: Path) -> str:
+    h = hashlib.sha256()
+    h.update(src.read_bytes())
+    for d in sorted((CSRC / "host").glob("*.hpp")) + sorted((CSRC / "common").glob("*.h")) + \
+            sorted((CSRC / "device").glob("*.cuh")) + sorted(INCLUDE.rglob("*.h*")):
+        h.update(d.read_bytes())
+    blob = BUILD / "gen" / "table_blob.inc"
+    if src.name == "table_default.cpp" and blob.exists():
+        h.update(blob.read_bytes())
+    return h.hexdigest()[:16]
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    _write_table_blob()
+    objs: list[Path] = []
+    incs = ["-I", INCLUDE, "-I", CSRC, "-I", BUILD / "gen"]
+    for src in sorted((CSRC / "host").glob("*.cpp")):
+        obj = BUILD / f"host_{src.stem}_{_deps_hash(src)}.o"
+        if force or not obj.exists():
+            _run([CXX, *HOST_FLAGS, *incs, "-c", src, "-o", obj], verbose)
+        objs.append(obj)
+    for src in sorted((CSRC / "device").glob("*.cu")):
+        obj = BUILD / f"dev_{src.stem}_{_deps_hash(src)}.o"
+        if force or not obj.exists():
+            _run([NVCC, *NVCC_FLAGS, *incs, "-c", src, "-o", obj], verbose)
+        objs.append(obj)
+    stamp = "".join(sorted(o.name for o in objs))
+    stamp_file = BUILD / "link.stamp"
+    if force or not LIB.exists() or not stamp_file.exists() or stamp_file.read_text() != stamp:
+        tmp = LIB.with_suffix(".so.tmp")
+        _run([NVCC, "-shared", *ARCH, "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp"], verbose)
+        os.replace(tmp, LIB)
+        stamp_file.write_text(stamp)
+    # drop stale objects
+    live = {o.name for o in objs}
+    for o in BUILD.glob("*.o"):
+        if o.name not in live:
+            o.unlink()
+    return LIB
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.verbose))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,161 @@
+// fft_smem.cuh -- batched mixed-radix Stockham FFT on shared memory (complex128).
+//
+// Realises batch_fft_columns for the per-CTA FFT pass of K1: `ncols`
+// columns of length n, column c at x + c*n.  Autosort Stockham formulation: stage s with
+// radix R and span Ns reads x[j + r*n/R] and writes y[(j/Ns)*Ns*R + j%Ns + r*Ns] after
+// the twiddle e^{-2 pi i (j mod Ns) r / (Ns R)}; output is in natural order.  Every
+// twiddle is a lookup in an exactly-reduced table of omega_n^t (host-computed,
+// SPEC.md:261,377), never a recurrence.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pftdev {
+
+struct FftRadices {
+    int n;          // transform length (product of radices)
+    int count;      // number of stages
+    int radix[24];  // stage radices in order
+};
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// multiply by -i
+__device__ __forceinline__ double2 cmul_mi(double2 a) { return make_double2(a.y, -a.x); }
+
+// Twiddle table accessor: omega_n^t for t in [n], stored as tab[t * stride] (the same
+// table serves several lengths that divide the table length).
+struct Twiddles {
+    const double2* tab;
+    uint32_t stride;
+    __device__ __forceinline__ double2 operator()(uint32_t t) const { return __ldg(tab + (size_t)t * stride); }
+};
+
+__device__ __forceinline__ void dft2(double2& a, double2& b) {
+    const double2 t = a;
+    a = cadd(t, b);
+    b = csub(t, b);
+}
+
+__device__ __forceinline__ void dft4(double2& v0, double2& v1, double2& v2, double2& v3) {
+    const double2 a = cadd(v0, v2), b = csub(v0, v2);
+    const double2 c = cadd(v1, v3), d = cmul_mi(csub(v1, v3));
+    v0 = cadd(a, c);
+    v2 = csub(a, c);
+    v1 = cadd(b, d);
+    v3 = csub(b, d);
+}
+
+__device__ __forceinline__ void dft8(double2 (&v)[8]) {
+    double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+    double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+    dft4(e0, e1, e2, e3);
+    dft4(o0, o1, o2, o3);
+    const double s = 0.70710678118654752440;  // sqrt(1/2)
+    const double2 t1 = make_double2((o1.x + o1.y) * s, (o1.y - o1.x) * s);  // o1 * e^{-i pi/4}
+    const double2 t2 = cmul_mi(o2);                                          // o2 * e^{-i pi/2}
+    const double2 t3 = make_double2((o3.y - o3.x) * s, -(o3.x + o3.y) * s);  // o3 * e^{-3 i pi/4}
+    v[0] = cadd(e0, o0);
+    v[4] = csub(e0, o0);
+    v[1] = cadd(e1, t1);
+    v[5] = csub(e1, t1);
+    v[2] = cadd(e2, t2);
+    v[6] = csub(e2, t2);
+    v[3] = cadd(e3, t3);
+    v[7] = csub(e3, t3);
+}
+
+__device__ __forceinline__ void dft3(double2& v0, double2& v1, double2& v2) {
+    const double h = 0.86602540378443864676;  // sqrt(3)/2
+    const double2 t = cadd(v1, v2);
+    const double2 d = csub(v1, v2);
+    const double2 m = make_double2(v0.x - 0.5 * t.x, v0.y - 0.5 * t.y);
+    v0 = cadd(v0, t);
+    // -i h d
+    const double2 r = make_double2(h * d.y, -h * d.x);
+    v1 = cadd(m, r);
+    v2 = csub(m, r);
+}
+
+// One Stockham stage with a radix known at compile time (2, 3, 4, 8).
+template <int R>
+__device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                     int ncols, int n, int Ns, const Twiddles& tw) {
+    const int nb = n / R;
+    const uint32_t tstride = (uint32_t)(n / (Ns * R));
+    for (int idx = threadIdx.x; idx < ncols * nb; idx += blockDim.x) {
+        const int col = idx / nb, j = idx - col * nb;
+        const double2* s = src + (size_t)col * n;
+        double2* d = dst + (size_t)col * n;
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = s[j + r * nb];
+        const int k = j % Ns;
+        if (k != 0) {
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw((uint32_t)(k * r) * tstride));
+        }
+        if constexpr (R == 2) dft2(v[0], v[1]);
+        if constexpr (R == 3) dft3(v[0], v[1], v[2]);
+        if constexpr (R == 4) dft4(v[0], v[1], v[2], v[3]);
+        if constexpr (R == 8) dft8(v);
+        const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) d[base + r * Ns] = v[r];
+    }
+}
+
+// Generic radix (any R): O(R^2) per butterfly, twiddles omega_R^{rs} = omega_n^{rs n/R}.
+__device__ __forceinline__ void stockham_stage_generic(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                       int ncols, int n, int Ns, int R, const Twiddles& tw) {
+    const int nb = n / R;
+    const uint32_t tstride = (uint32_t)(n / (Ns * R));
+    const uint32_t rstride = (uint32_t)(n / R);
+    for (int idx = threadIdx.x; idx < ncols * nb * R; idx += blockDim.x) {
+        const int col = idx / (nb * R);
+        const int rem = idx - col * nb * R;
+        const int j = rem / R, out_r = rem - j * R;
+        const double2* s = src + (size_t)col * n;
+        const int k = j % Ns;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int r = 0; r < R; ++r) {
+            double2 v = s[j + r * nb];
+            if (k != 0 && r != 0) v = cmul(v, tw((uint32_t)(k * r) * tstride));
+            const uint32_t e = (uint32_t)((out_r * r) % R);
+            acc = cadd(acc, e ? cmul(v, tw(e * rstride)) : v);
+        }
+        dst[(size_t)col * n + (j / Ns) * Ns * R + k + out_r * Ns] = acc;
+    }
+}
+
+// Full transform of ncols columns; returns the buffer holding the result (x or y).
+// Caller must __syncthreads() before (inputs written) and after (outputs read).
+__device__ __forceinline__ double2* fft_columns(double2* x, double2* y, int ncols, const FftRadices& plan,
+                                                const Twiddles& tw) {
+    double2* src = x;
+    double2* dst = y;
+    int Ns = 1;
+    const int n = plan.n;
+    for (int st = 0; st < plan.count; ++st) {
+        const int R = plan.radix[st];
+        switch (R) {
+            case 2: stockham_stage_fixed<2>(src, dst, ncols, n, Ns, tw); break;
+            case 3: stockham_stage_fixed<3>(src, dst, ncols, n, Ns, tw); break;
+            case 4: stockham_stage_fixed<4>(src, dst, ncols, n, Ns, tw); break;
+            case 8: stockham_stage_fixed<8>(src, dst, ncols, n, Ns, tw); break;
+            default: stockham_stage_generic(src, dst, ncols, n, Ns, R, tw); break;
+        }
+        __syncthreads();
+        double2* t = src;
+        src = dst;
+        dst = t;
+        Ns *= R;
+    }
+    return src;
+}
+
+}  // namespace pftdev

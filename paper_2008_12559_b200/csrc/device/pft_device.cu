@@ -1,0 +1,441 @@
+// pft_device.cu -- device plans and the extern "C" device entry points of pft_capi.h.
+//
+// A device plan is the immutable upload of a host PftPlan plus the
+// decomposition p = P1 * P2 used by the kernels:
+//   phase[q], tvals[q], w[r], omega[p] (e^{-2 pi i t/p}), post_powers[W][r],
+//   post_twiddles[W], and a default workspace Y[P1][P2][r] for batch 1.
+// There is no host compute path: if the device is missing every call fails.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../host/api_guard.hpp"
+#include "../host/internal.hpp"
+#include "kernels.cuh"
+
+#ifndef PFT_BUILD_DESC
+#define PFT_BUILD_DESC "dev"
+#endif
+
+using namespace pft;
+using namespace pft::detail;
+
+namespace {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // clear sticky-free errors
+        fail(PFT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+int usable_device_count() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// Radix schedule for the per-CTA FFT (largest supported radices first).
+bool factor_radices(uint32_t n, pftdev::FftRadices& out) {
+    out.n = (int)n;
+    out.count = 0;
+    uint32_t m = n;
+    auto push = [&](int r) {
+        if (out.count >= 24) return false;
+        out.radix[out.count++] = r;
+        return true;
+    };
+    while (m % 8 == 0) { if (!push(8)) return false; m /= 8; }
+    while (m % 4 == 0) { if (!push(4)) return false; m /= 4; }
+    while (m % 2 == 0) { if (!push(2)) return false; m /= 2; }
+    while (m % 3 == 0) { if (!push(3)) return false; m /= 3; }
+    for (uint32_t f = 5; m > 1 && f <= 64; f += 2) {
+        while (m % f == 0) { if (!push((int)f)) return false; m /= f; }
+    }
+    return m == 1;
+}
+
+constexpr size_t kK1SmemLimit = 100 * 1024;  // keep >= 2 CTAs per SM
+constexpr uint64_t kTargetCtas = 296;        // 2 x 148 SMs
+
+// Choose P2 | p: the smallest divisor giving >= kTargetCtas CTAs (with the batch) whose
+// co-factor P1 is FFT-friendly (prime factors <= 64) and fits the shared-memory budget.
+uint64_t choose_p2(uint64_t p, int r, size_t batch) {
+    const auto divs = divisors(p);
+    uint64_t fallback = 0;
+    for (uint64_t d : divs) {
+        const uint64_t P1 = p / d;
+        pftdev::FftRadices fr;
+        if (P1 > 1 && !factor_radices((uint32_t)P1, fr)) continue;
+        if (pftdev::k1_smem_bytes(r, (uint32_t)P1) > kK1SmemLimit) continue;
+        if (d * std::max<size_t>(batch, 1) >= kTargetCtas) return d;
+        fallback = d;  // largest valid so far
+    }
+    return fallback ? fallback : p;
+}
+
+}  // namespace
+
+struct pft_dplan_s {
+    int device = 0;
+    HostPlan host;  // parameters (tables are on the device)
+    uint64_t P1 = 0, P2 = 0;
+    pftdev::FftRadices fft{};
+    bool mu0 = false;
+    uint64_t W = 0;
+    // device allocations
+    void* tables = nullptr;
+    double2* d_phase = nullptr;
+    double* d_tvals = nullptr;
+    double2* d_w = nullptr;
+    double2* d_omega = nullptr;
+    double* d_post_powers = nullptr;
+    double2* d_post_twiddles = nullptr;
+    double2* d_ws = nullptr;  // batch-1 workspace
+    int* d_status = nullptr;
+
+    ~pft_dplan_s() {
+        if (tables) {
+            int prev = 0;
+            cudaGetDevice(&prev);
+            cudaSetDevice(device);
+            cudaFree(tables);
+            cudaFree(d_ws);
+            cudaFree(d_status);
+            cudaSetDevice(prev);
+        }
+    }
+
+    size_t slab_elems() const { return (size_t)host.p * host.r; }
+
+    pftdev::K1Params k1_params(const double2* a, size_t batch_stride, uint64_t row_stride, uint64_t lq,
+                               uint64_t l0, double2* Y) const {
+        pftdev::K1Params P{};
+        P.a = a;
+        P.batch_stride = batch_stride;
+        P.row_stride = row_stride;
+        P.lq = lq;
+        P.l0 = l0;
+        P.phase = d_phase;
+        P.tvals = d_tvals;
+        P.w = d_w;
+        P.omega = d_omega;
+        P.P1 = (uint32_t)P1;
+        P.P2 = (uint32_t)P2;
+        P.fft = fft;
+        P.Y = Y;
+        return P;
+    }
+
+    pftdev::K2Params k2_params(const double2* Y, double2* out) const {
+        pftdev::K2Params P{};
+        P.Y = Y;
+        P.post_powers = d_post_powers;
+        P.post_twiddles = d_post_twiddles;
+        P.omega = d_omega;
+        P.p = host.p;
+        P.P1 = (uint32_t)P1;
+        P.P2 = (uint32_t)P2;
+        P.W = W;
+        const int64_t first = host.mu - (int64_t)host.M;
+        P.first_mod_p = mod_index(first, host.p);
+        P.first_mod_p1 = (uint32_t)mod_index(first, P1);
+        P.out = out;
+        P.status = d_status;
+        return P;
+    }
+};
+
+namespace {
+
+pft_dplan_s* dp(pft_dplan_t d) {
+    PFT_REQUIRE(d != nullptr, "null device plan");
+    return d;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stride, double2* out, double2* Y,
+                 cudaStream_t st) {
+    const auto P1 = d->k1_params(in, in_stride, d->host.q, d->host.q, 0, Y);
+    cuda_check(pftdev::launch_k1(P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
+    const auto P2 = d->k2_params(Y, out);
+    cuda_check(pftdev::launch_k2(P2, d->host.r, (uint32_t)batch, st), "K2 launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pft_version(void) { return "pft-b200 " PFT_BUILD_DESC " sm_100a"; }
+
+pft_status pft_device_count(int* n) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(n != nullptr, "n is null");
+    *n = usable_device_count();
+    PFT_API_END
+}
+
+pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dplan_t* out) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(plan && out, "dplan_create: bad arguments");
+    *out = nullptr;
+    const HostPlan& H = plan->plan;
+    const int device = opts ? opts->device : 0;
+    const int ndev = usable_device_count();
+    if (ndev == 0) fail(PFT_ERR_NO_DEVICE, "no CUDA device visible (this library has no CPU fallback)");
+    PFT_REQUIRE(device >= 0 && device < ndev, "dplan_create: device ordinal out of range");
+    cudaDeviceProp prop{};
+    cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10 || prop.minor != 0)
+        fail(PFT_ERR_NO_DEVICE, "device " + std::to_string(device) + " is sm_" + std::to_string(prop.major) +
+                                    std::to_string(prop.minor) + "; this build targets sm_100a only");
+    if (H.p >= (1ull << 32)) fail(PFT_ERR_UNSUPPORTED, "p >= 2^32");
+    DeviceGuard guard(device);
+
+    auto d = std::make_unique<pft_dplan_s>();
+    d->device = device;
+    d->host.N = H.N;
+    d->host.M = H.M;
+    d->host.mu = H.mu;
+    d->host.p = H.p;
+    d->host.q = H.q;
+    d->host.r = H.r;
+    d->host.epsilon = H.epsilon;
+    d->host.achieved_epsilon = H.achieved_epsilon;
+    d->host.plan_id = H.plan_id;
+    d->W = 2 * H.M + 1;
+    const uint64_t p2 = (opts && opts->p2) ? opts->p2 : choose_p2(H.p, H.r, 1);
+    if (p2 == 0 || H.p % p2 != 0) fail(PFT_ERR_INVALID_ARGUMENT, "dplan_create: p2 must divide p");
+    d->P2 = p2;
+    d->P1 = H.p / p2;
+    if (d->P1 > 1 && !factor_radices((uint32_t)d->P1, d->fft))
+        fail(PFT_ERR_UNSUPPORTED, "dplan_create: P1 = p/P2 has a prime factor > 64");
+    if (d->P1 <= 1) d->fft.n = 1;
+    if (pftdev::k1_smem_bytes(H.r, (uint32_t)d->P1) > 200 * 1024)
+        fail(PFT_ERR_UNSUPPORTED, "dplan_create: P1 * r too large for shared memory; choose a larger p2");
+    d->mu0 = std::all_of(H.phase.begin(), H.phase.end(), [](const cplx& z) { return z == cplx(1.0, 0.0); });
+
+    // omega_p^t = e^{-2 pi i t / p}, exactly reduced
+    std::vector<cplx> omega(H.p);
+#pragma omp parallel for schedule(static)
+    for (long long t = 0; t < (long long)H.p; ++t) omega[t] = cispi_frac(-2 * (__int128)t, H.p);
+
+    // one allocation for all tables, 256-byte aligned pieces
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t b_phase = al(H.q * sizeof(double2)), b_tv = al(H.q * sizeof(double)),
+                 b_w = al(H.r * sizeof(double2)), b_om = al(H.p * sizeof(double2)),
+                 b_pp = al(d->W * H.r * sizeof(double)), b_pt = al(d->W * sizeof(double2));
+    const size_t total = b_phase + b_tv + b_w + b_om + b_pp + b_pt;
+    cuda_check(cudaMalloc(&d->tables, total), "cudaMalloc(tables)");
+    char* base = static_cast<char*>(d->tables);
+    d->d_phase = reinterpret_cast<double2*>(base);
+    d->d_tvals = reinterpret_cast<double*>(base + b_phase);
+    d->d_w = reinterpret_cast<double2*>(base + b_phase + b_tv);
+    d->d_omega = reinterpret_cast<double2*>(base + b_phase + b_tv + b_w);
+    d->d_post_powers = reinterpret_cast<double*>(base + b_phase + b_tv + b_w + b_om);
+    d->d_post_twiddles = reinterpret_cast<double2*>(base + b_phase + b_tv + b_w + b_om + b_pp);
+    cuda_check(cudaMemcpy(d->d_phase, H.phase.data(), H.q * sizeof(double2), cudaMemcpyHostToDevice), "upload phase");
+    cuda_check(cudaMemcpy(d->d_tvals, H.tvals.data(), H.q * sizeof(double), cudaMemcpyHostToDevice), "upload tvals");
+    cuda_check(cudaMemcpy(d->d_w, H.w.data(), H.r * sizeof(double2), cudaMemcpyHostToDevice), "upload w");
+    cuda_check(cudaMemcpy(d->d_omega, omega.data(), H.p * sizeof(double2), cudaMemcpyHostToDevice), "upload omega");
+    cuda_check(cudaMemcpy(d->d_post_powers, H.post_powers.data(), d->W * H.r * sizeof(double), cudaMemcpyHostToDevice),
+               "upload post_powers");
+    cuda_check(cudaMemcpy(d->d_post_twiddles, H.post_twiddles.data(), d->W * sizeof(double2), cudaMemcpyHostToDevice),
+               "upload post_twiddles");
+    cuda_check(cudaMalloc(&d->d_ws, d->slab_elems() * sizeof(double2)), "cudaMalloc(workspace)");
+    cuda_check(cudaMalloc(&d->d_status, sizeof(int)), "cudaMalloc(status)");
+    cuda_check(cudaMemset(d->d_status, 0, sizeof(int)), "cudaMemset(status)");
+    cuda_check(pftdev::configure_k1(H.r, (uint32_t)d->P1, d->mu0), "configure K1");
+    *out = d.release();
+    PFT_API_END
+}
+
+void pft_dplan_destroy(pft_dplan_t d) { delete d; }
+
+pft_status pft_dplan_layout(pft_dplan_t d, uint64_t* p1, uint64_t* p2) {
+    PFT_API_BEGIN
+    if (p1) *p1 = dp(d)->P1;
+    if (p2) *p2 = dp(d)->P2;
+    PFT_API_END
+}
+
+pft_status pft_workspace_bytes(pft_dplan_t d, size_t batch, size_t* bytes) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(bytes != nullptr, "bytes is null");
+    *bytes = dp(d)->slab_elems() * sizeof(double2) * batch;
+    PFT_API_END
+}
+
+pft_status pft_partial_bytes(pft_dplan_t d, size_t batch, size_t* bytes) {
+    return pft_workspace_bytes(d, batch, bytes);
+}
+
+pft_status pft_launches_per_execute(pft_dplan_t d, int* launches) {
+    PFT_API_BEGIN
+    dp(d);
+    PFT_REQUIRE(launches != nullptr, "launches is null");
+    *launches = 2;
+    PFT_API_END
+}
+
+pft_status pft_execute(pft_dplan_t dh, const pft_c128* d_in, size_t batch, size_t in_stride, pft_c128* d_out,
+                       void* d_ws, void* stream) {
+    PFT_API_BEGIN
+    pft_dplan_s* d = dp(dh);
+    if (batch == 0) return PFT_OK;
+    PFT_REQUIRE(d_in && d_out, "execute: null buffer");
+    PFT_REQUIRE(batch <= 65535, "execute: batch > 65535 per call");
+    if (in_stride == 0) in_stride = d->host.N;
+    PFT_REQUIRE(in_stride >= d->host.N || batch == 1, "execute: in_stride < N");
+    double2* Y = static_cast<double2*>(d_ws);
+    if (!Y) {
+        PFT_REQUIRE(batch == 1, "execute: batch > 1 needs a caller workspace (pft_workspace_bytes)");
+        Y = d->d_ws;
+    }
+    DeviceGuard guard(d->device);
+    run_execute(d, reinterpret_cast<const double2*>(d_in), batch, in_stride, reinterpret_cast<double2*>(d_out), Y,
+                static_cast<cudaStream_t>(stream));
+    PFT_API_END
+}
+
+pft_status pft_execute_partial(pft_dplan_t dh, const pft_c128* d_in_local, uint64_t l0, uint64_t lq,
+                               uint64_t row_stride, pft_c128* d_partial, void* stream) {
+    PFT_API_BEGIN
+    pft_dplan_s* d = dp(dh);
+    PFT_REQUIRE(d_in_local && d_partial, "execute_partial: null buffer");
+    PFT_REQUIRE(l0 + lq <= d->host.q, "execute_partial: column slice outside [0, q)");
+    PFT_REQUIRE(row_stride >= lq, "execute_partial: row_stride < lq");
+    DeviceGuard guard(d->device);
+    const auto P = d->k1_params(reinterpret_cast<const double2*>(d_in_local), 0, row_stride, lq, l0,
+                                reinterpret_cast<double2*>(d_partial));
+    cuda_check(pftdev::launch_k1(P, d->host.r, 1, d->mu0, static_cast<cudaStream_t>(stream)), "K1 launch");
+    PFT_API_END
+}
+
+pft_status pft_finalize(pft_dplan_t dh, const pft_c128* d_partial, size_t batch, pft_c128* d_out, void* stream) {
+    PFT_API_BEGIN
+    pft_dplan_s* d = dp(dh);
+    if (batch == 0) return PFT_OK;
+    PFT_REQUIRE(d_partial && d_out, "finalize: null buffer");
+    DeviceGuard guard(d->device);
+    const auto P = d->k2_params(reinterpret_cast<const double2*>(d_partial), reinterpret_cast<double2*>(d_out));
+    cuda_check(pftdev::launch_k2(P, d->host.r, (uint32_t)batch, static_cast<cudaStream_t>(stream)), "K2 launch");
+    PFT_API_END
+}
+
+pft_status pft_status_query(pft_dplan_t dh, void* stream, int* flags, int reset) {
+    PFT_API_BEGIN
+    pft_dplan_s* d = dp(dh);
+    PFT_REQUIRE(flags != nullptr, "flags is null");
+    DeviceGuard guard(d->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cuda_check(cudaStreamSynchronize(st), "stream synchronize");
+    cuda_check(cudaMemcpy(flags, d->d_status, sizeof(int), cudaMemcpyDeviceToHost), "read status");
+    if (reset) cuda_check(cudaMemset(d->d_status, 0, sizeof(int)), "reset status");
+    PFT_API_END
+}
+
+pft_status pft_execute_host(pft_dplan_t dh, const pft_c128* h_in, size_t batch, pft_c128* h_out, pft_c128* d_in,
+                            pft_c128* d_out, void* stream) {
+    PFT_API_BEGIN
+    pft_dplan_s* d = dp(dh);
+    if (batch == 0) return PFT_OK;
+    PFT_REQUIRE(h_in && h_out, "execute_host: null host buffer");
+    DeviceGuard guard(d->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t n_in = d->host.N * batch, n_out = d->W * batch;
+    pft_c128* din = d_in;
+    pft_c128* dout = d_out;
+    double2* ws = nullptr;
+    bool own_in = false, own_out = false;
+    struct Cleanup {
+        pft_c128*& a; pft_c128*& b; double2*& w; bool& oa; bool& ob;
+        ~Cleanup() {
+            if (oa) cudaFree(a);
+            if (ob) cudaFree(b);
+            if (w) cudaFree(w);
+        }
+    } cleanup{din, dout, ws, own_in, own_out};
+    if (!din) {
+        cuda_check(cudaMalloc(&din, n_in * sizeof(pft_c128)), "cudaMalloc(input)");
+        own_in = true;
+    }
+    if (!dout) {
+        cuda_check(cudaMalloc(&dout, n_out * sizeof(pft_c128)), "cudaMalloc(output)");
+        own_out = true;
+    }
+    double2* Y = d->d_ws;
+    if (batch > 1) {
+        cuda_check(cudaMalloc(&ws, d->slab_elems() * sizeof(double2) * batch), "cudaMalloc(workspace)");
+        Y = ws;
+    }
+    cuda_check(cudaMemcpyAsync(din, h_in, n_in * sizeof(pft_c128), cudaMemcpyHostToDevice, st), "H2D input");
+    run_execute(d, reinterpret_cast<const double2*>(din), batch, d->host.N, reinterpret_cast<double2*>(dout), Y, st);
+    cuda_check(cudaMemcpyAsync(h_out, dout, n_out * sizeof(pft_c128), cudaMemcpyDeviceToHost, st), "D2H output");
+    cuda_check(cudaStreamSynchronize(st), "stream synchronize");
+    int flags = 0;
+    cuda_check(cudaMemcpy(&flags, d->d_status, sizeof(int), cudaMemcpyDeviceToHost), "read status");
+    if (flags) {
+        cuda_check(cudaMemset(d->d_status, 0, sizeof(int)), "reset status");
+        fail(PFT_ERR_NON_FINITE, "execute: non-finite input entries (non-finite output detected)");
+    }
+    PFT_API_END
+}
+
+pft_status pft_generate_device(const pft_signal_desc* desc, pft_c128* d_out, uint64_t count, void* stream) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(desc && (d_out || count == 0), "generate_device: bad arguments");
+    PFT_REQUIRE(desc->kind >= 0 && desc->kind <= 2, "generate_device: unknown kind");
+    PFT_REQUIRE(desc->kind != 2 || desc->N >= 1, "generate_device: sparse kind needs N");
+    if (usable_device_count() == 0) fail(PFT_ERR_NO_DEVICE, "no CUDA device visible");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    pftdev::GenParams G{};
+    G.kind = desc->kind;
+    G.seed = desc->seed;
+    G.N = desc->N ? desc->N : 1;
+    G.index_offset = desc->index_offset;
+    G.count = count;
+    G.sigma = desc->sigma;
+    G.out = reinterpret_cast<double2*>(d_out);
+    void* tones = nullptr;
+    if (desc->kind == 2 && desc->n_tones > 0) {
+        PFT_REQUIRE(desc->freqs && desc->amps, "generate_device: tones missing");
+        const size_t nt = desc->n_tones;
+        cuda_check(cudaMalloc(&tones, nt * (sizeof(int64_t) + sizeof(double2))), "cudaMalloc(tones)");
+        cuda_check(cudaMemcpy(tones, desc->freqs, nt * sizeof(int64_t), cudaMemcpyHostToDevice), "upload freqs");
+        cuda_check(cudaMemcpy(static_cast<char*>(tones) + nt * sizeof(int64_t), desc->amps, nt * sizeof(double2),
+                              cudaMemcpyHostToDevice),
+                   "upload amps");
+        G.n_tones = desc->n_tones;
+        G.freqs = static_cast<const int64_t*>(tones);
+        G.amps = reinterpret_cast<const double2*>(static_cast<char*>(tones) + nt * sizeof(int64_t));
+    }
+    cudaError_t e = pftdev::launch_k0(G, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (tones) cudaFree(tones);
+    cuda_check(e, "K0 generate");
+    PFT_API_END
+}
+
+}  // extern "C"
