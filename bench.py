@@ -1,0 +1,348 @@
+#!/usr/bin/env python3
+"""Benchmark of the PFT execute hot path (BASELINE.json metric: PFT transforms/sec and input
+GB/s, fraction of the HBM roofline) on 1..N B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2b] [--impl ours|reference]
+
+A "step" is one transform (one pass of transform.execute) over one
+synthetic input already resident in HBM.  Default workload = BASELINE.json configs[1] at
+M = 2^10 (the north-star "C2b": N = 2^24, mu = N/4, eps = 1e-12, 32 seeded tones + CN
+noise).  Multi-GPU: one process per GPU (torchrun), each rank runs an independent replica
+stream of transforms ("replicas only" for single transforms, weak scaling); the step time
+is the max over ranks of the device time.  Prints ONE JSON line on rank 0.
+
+--impl reference times the reference algorithm's CPU restatement (oracle/, the
+reference ships no runnable implementation -- SURVEY.md §8(c)) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (N, M, mu, p, kind, description)
+    "c1": (2 ** 20, 64, 0, 2 ** 14, "uniform", "BASELINE configs[0]: N=2^20, M=64, mu=0, U[-1,1] re/im"),
+    "c2a": (2 ** 24, 2 ** 6, 2 ** 22, 2 ** 16, "sparse", "BASELINE configs[1]: N=2^24, M=2^6, mu=N/4, 32 tones + CN noise"),
+    "c2b": (2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, "sparse", "BASELINE configs[1]: N=2^24, M=2^10, mu=N/4, 32 tones + CN noise"),
+    "c2c": (2 ** 24, 2 ** 14, 2 ** 22, 2 ** 16, "sparse", "BASELINE configs[1]: N=2^24, M=2^14, mu=N/4, 32 tones + CN noise"),
+    "c4": (6220800, 1000, -12345, 62208, "normal", "BASELINE configs[3]: N=2^10 3^5 5^2, M=1000, mu=-12345, CN(0,1)"),
+}
+SEEDS = {"c1": 1, "c2a": 2, "c2b": 2, "c2c": 2, "c4": 4}
+EPS = 1e-12
+L2_BYTES = 126 * 1024 * 1024
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_hbm_peak():
+    f = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(f.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def committed_traffic(config):
+    f = ROOT / "profiles" / "k1_dram_traffic.json"
+    try:
+        return json.loads(f.read_text()).get(config)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi style clocks/throttle sampling (NVML) during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            log("NVML unavailable:", e)
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        s = sorted(self.samples)
+        reasons = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(s)}
+
+
+def make_input_host(pft, cfg, N, mu, M, seed, kind):
+    if kind == "sparse":
+        freqs, amps = pft.sparse_tones(seed, 32, mu - M, mu + M)
+        return pft.generate_signal(pft.KIND_SPARSE, seed, N, N=N, freqs=freqs, amps=amps, sigma=1e-3)
+    return pft.generate_signal(pft.KIND_NORMAL if kind == "normal" else pft.KIND_UNIFORM, seed, N)
+
+
+def make_input_device(pft, buf, N, mu, M, seed, kind, offset=0):
+    if kind == "sparse":
+        freqs, amps = pft.sparse_tones(seed, 32, mu - M, mu + M)
+        pft.generate_signal_device(buf.data_ptr(), pft.KIND_SPARSE, seed, N, N=N, offset=offset, freqs=freqs,
+                                   amps=amps, sigma=1e-3)
+    else:
+        pft.generate_signal_device(buf.data_ptr(), pft.KIND_NORMAL if kind == "normal" else pft.KIND_UNIFORM, seed,
+                                   N, offset=offset)
+
+
+def cpu_oracle_rate(pft_mod, plan, a, budget_s: float):
+    """Transforms/s of the CPU oracle (all host threads) on the same plan and input."""
+    import oracle
+    oracle.execute(plan, a)  # warm (twiddle tables, page faults)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        oracle.execute(plan, a)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            return n / el, n, el
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (CPU restatement) on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    import oracle
+    import paper_2008_12559_b200 as pft
+    N, M, mu, p, kind, desc = CONFIGS[args.config]
+    plan = pft.build_plan(N, M, mu, p, EPS)
+    a = make_input_host(pft, args.config, N, mu, M, SEEDS[args.config], kind)
+    cores = os.cpu_count()
+    for _ in range(max(args.warmup, 0)):
+        oracle.execute(plan, a)
+    # each step is one full transform; cap the run at ~150 s of CPU time
+    t0 = time.perf_counter()
+    oracle.execute(plan, a)
+    per = time.perf_counter() - t0
+    steps = max(1, min(args.steps, int(150.0 / max(per, 1e-6))))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle.execute(plan, a)
+    el = time.perf_counter() - t0
+    value = steps / el
+    line = {
+        "impl": "reference", "metric": "PFT transforms/sec", "value": value, "unit": "transforms/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": el / steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)",
+        "data": "synthetic",
+        "config": {"workload": desc, "p": plan.p, "q": plan.q, "r": plan.r, "epsilon": EPS},
+        "input_gbs": value * 16 * N / 1e9,
+        "cpu_baseline": {"value": value, "unit": "transforms/s", "cores": cores, "kind": "port",
+                         "sample": f"{steps} full transforms (oracle/oracle.cpp, OpenMP {cores} threads)"},
+        "e2e": {"value": value, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2008_12559_b200 as pft
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    N, M, mu, p, kind, desc = CONFIGS[args.config]
+    W = 2 * M + 1
+    plan = pft.build_plan(N, M, mu, p, EPS)
+    d = pft.DevicePlan(plan, device=local, p2=args.p2)
+    launches = d.launches_per_execute()
+
+    # inputs: >= 2 buffers, together > 2x L2, rotated so no step re-reads a cached input
+    nbuf = max(2, -(-2 * L2_BYTES // (16 * N)))
+    bufs = [torch.empty(N, dtype=torch.complex128, device=dev) for _ in range(nbuf)]
+    for i, b in enumerate(bufs):
+        make_input_device(pft, b, N, mu, M, SEEDS[args.config] + 100 * rank, kind, offset=i * N)
+    out = torch.empty(W, dtype=torch.complex128, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    sp = stream.cuda_stream
+
+    def step(i):
+        d.execute_ptr(bufs[i % nbuf].data_ptr(), out.data_ptr(), stream=sp)
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+        # capture exactly K steps into one graph (launch overhead off the timed path)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            for i in range(args.steps):
+                step(i)
+        graph.replay()  # warm replay
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * args.steps / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (K1): K1 alone, same stream, same inputs
+    Yb = torch.empty(plan.p * plan.r, dtype=torch.complex128, device=dev)
+    with torch.cuda.stream(stream):
+        for i in range(3):
+            d.execute_partial_ptr(bufs[i % nbuf].data_ptr(), 0, plan.q, plan.q, Yb.data_ptr(), stream=sp)
+        g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1, stream=stream):
+            for i in range(args.steps):
+                d.execute_partial_ptr(bufs[i % nbuf].data_ptr(), 0, plan.q, plan.q, Yb.data_ptr(), stream=sp)
+        g1.replay()
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    g1.replay()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    k1_ms = e0.elapsed_time(e1) / args.steps
+    peak, peak_src = measured_hbm_peak()
+    k1_gbs = 16 * N / (k1_ms * 1e-3) / 1e9
+
+    # parity spot-check of this run's output against the oracle is in tests/; here only
+    # the non-finite status word is checked
+    status = d.status(stream=sp)
+
+    line = None
+    if rank == 0:
+        # ---- e2e through the public host API (H2D of the input + D2H of the spectrum)
+        e2e = None
+        if not args.no_e2e:
+            h_in = torch.empty(N, dtype=torch.complex128, pin_memory=True)
+            h_in.copy_(bufs[0].cpu())
+            h_out = torch.empty(W, dtype=torch.complex128, pin_memory=True)
+            import ctypes as C
+            L = pft.lib()
+            def e2e_call():
+                st = L.pft_execute_host(d.handle, C.c_void_p(h_in.data_ptr()), 1, C.c_void_p(h_out.data_ptr()),
+                                        C.c_void_p(bufs[1].data_ptr()), C.c_void_p(out.data_ptr()), C.c_void_p(sp))
+                if st != 0:
+                    raise RuntimeError(f"pft_execute_host failed: {st}")
+            for _ in range(2):
+                e2e_call()
+            n_e2e = max(3, min(args.steps, 20))
+            t0 = time.perf_counter()
+            for _ in range(n_e2e):
+                e2e_call()
+            el = time.perf_counter() - t0
+            e2e = {"value": n_e2e / el, "unit": "transforms/s", "h2d_bytes_per_step": 16 * N,
+                   "d2h_bytes_per_step": 16 * W, "steps": n_e2e, "timer": "host wall clock around synchronous "
+                   "pft_execute_host (pinned host buffers)"}
+        # ---- CPU baseline: the oracle on this host, bounded sample
+        cpu = None
+        if not args.no_cpu and world == 1:
+            try:
+                a_host = bufs[0].cpu().numpy()
+                rate, n, el = cpu_oracle_rate(pft, plan, a_host, args.cpu_seconds)
+                cpu = {"value": rate, "unit": "transforms/s", "cores": os.cpu_count(), "kind": "port",
+                       "sample": f"{n} full {args.config} transforms in {el:.1f} s (oracle/oracle.cpp, "
+                                 f"OpenMP {os.cpu_count()} threads)"}
+            except Exception as e:  # the baseline is reported, never required
+                cpu = {"value": None, "error": str(e)}
+        line = {
+            "metric": "PFT transforms/sec", "value": value, "unit": "transforms/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {desc}", "N": N, "M": M, "mu": mu, "epsilon": EPS,
+                       "p": plan.p, "q": plan.q, "r": plan.r, "P1": d.P1, "P2": d.P2,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": f"{nbuf} rotating inputs of {16 * N / 2**20:.0f} MiB (> L2 126 MiB)",
+                       "timing": "CUDA graph of K steps, CUDA events on the launch stream"},
+            "input_gbs": value * 16 * N / 1e9,
+            "input_gbs_frac_of_peak": value * 16 * N / 1e9 / world / peak,
+            "roofline": {"bound": "hbm", "kernel": "k1_contract_fft", "achieved": k1_gbs, "peak": peak,
+                         "unit": "GB/s", "frac": k1_gbs / peak, "peak_source": peak_src,
+                         "traffic": committed_traffic(args.config),
+                         "algorithmic_bytes_per_launch": 16 * N, "k1_ms": k1_ms,
+                         "k1_share_of_step": k1_ms / ms_step},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+            "status_flags": status,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c2b", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--p2", type=int, default=0, help="override K1 residue classes (0 = planner)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -191,7 +191,10 @@ class ScopeTable:
 
     def __del__(self):
         if getattr(self, "_owned", False) and self._h:
-            lib().pft_table_destroy(self._h)
+            try:
+                lib().pft_table_destroy(self._h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     @property
@@ -326,7 +329,10 @@ class PftPlan:
         for d in getattr(self, "_dplans", {}).values():
             d.close()
         if getattr(self, "_h", None):
-            lib().pft_plan_destroy(self._h)
+            try:
+                lib().pft_plan_destroy(self._h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     @property
@@ -419,7 +425,10 @@ class DevicePlan:
 
     def close(self) -> None:
         if getattr(self, "_h", None):
-            lib().pft_dplan_destroy(self._h)
+            try:
+                lib().pft_dplan_destroy(self._h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     def __del__(self):

@@ -5,6 +5,8 @@
 //   phase[q], tvals[q], w[r], omega[p] (e^{-2 pi i t/p}), post_powers[W][r],
 //   post_twiddles[W], and a default workspace Y[P1][P2][r] for batch 1.
 // There is no host compute path: if the device is missing every call fails.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -64,23 +66,38 @@ bool factor_radices(uint32_t n, pftdev::FftRadices& out) {
     return m == 1;
 }
 
-constexpr size_t kK1SmemLimit = 100 * 1024;  // keep >= 2 CTAs per SM
-constexpr uint64_t kTargetCtas = 296;        // 2 x 148 SMs
+constexpr uint64_t kTargetCtas = 256;        // >= 1.7 CTAs per SM on 148 SMs
+constexpr size_t kK2SmemLimit = 220 * 1024;
 
-// Choose P2 | p: the smallest divisor giving >= kTargetCtas CTAs (with the batch) whose
-// co-factor P1 is FFT-friendly (prime factors <= 64) and fits the shared-memory budget.
+bool k1_feasible(uint64_t P1, int r) {
+    pftdev::FftRadices fr;
+    if (P1 > 1 && !factor_radices((uint32_t)P1, fr)) return false;
+    return sizeof(double2) * (size_t)r * P1 <= pftdev::K1_RING_BYTES;  // FFT scratch = the ring
+}
+
+bool k2_fft_feasible(uint64_t P2, int r) {
+    pftdev::FftRadices fr;
+    if (P2 > 1 && !factor_radices((uint32_t)P2, fr)) return false;
+    return pftdev::k2_smem_bytes(r, (uint32_t)P2) <= kK2SmemLimit;
+}
+
+// Choose P2 | p (K1 grid = P2 x batch CTAs; P1 = p / P2 is K1's in-CTA FFT length, P2 is
+// K2's).  Prefer decompositions where both FFT passes fit shared memory, then the
+// smallest P2 that still gives >= kTargetCtas CTAs (fewer residue classes = less K2 work).
 uint64_t choose_p2(uint64_t p, int r, size_t batch) {
     const auto divs = divisors(p);
-    uint64_t fallback = 0;
-    for (uint64_t d : divs) {
-        const uint64_t P1 = p / d;
-        pftdev::FftRadices fr;
-        if (P1 > 1 && !factor_radices((uint32_t)P1, fr)) continue;
-        if (pftdev::k1_smem_bytes(r, (uint32_t)P1) > kK1SmemLimit) continue;
-        if (d * std::max<size_t>(batch, 1) >= kTargetCtas) return d;
-        fallback = d;  // largest valid so far
+    const size_t nb = std::max<size_t>(batch, 1);
+    for (int pass = 0; pass < 2; ++pass) {
+        uint64_t best = 0;
+        for (uint64_t d : divs) {
+            if (!k1_feasible(p / d, r)) continue;
+            if (pass == 0 && !k2_fft_feasible(d, r)) continue;
+            best = d;
+            if (d * nb >= kTargetCtas) return d;
+        }
+        if (best) return best;
     }
-    return fallback ? fallback : p;
+    return p;
 }
 
 }  // namespace
@@ -89,7 +106,9 @@ struct pft_dplan_s {
     int device = 0;
     HostPlan host;  // parameters (tables are on the device)
     uint64_t P1 = 0, P2 = 0;
-    pftdev::FftRadices fft{};
+    pftdev::FftRadices fft{};   // radices of P1 (K1)
+    pftdev::FftRadices fft2{};  // radices of P2 (K2)
+    bool k2_fft = false;
     bool mu0 = false;
     uint64_t W = 0;
     // device allocations
@@ -117,12 +136,8 @@ struct pft_dplan_s {
 
     size_t slab_elems() const { return (size_t)host.p * host.r; }
 
-    pftdev::K1Params k1_params(const double2* a, size_t batch_stride, uint64_t row_stride, uint64_t lq,
-                               uint64_t l0, double2* Y) const {
+    pftdev::K1Params k1_params(uint64_t lq, uint64_t l0, double2* Y) const {
         pftdev::K1Params P{};
-        P.a = a;
-        P.batch_stride = batch_stride;
-        P.row_stride = row_stride;
         P.lq = lq;
         P.l0 = l0;
         P.phase = d_phase;
@@ -149,6 +164,8 @@ struct pft_dplan_s {
         const int64_t first = host.mu - (int64_t)host.M;
         P.first_mod_p = mod_index(first, host.p);
         P.first_mod_p1 = (uint32_t)mod_index(first, P1);
+        P.use_fft = k2_fft ? 1 : 0;
+        P.fft2 = fft2;
         P.out = out;
         P.status = d_status;
         return P;
@@ -175,10 +192,44 @@ struct DeviceGuard {
     }
 };
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    if (!fn) fail(PFT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    return fn;
+}
+
+// 4-D view of the input for K1's bulk tensor copies: (2*lq doubles of a row, residue c,
+// k1, signal) with row k = c + P2 k1 at base + k * row_stride elements.
+CUtensorMap make_input_map(const pft_dplan_s* d, const void* base, uint64_t lq, uint64_t row_stride,
+                           size_t batch, size_t batch_stride) {
+    PFT_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, "input must be 16-byte aligned");
+    CUtensorMap map;
+    const cuuint64_t dims[4] = {2 * lq, d->P2, d->P1, std::max<size_t>(batch, 1)};
+    const cuuint64_t row_bytes = row_stride * 16;
+    const cuuint64_t strides[3] = {row_bytes, row_bytes * d->P2,
+                                   (batch > 1 ? batch_stride : d->P1 * d->P2 * row_stride) * 16};
+    const cuuint32_t box[4] = {2 * pftdev::K1_CH, 1, pftdev::K1_BOX_ROWS, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims,
+                                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(PFT_ERR_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+    return map;
+}
+
 void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stride, double2* out, double2* Y,
                  cudaStream_t st) {
-    const auto P1 = d->k1_params(in, in_stride, d->host.q, d->host.q, 0, Y);
-    cuda_check(pftdev::launch_k1(P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
+    const CUtensorMap map = make_input_map(d, in, d->host.q, d->host.q, batch, in_stride);
+    const auto P1 = d->k1_params(d->host.q, 0, Y);
+    cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
     const auto P2 = d->k2_params(Y, out);
     cuda_check(pftdev::launch_k2(P2, d->host.r, (uint32_t)batch, st), "K2 launch");
 }
@@ -232,8 +283,13 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     if (d->P1 > 1 && !factor_radices((uint32_t)d->P1, d->fft))
         fail(PFT_ERR_UNSUPPORTED, "dplan_create: P1 = p/P2 has a prime factor > 64");
     if (d->P1 <= 1) d->fft.n = 1;
-    if (pftdev::k1_smem_bytes(H.r, (uint32_t)d->P1) > 200 * 1024)
-        fail(PFT_ERR_UNSUPPORTED, "dplan_create: P1 * r too large for shared memory; choose a larger p2");
+    if (!k1_feasible(d->P1, H.r))
+        fail(PFT_ERR_UNSUPPORTED, "dplan_create: P1 * r too large for K1 shared memory; choose a larger p2");
+    d->k2_fft = k2_fft_feasible(d->P2, H.r);
+    if (d->k2_fft) {
+        if (d->P2 > 1) factor_radices((uint32_t)d->P2, d->fft2);
+        else d->fft2.n = 1;
+    }
     d->mu0 = std::all_of(H.phase.begin(), H.phase.end(), [](const cplx& z) { return z == cplx(1.0, 0.0); });
 
     // omega_p^t = e^{-2 pi i t / p}, exactly reduced
@@ -267,6 +323,7 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     cuda_check(cudaMalloc(&d->d_status, sizeof(int)), "cudaMalloc(status)");
     cuda_check(cudaMemset(d->d_status, 0, sizeof(int)), "cudaMemset(status)");
     cuda_check(pftdev::configure_k1(H.r, (uint32_t)d->P1, d->mu0), "configure K1");
+    if (d->k2_fft) cuda_check(pftdev::configure_k2(H.r, (uint32_t)d->P2), "configure K2");
     *out = d.release();
     PFT_API_END
 }
@@ -327,9 +384,10 @@ pft_status pft_execute_partial(pft_dplan_t dh, const pft_c128* d_in_local, uint6
     PFT_REQUIRE(l0 + lq <= d->host.q, "execute_partial: column slice outside [0, q)");
     PFT_REQUIRE(row_stride >= lq, "execute_partial: row_stride < lq");
     DeviceGuard guard(d->device);
-    const auto P = d->k1_params(reinterpret_cast<const double2*>(d_in_local), 0, row_stride, lq, l0,
-                                reinterpret_cast<double2*>(d_partial));
-    cuda_check(pftdev::launch_k1(P, d->host.r, 1, d->mu0, static_cast<cudaStream_t>(stream)), "K1 launch");
+    PFT_REQUIRE(lq >= 1, "execute_partial: empty column slice");
+    const CUtensorMap map = make_input_map(d, d_in_local, lq, row_stride, 1, 0);
+    const auto P = d->k1_params(lq, l0, reinterpret_cast<double2*>(d_partial));
+    cuda_check(pftdev::launch_k1(map, P, d->host.r, 1, d->mu0, static_cast<cudaStream_t>(stream)), "K1 launch");
     PFT_API_END
 }
 
