@@ -223,10 +223,10 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk, torch.cuda.stream(stream):
         torch.cuda.synchronize(dev)
         e0.record(stream)
-        graph.replay()
+        graph.replay()  # replays on the current stream == `stream`
         e1.record(stream)
         torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
@@ -241,16 +241,17 @@ def run_ours(args):
     Yb = torch.empty(plan.p * plan.r, dtype=torch.complex128, device=dev)
     with torch.cuda.stream(stream):
         for i in range(3):
-            d.execute_partial_ptr(bufs[i % nbuf].data_ptr(), 0, plan.q, plan.q, Yb.data_ptr(), stream=sp)
+            d.execute_partial_ptr(bufs[i % nbuf].data_ptr(), Yb.data_ptr(), stream=sp)
         g1 = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g1, stream=stream):
             for i in range(args.steps):
-                d.execute_partial_ptr(bufs[i % nbuf].data_ptr(), 0, plan.q, plan.q, Yb.data_ptr(), stream=sp)
+                d.execute_partial_ptr(bufs[i % nbuf].data_ptr(), Yb.data_ptr(), stream=sp)
         g1.replay()
     torch.cuda.synchronize(dev)
-    e0.record(stream)
-    g1.replay()
-    e1.record(stream)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        g1.replay()
+        e1.record(stream)
     torch.cuda.synchronize(dev)
     k1_ms = e0.elapsed_time(e1) / args.steps
     peak, peak_src = measured_hbm_peak()
@@ -327,7 +328,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2b", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -144,7 +144,7 @@ typedef struct pft_dplan_s* pft_dplan_t;
 typedef struct pft_dplan_opts {
     int device;        /* CUDA ordinal                                              */
     uint64_t p2;       /* residue classes for K1 (0 = auto); must divide p          */
-    int threads;       /* K1 block size (0 = auto)                                  */
+    int k1_stages;     /* K1 TMA ring depth, 4..8 (0 = deepest that keeps 2 CTAs/SM) */
     int reserved[6];
 } pft_dplan_opts;
 
@@ -165,18 +165,31 @@ pft_status pft_partial_bytes(pft_dplan_t d, size_t batch, size_t* bytes);
 pft_status pft_execute(pft_dplan_t d, const pft_c128* d_in, size_t batch, size_t in_stride,
                        pft_c128* d_out, void* d_ws, void* stream);
 
-/* Sharded single transform (contraction-axis split, BASELINE.json configs[4]):
- * each rank owns, for every row k in [p], the column slice [l0, l0 + lq) of A (its
- * local buffer is p rows of row_stride >= lq elements); see pft_shard_columns.  execute_partial contracts the local slice
- * and applies K1's FFT pass, writing a reducible partial slab (sum over ranks ==
- * the unsharded slab); finalize turns the reduced slab into the 2M+1 outputs. */
-pft_status pft_execute_partial(pft_dplan_t d, const pft_c128* d_in_local, uint64_t l0,
-                               uint64_t lq, uint64_t row_stride, pft_c128* d_partial,
-                               void* stream);
-pft_status pft_finalize(pft_dplan_t d, const pft_c128* d_partial, size_t batch,
-                        pft_c128* d_out, void* stream);
-/* Column range [l0, l0+lq) of rank `rank` among `world` (contiguous, near-equal). */
-pft_status pft_shard_columns(uint64_t q, int world, int rank, uint64_t* l0, uint64_t* lq);
+/* Sharded single transform (contraction-axis split, BASELINE.json configs[4]).
+ * Columns of A are owned in mirror pairs (l, q-l), l in [1, ceil(q/2)), split contiguously
+ * over ranks; the unpaired columns l = 0 and (even q) l = q/2 belong to rank 0.  Each rank's
+ * local buffer holds p rows of `row_stride` elements laid out as pft_shard_layout says.
+ * execute_partial contracts the local slice and applies K1's FFT pass, writing a reducible
+ * partial slab of pft_partial_bytes (the sum over ranks == the unsharded slab, e.g. via
+ * ncclReduce/ncclAllReduce with ncclDouble/ncclSum); finalize turns the reduced slab into
+ * the 2M+1 outputs.  world == 1 is the natural (unsharded) layout. */
+typedef struct pft_shard_info {
+    uint64_t pair_begin, pair_end; /* global pair indices [pair_begin, pair_end)            */
+    uint64_t row_len;              /* local columns per row                                 */
+    int64_t front_col;             /* local column of l = pair_begin (l ascending)          */
+    int64_t mirror_col;            /* local column of q - pair_begin (descending with l)    */
+    int64_t single0_col;           /* local column of l = 0, or -1                          */
+    int64_t singleh_col;           /* local column of l = q/2 (even q), or -1               */
+} pft_shard_info;
+
+pft_status pft_shard_layout(uint64_t q, int world, int rank, pft_shard_info* info);
+/* Host helper: scatter the global signal a (p rows of q) into rank's local layout. */
+pft_status pft_shard_gather_host(uint64_t p, uint64_t q, int world, int rank, const pft_c128* a,
+                                 pft_c128* local, uint64_t row_stride);
+pft_status pft_execute_partial(pft_dplan_t d, const pft_c128* d_in_local, int world, int rank,
+                               uint64_t row_stride, pft_c128* d_partial, void* stream);
+pft_status pft_finalize(pft_dplan_t d, const pft_c128* d_partial, size_t batch, pft_c128* d_out,
+                        void* stream);
 
 /* Status word written by the kernels (non-finite output => non-finite input).
  * Synchronises `stream`; *flags bit0 = non-finite seen since the last reset. */

@@ -21,7 +21,8 @@ from ._capi import c128
 __all__ = [
     "PftError", "ApproxPoly", "ScopeTable", "CostEstimate", "TargetRange", "PartialSpectrum", "PftPlan",
     "DevicePlan", "best_approx", "scope_xi", "translate_poly", "divisors", "min_terms", "select_divisor",
-    "build_plan", "execute", "mod_index", "l1_norm", "generate_signal", "sparse_tones", "shard_columns",
+    "build_plan", "execute", "mod_index", "l1_norm", "generate_signal", "sparse_tones", "shard_layout",
+    "shard_gather",
     "device_count", "lib",
 ]
 
@@ -410,11 +411,12 @@ class DevicePlan:
     """A plan uploaded to one B200 (pft_dplan_t).  Device buffers are passed as raw
     pointers (e.g. torch.Tensor.data_ptr() of complex128 CUDA tensors)."""
 
-    def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0):
+    def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0, k1_stages: int = 0):
         self.plan = plan
         opts = _capi.DPlanOpts()
         opts.device = device
         opts.p2 = p2
+        opts.k1_stages = k1_stages
         h = C.c_void_p()
         _check(lib().pft_dplan_create(plan.handle, C.byref(opts), C.byref(h)))
         self._h = h
@@ -453,9 +455,10 @@ class DevicePlan:
         _check(lib().pft_execute(self._h, C.c_void_p(d_in), batch, in_stride, C.c_void_p(d_out),
                                  C.c_void_p(d_ws or None), C.c_void_p(stream or None)))
 
-    def execute_partial_ptr(self, d_in_local: int, l0: int, lq: int, row_stride: int, d_partial: int,
-                            stream: int = 0) -> None:
-        _check(lib().pft_execute_partial(self._h, C.c_void_p(d_in_local), l0, lq, row_stride,
+    def execute_partial_ptr(self, d_in_local: int, d_partial: int, world: int = 1, rank: int = 0,
+                            row_stride: int = 0, stream: int = 0) -> None:
+        """K1 only, on rank `rank`'s slice (shard_layout) of A: writes the reducible slab."""
+        _check(lib().pft_execute_partial(self._h, C.c_void_p(d_in_local), int(world), int(rank), row_stride,
                                          C.c_void_p(d_partial), C.c_void_p(stream or None)))
 
     def finalize_ptr(self, d_partial: int, d_out: int, batch: int = 1, stream: int = 0) -> None:
@@ -488,11 +491,33 @@ def execute(plan: PftPlan, a, device: int = 0) -> PartialSpectrum:
 
 # ----------------------------------------------------------------------------- sharding + inputs
 
-def shard_columns(q: int, world: int, rank: int) -> tuple[int, int]:
-    """Contraction-axis slice [l0, l0+lq) owned by `rank` (C5 sharding)."""
-    l0, lq = C.c_uint64(), C.c_uint64()
-    _check(lib().pft_shard_columns(int(q), int(world), int(rank), C.byref(l0), C.byref(lq)))
-    return l0.value, lq.value
+@dataclasses.dataclass(frozen=True)
+class ShardLayout:
+    """Contraction-axis slice of one rank (pft_shard_info): mirror column pairs
+    (l, q-l) for l in [pair_begin, pair_end), plus the unpaired columns on rank 0."""
+    pair_begin: int
+    pair_end: int
+    row_len: int
+    front_col: int
+    mirror_col: int
+    single0_col: int
+    singleh_col: int
+
+
+def shard_layout(q: int, world: int, rank: int) -> ShardLayout:
+    info = _capi.ShardInfo()
+    _check(lib().pft_shard_layout(int(q), int(world), int(rank), C.byref(info)))
+    return ShardLayout(info.pair_begin, info.pair_end, info.row_len, info.front_col, info.mirror_col,
+                       info.single0_col, info.singleh_col)
+
+
+def shard_gather(a, p: int, q: int, world: int, rank: int) -> np.ndarray:
+    """Host scatter of the global signal into `rank`'s local layout (p x row_len)."""
+    a = np.ascontiguousarray(a, dtype=np.complex128).reshape(-1)
+    v = shard_layout(q, world, rank)
+    out = np.zeros(max(p * v.row_len, 1), dtype=np.complex128)
+    _check(lib().pft_shard_gather_host(int(p), int(q), int(world), int(rank), _ptr(a), _ptr(out), v.row_len))
+    return out[:p * v.row_len].reshape(p, v.row_len)
 
 
 def sparse_tones(seed: int, n: int, lo: int, hi: int) -> tuple[np.ndarray, np.ndarray]:

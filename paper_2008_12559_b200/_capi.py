@@ -25,7 +25,13 @@ class PlanInfo(C.Structure):
 
 
 class DPlanOpts(C.Structure):
-    _fields_ = [("device", C.c_int), ("p2", C.c_uint64), ("threads", C.c_int), ("reserved", C.c_int * 6)]
+    _fields_ = [("device", C.c_int), ("p2", C.c_uint64), ("k1_stages", C.c_int), ("reserved", C.c_int * 6)]
+
+
+class ShardInfo(C.Structure):
+    _fields_ = [("pair_begin", C.c_uint64), ("pair_end", C.c_uint64), ("row_len", C.c_uint64),
+                ("front_col", C.c_int64), ("mirror_col", C.c_int64), ("single0_col", C.c_int64),
+                ("singleh_col", C.c_int64)]
 
 
 class SignalDesc(C.Structure):
@@ -80,9 +86,10 @@ SIGNATURES: dict[str, tuple] = {
     "pft_workspace_bytes": (ST, [P, SZ, C.POINTER(SZ)]),
     "pft_partial_bytes": (ST, [P, SZ, C.POINTER(SZ)]),
     "pft_execute": (ST, [P, P, SZ, SZ, P, P, P]),
-    "pft_execute_partial": (ST, [P, P, U64, U64, U64, P, P]),
+    "pft_execute_partial": (ST, [P, P, I, I, U64, P, P]),
     "pft_finalize": (ST, [P, P, SZ, P, P]),
-    "pft_shard_columns": (ST, [U64, I, I, C.POINTER(U64), C.POINTER(U64)]),
+    "pft_shard_layout": (ST, [U64, I, I, C.POINTER(ShardInfo)]),
+    "pft_shard_gather_host": (ST, [U64, U64, I, I, P, P, U64]),
     "pft_status_query": (ST, [P, P, C.POINTER(I), I]),
     "pft_execute_host": (ST, [P, P, SZ, P, P, P, P]),
     "pft_generate_host": (ST, [C.POINTER(SignalDesc), P, U64]),

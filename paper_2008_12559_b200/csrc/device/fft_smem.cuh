@@ -35,6 +35,12 @@ struct Twiddles {
     __device__ __forceinline__ double2 operator()(uint32_t t) const { return __ldg(tab + (size_t)t * stride); }
 };
 
+// Same, for a dense omega_n table staged in shared memory (no global round trip per stage).
+struct SmemTwiddles {
+    const double2* tab;
+    __device__ __forceinline__ double2 operator()(uint32_t t) const { return tab[t]; }
+};
+
 __device__ __forceinline__ void dft2(double2& a, double2& b) {
     const double2 t = a;
     a = cadd(t, b);
@@ -82,9 +88,9 @@ __device__ __forceinline__ void dft3(double2& v0, double2& v1, double2& v2) {
 }
 
 // One Stockham stage with a radix known at compile time (2, 3, 4, 8).
-template <int R>
+template <int R, class TW>
 __device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__ src, double2* __restrict__ dst,
-                                                     int ncols, int n, int Ns, const Twiddles& tw) {
+                                                     int ncols, int n, int Ns, const TW& tw) {
     const int nb = n / R;
     const uint32_t tstride = (uint32_t)(n / (Ns * R));
     for (int idx = threadIdx.x; idx < ncols * nb; idx += blockDim.x) {
@@ -110,8 +116,9 @@ __device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__
 }
 
 // Generic radix (any R): O(R^2) per butterfly, twiddles omega_R^{rs} = omega_n^{rs n/R}.
+template <class TW>
 __device__ __forceinline__ void stockham_stage_generic(const double2* __restrict__ src, double2* __restrict__ dst,
-                                                       int ncols, int n, int Ns, int R, const Twiddles& tw) {
+                                                       int ncols, int n, int Ns, int R, const TW& tw) {
     const int nb = n / R;
     const uint32_t tstride = (uint32_t)(n / (Ns * R));
     const uint32_t rstride = (uint32_t)(n / R);
@@ -134,8 +141,9 @@ __device__ __forceinline__ void stockham_stage_generic(const double2* __restrict
 
 // Full transform of ncols columns; returns the buffer holding the result (x or y).
 // Caller must __syncthreads() before (inputs written) and after (outputs read).
+template <class TW>
 __device__ __forceinline__ double2* fft_columns(double2* x, double2* y, int ncols, const FftRadices& plan,
-                                                const Twiddles& tw) {
+                                                const TW& tw) {
     double2* src = x;
     double2* dst = y;
     int Ns = 1;

@@ -8,31 +8,49 @@
 
 namespace pftdev {
 
-// K1: 8 consumer warps + 1 TMA producer warp; a stage is a 32-row x 32-column box of A
-// (16 KiB of complex128); 4 stages in flight per CTA, 2 CTAs per SM.
+// K1: 8 consumer warps + 1 TMA producer warp.  A stage holds, for 16 rows of A, a chunk of
+// 32 column pairs (l, q-l): the "front" box (columns l ascending) and the "mirror" box
+// (columns q-l), 16 x 32 complex128 each, plus the 32-entry pair table slice
+// {Re phase_l, Im phase_l, t_l, 0}.  Two K1 CTAs share an SM.
 constexpr int K1_CONSUMER_WARPS = 8;
 constexpr int K1_THREADS = 32 * (K1_CONSUMER_WARPS + 1);
-constexpr int K1_GROUP = 8;       // lanes per row
-constexpr int K1_BOX_ROWS = 32;   // = K1_CONSUMER_WARPS * (32 / K1_GROUP)
-constexpr int K1_CH = 32;         // columns per stage
-constexpr int K1_STAGES = 4;
-constexpr int K1_STAGE_ELEMS = K1_BOX_ROWS * K1_CH;
-constexpr uint32_t K1_STAGE_BYTES = K1_STAGE_ELEMS * 16;
-constexpr size_t K1_RING_BYTES = (size_t)K1_STAGES * K1_STAGE_BYTES;
-static_assert(K1_BOX_ROWS == K1_CONSUMER_WARPS * (32 / K1_GROUP), "one row per lane group");
+constexpr int K1_BR = 16;          // rows per box (2 per consumer warp, 16 lanes per row)
+constexpr int K1_CP = 32;          // column pairs per chunk
+constexpr int K1_LANES_PER_ROW = 16;
+constexpr uint32_t K1_BOX_BYTES = K1_BR * K1_CP * 16;  // 8 KiB
+constexpr uint32_t K1_TAB_BYTES = K1_CP * 32;           // 1 KiB
+constexpr uint32_t K1_STAGE_BYTES = 2 * K1_BOX_BYTES + K1_TAB_BYTES;
+constexpr int K1_MIN_STAGES = 4, K1_MAX_STAGES = 8;
+constexpr size_t K1_MIN_RING_BYTES = (size_t)K1_MIN_STAGES * K1_STAGE_BYTES;
+static_assert(K1_BR == K1_CONSUMER_WARPS * (32 / K1_LANES_PER_ROW), "one row per half-warp");
+static_assert(K1_STAGE_BYTES % 128 == 0, "TMA destinations stay 128-byte aligned");
 
 constexpr int K2_THREADS = 256;
 
+// Pair-table entry (host-built): phase_l = e^{-2 pi i mu (l - q/2)/N} and t_l = 1 - 2l/q.
+// The mirror column q-l uses conj(phase_l) and -t_l (exact identities of SPEC.md:126).
+struct PairEntry {
+    double c, s, t, pad;
+};
+
 struct K1Params {
-    uint64_t lq;            // columns of each row processed by this launch
-    uint64_t l0;            // global column index of local column 0 (table offset)
-    const double2* phase;   // [q]  e^{-2 pi i mu (l - q/2) / N}
-    const double* tvals;    // [q]  1 - 2l/q
-    const double2* w;       // [r]  w_{eps, r-1, j}
-    const double2* omega;   // [p]  e^{-2 pi i t / p}
-    uint32_t P1, P2;        // p = P1 * P2
-    FftRadices fft;         // radices of P1
-    double2* Y;             // [batch][P1][P2][r]
+    // local view of A (rows k = c + P2 k1 at a + k * row_stride, signal b at + b * batch_stride)
+    const double2* a;
+    uint64_t row_stride, batch_stride;
+    // column pairs handled by this launch: global pair indices [gp0, gp_end), gp0 >= 1;
+    // pair gp0 + t sits at local column fcol0 + t (front) and mcol0 - t (mirror)
+    uint32_t gp0, gp_end;
+    int32_t fcol0, mcol0;
+    // unpaired columns: l = 0 (t = 1) and, for even q, l = q/2 (t = 0); -1 = not in this view
+    int32_t single0_col, singleh_col;
+    double2 phase0, phaseh;     // phase_0, phase_{q/2}
+    const PairEntry* pairtab;   // [>= gp_end + K1_CP]
+    const double2* w;           // [r]  w_{eps, r-1, j}
+    const double2* omega;       // [p]  e^{-2 pi i t / p}
+    uint32_t P1, P2;            // p = P1 * P2
+    FftRadices fft;             // radices of P1
+    uint32_t stages;            // ring depth (K1_MIN_STAGES..K1_MAX_STAGES)
+    double2* Y;                 // [batch][P1][P2][r]
 };
 
 struct K2Params {
@@ -61,11 +79,21 @@ struct GenParams {
     double2* out;
 };
 
-// ring + C slab + 2*S mbarriers; the ring doubles as the FFT scratch (needs r*P1*16 <= ring)
-inline size_t k1_smem_bytes(int r, uint32_t P1) {
-    return K1_RING_BYTES + sizeof(double2) * (size_t)r * (P1 ? P1 : 1) + 2 * K1_STAGES * sizeof(uint64_t);
+// ring + C slab + P1 twiddles + 2*S mbarriers; the ring doubles as the FFT scratch
+// (needs r*P1*16 <= the smallest ring)
+inline size_t k1_smem_bytes(int r, uint32_t P1, uint32_t stages) {
+    const size_t p1 = P1 ? P1 : 1;
+    return (size_t)stages * K1_STAGE_BYTES + sizeof(double2) * ((size_t)r * p1 + p1) + 2 * stages * sizeof(uint64_t);
 }
-inline size_t k2_smem_bytes(int r, uint32_t P2) { return 2 * sizeof(double2) * (size_t)r * P2; }
+// K1 ring depth: as deep as possible while two CTAs still share an SM.
+inline uint32_t k1_pick_stages(int r, uint32_t P1) {
+    const size_t per_cta = (228 * 1024) / 2 - 1024;
+    uint32_t s = K1_MAX_STAGES;
+    while (s > K1_MIN_STAGES && k1_smem_bytes(r, P1, s) > per_cta) --s;
+    return s;
+}
+// Z + scratch (r x P2 each) + omega_P2 + four-step twiddles (P2 each)
+inline size_t k2_smem_bytes(int r, uint32_t P2) { return sizeof(double2) * (2 * (size_t)r * P2 + 2 * (size_t)P2); }
 
 cudaError_t configure_k1(int r, uint32_t P1, bool mu0);
 cudaError_t configure_k2(int r, uint32_t P2);

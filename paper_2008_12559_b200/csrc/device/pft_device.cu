@@ -72,7 +72,7 @@ constexpr size_t kK2SmemLimit = 220 * 1024;
 bool k1_feasible(uint64_t P1, int r) {
     pftdev::FftRadices fr;
     if (P1 > 1 && !factor_radices((uint32_t)P1, fr)) return false;
-    return sizeof(double2) * (size_t)r * P1 <= pftdev::K1_RING_BYTES;  // FFT scratch = the ring
+    return sizeof(double2) * (size_t)r * P1 <= pftdev::K1_MIN_RING_BYTES;  // FFT scratch = the ring
 }
 
 bool k2_fft_feasible(uint64_t P2, int r) {
@@ -108,14 +108,15 @@ struct pft_dplan_s {
     uint64_t P1 = 0, P2 = 0;
     pftdev::FftRadices fft{};   // radices of P1 (K1)
     pftdev::FftRadices fft2{};  // radices of P2 (K2)
+    uint32_t k1_stages = pftdev::K1_MIN_STAGES;
     bool k2_fft = false;
     bool mu0 = false;
     uint64_t W = 0;
     // device allocations
     void* tables = nullptr;
-    double2* d_phase = nullptr;
-    double* d_tvals = nullptr;
+    pftdev::PairEntry* d_pairtab = nullptr;
     double2* d_w = nullptr;
+    double2 phase0{1.0, 0.0}, phaseh{1.0, 0.0};
     double2* d_omega = nullptr;
     double* d_post_powers = nullptr;
     double2* d_post_twiddles = nullptr;
@@ -136,17 +137,27 @@ struct pft_dplan_s {
 
     size_t slab_elems() const { return (size_t)host.p * host.r; }
 
-    pftdev::K1Params k1_params(uint64_t lq, uint64_t l0, double2* Y) const {
+    pftdev::K1Params k1_params(const ShardLayout& v, const double2* a, uint64_t row_stride, size_t batch_stride,
+                               double2* Y) const {
         pftdev::K1Params P{};
-        P.lq = lq;
-        P.l0 = l0;
-        P.phase = d_phase;
-        P.tvals = d_tvals;
+        P.a = a;
+        P.row_stride = row_stride;
+        P.batch_stride = batch_stride;
+        P.gp0 = (uint32_t)v.pair_begin;
+        P.gp_end = (uint32_t)v.pair_end;
+        P.fcol0 = (int32_t)v.front_col;
+        P.mcol0 = (int32_t)v.mirror_col;
+        P.single0_col = (int32_t)v.single0_col;
+        P.singleh_col = (int32_t)v.singleh_col;
+        P.phase0 = phase0;
+        P.phaseh = phaseh;
+        P.pairtab = d_pairtab;
         P.w = d_w;
         P.omega = d_omega;
         P.P1 = (uint32_t)P1;
         P.P2 = (uint32_t)P2;
         P.fft = fft;
+        P.stages = k1_stages;
         P.Y = Y;
         return P;
     }
@@ -205,17 +216,18 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-// 4-D view of the input for K1's bulk tensor copies: (2*lq doubles of a row, residue c,
-// k1, signal) with row k = c + P2 k1 at base + k * row_stride elements.
-CUtensorMap make_input_map(const pft_dplan_s* d, const void* base, uint64_t lq, uint64_t row_stride,
+// 4-D view of the input for K1's bulk tensor copies: (2*row_len doubles of a row, residue
+// c, k1, signal) with row k = c + P2 k1 at base + k * row_stride elements.  Boxes of
+// 16 rows x 32 columns; out-of-range coordinates (including negative) are zero-filled.
+CUtensorMap make_input_map(const pft_dplan_s* d, const void* base, uint64_t row_len, uint64_t row_stride,
                            size_t batch, size_t batch_stride) {
     PFT_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, "input must be 16-byte aligned");
     CUtensorMap map;
-    const cuuint64_t dims[4] = {2 * lq, d->P2, d->P1, std::max<size_t>(batch, 1)};
+    const cuuint64_t dims[4] = {2 * std::max<uint64_t>(row_len, 1), d->P2, d->P1, std::max<size_t>(batch, 1)};
     const cuuint64_t row_bytes = row_stride * 16;
     const cuuint64_t strides[3] = {row_bytes, row_bytes * d->P2,
                                    (batch > 1 ? batch_stride : d->P1 * d->P2 * row_stride) * 16};
-    const cuuint32_t box[4] = {2 * pftdev::K1_CH, 1, pftdev::K1_BOX_ROWS, 1};
+    const cuuint32_t box[4] = {2 * pftdev::K1_CP, 1, pftdev::K1_BR, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUresult r = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims,
                                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -227,8 +239,9 @@ CUtensorMap make_input_map(const pft_dplan_s* d, const void* base, uint64_t lq, 
 
 void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stride, double2* out, double2* Y,
                  cudaStream_t st) {
-    const CUtensorMap map = make_input_map(d, in, d->host.q, d->host.q, batch, in_stride);
-    const auto P1 = d->k1_params(d->host.q, 0, Y);
+    const ShardLayout v = shard_layout(d->host.q, 1, 0);
+    const CUtensorMap map = make_input_map(d, in, v.row_len, d->host.q, batch, in_stride);
+    const auto P1 = d->k1_params(v, in, d->host.q, in_stride, Y);
     cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
     const auto P2 = d->k2_params(Y, out);
     cuda_check(pftdev::launch_k2(P2, d->host.r, (uint32_t)batch, st), "K2 launch");
@@ -285,6 +298,8 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     if (d->P1 <= 1) d->fft.n = 1;
     if (!k1_feasible(d->P1, H.r))
         fail(PFT_ERR_UNSUPPORTED, "dplan_create: P1 * r too large for K1 shared memory; choose a larger p2");
+    d->k1_stages = (opts && opts->k1_stages) ? (uint32_t)opts->k1_stages : pftdev::k1_pick_stages(H.r, (uint32_t)d->P1);
+    PFT_REQUIRE(d->k1_stages >= (uint32_t)pftdev::K1_MIN_STAGES && d->k1_stages <= (uint32_t)pftdev::K1_MAX_STAGES, "dplan_create: k1_stages out of [4, 8]");
     d->k2_fft = k2_fft_feasible(d->P2, H.r);
     if (d->k2_fft) {
         if (d->P2 > 1) factor_radices((uint32_t)d->P2, d->fft2);
@@ -297,22 +312,30 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
 #pragma omp parallel for schedule(static)
     for (long long t = 0; t < (long long)H.p; ++t) omega[t] = cispi_frac(-2 * (__int128)t, H.p);
 
+    // pair table {Re phase_l, Im phase_l, t_l, 0} for l in [0, L), zero-padded so a chunk
+    // read past the last pair stays in bounds
+    const uint64_t L = (H.q + 1) / 2;
+    const uint64_t n_pt = L + 2 * pftdev::K1_CP;
+    std::vector<pftdev::PairEntry> pairtab(n_pt, pftdev::PairEntry{0.0, 0.0, 0.0, 0.0});
+    for (uint64_t l = 0; l < L; ++l) pairtab[l] = {H.phase[l].real(), H.phase[l].imag(), H.tvals[l], 0.0};
+    d->phase0 = make_double2(H.phase[0].real(), H.phase[0].imag());
+    if (H.q % 2 == 0) d->phaseh = make_double2(H.phase[H.q / 2].real(), H.phase[H.q / 2].imag());
+
     // one allocation for all tables, 256-byte aligned pieces
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-    const size_t b_phase = al(H.q * sizeof(double2)), b_tv = al(H.q * sizeof(double)),
-                 b_w = al(H.r * sizeof(double2)), b_om = al(H.p * sizeof(double2)),
-                 b_pp = al(d->W * H.r * sizeof(double)), b_pt = al(d->W * sizeof(double2));
-    const size_t total = b_phase + b_tv + b_w + b_om + b_pp + b_pt;
+    const size_t b_pt0 = al(n_pt * sizeof(pftdev::PairEntry)), b_w = al(H.r * sizeof(double2)),
+                 b_om = al(H.p * sizeof(double2)), b_pp = al(d->W * H.r * sizeof(double)),
+                 b_pt = al(d->W * sizeof(double2));
+    const size_t total = b_pt0 + b_w + b_om + b_pp + b_pt;
     cuda_check(cudaMalloc(&d->tables, total), "cudaMalloc(tables)");
     char* base = static_cast<char*>(d->tables);
-    d->d_phase = reinterpret_cast<double2*>(base);
-    d->d_tvals = reinterpret_cast<double*>(base + b_phase);
-    d->d_w = reinterpret_cast<double2*>(base + b_phase + b_tv);
-    d->d_omega = reinterpret_cast<double2*>(base + b_phase + b_tv + b_w);
-    d->d_post_powers = reinterpret_cast<double*>(base + b_phase + b_tv + b_w + b_om);
-    d->d_post_twiddles = reinterpret_cast<double2*>(base + b_phase + b_tv + b_w + b_om + b_pp);
-    cuda_check(cudaMemcpy(d->d_phase, H.phase.data(), H.q * sizeof(double2), cudaMemcpyHostToDevice), "upload phase");
-    cuda_check(cudaMemcpy(d->d_tvals, H.tvals.data(), H.q * sizeof(double), cudaMemcpyHostToDevice), "upload tvals");
+    d->d_pairtab = reinterpret_cast<pftdev::PairEntry*>(base);
+    d->d_w = reinterpret_cast<double2*>(base + b_pt0);
+    d->d_omega = reinterpret_cast<double2*>(base + b_pt0 + b_w);
+    d->d_post_powers = reinterpret_cast<double*>(base + b_pt0 + b_w + b_om);
+    d->d_post_twiddles = reinterpret_cast<double2*>(base + b_pt0 + b_w + b_om + b_pp);
+    cuda_check(cudaMemcpy(d->d_pairtab, pairtab.data(), n_pt * sizeof(pftdev::PairEntry), cudaMemcpyHostToDevice),
+               "upload pair table");
     cuda_check(cudaMemcpy(d->d_w, H.w.data(), H.r * sizeof(double2), cudaMemcpyHostToDevice), "upload w");
     cuda_check(cudaMemcpy(d->d_omega, omega.data(), H.p * sizeof(double2), cudaMemcpyHostToDevice), "upload omega");
     cuda_check(cudaMemcpy(d->d_post_powers, H.post_powers.data(), d->W * H.r * sizeof(double), cudaMemcpyHostToDevice),
@@ -376,17 +399,18 @@ pft_status pft_execute(pft_dplan_t dh, const pft_c128* d_in, size_t batch, size_
     PFT_API_END
 }
 
-pft_status pft_execute_partial(pft_dplan_t dh, const pft_c128* d_in_local, uint64_t l0, uint64_t lq,
+pft_status pft_execute_partial(pft_dplan_t dh, const pft_c128* d_in_local, int world, int rank,
                                uint64_t row_stride, pft_c128* d_partial, void* stream) {
     PFT_API_BEGIN
     pft_dplan_s* d = dp(dh);
     PFT_REQUIRE(d_in_local && d_partial, "execute_partial: null buffer");
-    PFT_REQUIRE(l0 + lq <= d->host.q, "execute_partial: column slice outside [0, q)");
-    PFT_REQUIRE(row_stride >= lq, "execute_partial: row_stride < lq");
+    const ShardLayout v = shard_layout(d->host.q, world, rank);
+    if (row_stride == 0) row_stride = v.row_len;
+    PFT_REQUIRE(row_stride >= v.row_len, "execute_partial: row_stride < local row length");
     DeviceGuard guard(d->device);
-    PFT_REQUIRE(lq >= 1, "execute_partial: empty column slice");
-    const CUtensorMap map = make_input_map(d, d_in_local, lq, row_stride, 1, 0);
-    const auto P = d->k1_params(lq, l0, reinterpret_cast<double2*>(d_partial));
+    const CUtensorMap map = make_input_map(d, d_in_local, v.row_len, row_stride, 1, 0);
+    const auto P = d->k1_params(v, reinterpret_cast<const double2*>(d_in_local), row_stride, 0,
+                                reinterpret_cast<double2*>(d_partial));
     cuda_check(pftdev::launch_k1(map, P, d->host.r, 1, d->mu0, static_cast<cudaStream_t>(stream)), "K1 launch");
     PFT_API_END
 }

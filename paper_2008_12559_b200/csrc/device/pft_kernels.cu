@@ -3,12 +3,14 @@
 //
 //  K1  k1_contract_fft<R, MU0>  one CTA per (residue class c mod P2, signal).  A producer
 //      warp streams the P1 rows k = c + P2*k1 of A (A[k][l] = a[q k + l])
-//      from HBM into a 4-stage shared-memory ring with 4-D bulk tensor copies (TMA,
-//      cp.async.bulk.tensor + mbarrier complete_tx), 32 rows x 32 columns per stage.
-//      Eight consumer warps contract each row against the plan in the structured form
-//      B[l][j] = phase_l * w_j * t_l^j: 3r+3 FP64 ops per element instead of
-//      the dense 4r, 8 lanes per row, xor-shuffle reduction per row.  The P1 x r slab C_c
-//      stays in shared memory and gets the first FFT pass there:
+//      from HBM into a shared-memory ring with 4-D bulk tensor copies (TMA,
+//      cp.async.bulk.tensor + mbarrier complete_tx).  Columns are processed in mirror
+//      pairs (l, q-l): with B[l][j] = phase_l w_j t_l^j, t_{q-l} = -t_l and
+//      phase_{q-l} = conj(phase_l), so a pair contributes t_l^j (b_l + (-1)^j b_{q-l}),
+//      b = a * phase -- (3r+10)/2 FP64 ops per element instead of the dense 4r.  A stage
+//      is 16 rows x 32 pairs (front box, mirror box) plus the pair-table slice.  Eight
+//      consumer warps (16 lanes per row) accumulate, reduce per row by shuffles, and keep
+//      the P1 x r slab C_c in shared memory for the first FFT pass:
 //      Y_c[m1][j] = sum_k1 C[c + P2 k1][j] e^{-2 pi i m1 k1 / P1}.
 //  K2  k2_fft_post<R>           one CTA per m1 in [P1].  Applies the four-step twiddle
 //      e^{-2 pi i m1 c / p}, runs the length-P2 FFT over c in shared memory, and evaluates
@@ -36,106 +38,150 @@ template <int R, bool MU0>
 __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_constant__ CUtensorMap tmap,
                                                                   const K1Params P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double2* ring = reinterpret_cast<double2*>(smem_raw);    // [S][32 rows][CH]
-    double2* Cs = ring + (size_t)K1_STAGES * K1_STAGE_ELEMS;  // [R][P1]
-    uint64_t* full = reinterpret_cast<uint64_t*>(Cs + (size_t)R * P.P1);
-    uint64_t* empty = full + K1_STAGES;
+    const uint32_t S = P.stages;
+    unsigned char* ring = smem_raw;                                                     // [S] stages
+    double2* Cs = reinterpret_cast<double2*>(smem_raw + (size_t)S * K1_STAGE_BYTES);  // [R][P1]
+    double2* tw1 = Cs + (size_t)R * P.P1;                                              // omega_P1^t
+    uint64_t* full = reinterpret_cast<uint64_t*>(tw1 + P.P1);
+    uint64_t* empty = full + S;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int s = 0; s < K1_STAGES; ++s) {
+        for (uint32_t s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], K1_CONSUMER_WARPS);
         }
         fence_barrier_init();
     }
+    // stage the FFT twiddles omega_P1^t = omega_p^{t P2} once (read in every FFT stage)
+    for (uint32_t t = tid; t < P.P1; t += blockDim.x) tw1[t] = __ldg(P.omega + (size_t)t * P.P2);
     __syncthreads();
 
     const uint32_t c = blockIdx.x;  // residue class k = c (mod P2)
     const uint32_t b = blockIdx.y;  // signal
-    const uint32_t nch = (uint32_t)((P.lq + K1_CH - 1) / K1_CH);
-    const uint32_t nrb = (P.P1 + K1_BOX_ROWS - 1) / K1_BOX_ROWS;
+    const uint32_t npairs = P.gp_end > P.gp0 ? P.gp_end - P.gp0 : 0;
+    const uint32_t nch = (npairs + K1_CP - 1) / K1_CP;
+    const uint32_t nrb = (P.P1 + K1_BR - 1) / K1_BR;
     const uint32_t total = nch * nrb;
 
     if (warp == K1_CONSUMER_WARPS) {
-        // ---- producer: one elected lane streams 32-row x CH-column boxes of A into the ring
-        if (lane == 0) {
+        // ---- producer: one elected lane streams front/mirror boxes + table slices
+        if (lane == 0 && total > 0) {
             prefetch_tensormap(&tmap);
             for (uint32_t it = 0; it < total; ++it) {
-                const uint32_t s = it % K1_STAGES, n = it / K1_STAGES;
+                const uint32_t s = it % S, n = it / S;
                 if (n > 0) mbar_wait(&empty[s], (n - 1) & 1);
                 const uint32_t rb = it / nch, ch = it - rb * nch;
+                unsigned char* st = ring + (size_t)s * K1_STAGE_BYTES;
                 mbar_arrive_expect_tx(&full[s], K1_STAGE_BYTES);
-                tma_load_4d(ring + (size_t)s * K1_STAGE_ELEMS, &tmap, (int)(2 * ch * K1_CH), (int)c,
-                            (int)(rb * K1_BOX_ROWS), (int)b, &full[s]);
+                const int row0 = (int)(rb * K1_BR);
+                const int f0 = P.fcol0 + (int)(ch * K1_CP);
+                const int m0 = P.mcol0 - (int)(ch * K1_CP) - (K1_CP - 1);  // may be < 0: zero fill
+                tma_load_4d(st, &tmap, 2 * f0, (int)c, row0, (int)b, &full[s]);
+                tma_load_4d(st + K1_BOX_BYTES, &tmap, 2 * m0, (int)c, row0, (int)b, &full[s]);
+                bulk_load(st + 2 * K1_BOX_BYTES, P.pairtab + P.gp0 + ch * K1_CP, K1_TAB_BYTES, &full[s]);
             }
         }
     } else {
-        // ---- consumers: 8 lanes per row, 4 rows per warp, 32 rows per box
-        const int gl = lane & (K1_GROUP - 1);
-        const int grp = warp * (32 / K1_GROUP) + lane / K1_GROUP;
-        const uint64_t lmax = P.l0 + P.lq - 1;  // last valid global column (clamp for zero-filled lanes)
+        // ---- consumers: half-warp per row, lane li takes pairs li and li + 16 of each chunk
+        const int li = lane & (K1_LANES_PER_ROW - 1);
+        const int rin = warp * 2 + (lane >> 4);  // row within the box
         for (uint32_t rb = 0; rb < nrb; ++rb) {
             double are[R], aim[R];
 #pragma unroll
             for (int j = 0; j < R; ++j) are[j] = aim[j] = 0.0;
+            const uint32_t k1 = rb * K1_BR + rin;
+            // unpaired column of this lane (l = 0 on li 0, l = q/2 on li 1): issue the load now,
+            // consume it after the chunk loop so its DRAM latency is hidden
+            const int scol = li == 0 ? P.single0_col : (li == 1 ? P.singleh_col : -1);
+            double2 xs = make_double2(0.0, 0.0);
+            if (k1 < P.P1 && scol >= 0)
+                xs = __ldg(P.a + (size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride + scol);
             for (uint32_t ch = 0; ch < nch; ++ch) {
                 const uint32_t it = rb * nch + ch;
-                const uint32_t s = it % K1_STAGES, n = it / K1_STAGES;
+                const uint32_t s = it % S, n = it / S;
                 mbar_wait(&full[s], n & 1);
                 // Reconverge before touching the stage: lane 0's `empty` arrive below leaves
                 // the warp diverged, and reading a stage from a diverged warp was observed to
                 // return corrupt rows on B200 when two K1 CTAs share an SM.
                 __syncwarp();
-                const double2* row = ring + (size_t)s * K1_STAGE_ELEMS + (size_t)grp * K1_CH;
+                const unsigned char* st = ring + (size_t)s * K1_STAGE_BYTES;
+                const double2* front = reinterpret_cast<const double2*>(st) + rin * K1_CP;
+                const double2* mirror = reinterpret_cast<const double2*>(st + K1_BOX_BYTES) + rin * K1_CP;
+                const PairEntry* tab = reinterpret_cast<const PairEntry*>(st + 2 * K1_BOX_BYTES);
+                const uint32_t valid = min((uint32_t)K1_CP, npairs - ch * K1_CP);
 #pragma unroll
-                for (int u = 0; u < K1_CH / K1_GROUP; ++u) {
-                    const int col = gl + u * K1_GROUP;
-                    // out-of-range columns/rows arrive as TMA zero fill and contribute 0
-                    uint64_t l = P.l0 + (uint64_t)ch * K1_CH + col;
-                    l = l > lmax ? lmax : l;
-                    double2 x = row[col];
-                    if constexpr (!MU0) x = cmul(x, __ldg(P.phase + l));  // a * e^{-2 pi i mu (l - q/2)/N}
-                    const double t = __ldg(P.tvals + l);                   // 1 - 2l/q
-                    are[0] += x.x;
-                    aim[0] += x.y;
-                    double tp = t;
+                for (int u = 0; u < K1_CP / K1_LANES_PER_ROW; ++u) {
+                    const int i = li + u * K1_LANES_PER_ROW;
+                    if ((uint32_t)i < valid) {
+                        const double2 x1 = front[i];                   // column l
+                        const double2 x2 = mirror[K1_CP - 1 - i];      // column q - l
+                        const double2 cs = *reinterpret_cast<const double2*>(&tab[i].c);
+                        const double t = tab[i].t;
+                        const double2 su = make_double2(x1.x + x2.x, x1.y + x2.y);
+                        const double2 di = make_double2(x1.x - x2.x, x1.y - x2.y);
+                        double2 Sv, Dv;  // phase_l x1 +/- conj(phase_l) x2
+                        if constexpr (MU0) {
+                            Sv = su;
+                            Dv = di;
+                        } else {
+                            Sv = make_double2(fma(cs.x, su.x, -cs.y * di.y), fma(cs.x, su.y, cs.y * di.x));
+                            Dv = make_double2(fma(cs.x, di.x, -cs.y * su.y), fma(cs.x, di.y, cs.y * su.x));
+                        }
+                        are[0] += Sv.x;
+                        aim[0] += Sv.y;
+                        double tp = t;
 #pragma unroll
-                    for (int j = 1; j < R; ++j) {
-                        are[j] = fma(x.x, tp, are[j]);
-                        aim[j] = fma(x.y, tp, aim[j]);
-                        if (j + 1 < R) tp *= t;
+                        for (int j = 1; j < R; ++j) {
+                            const double2 v = (j & 1) ? Dv : Sv;  // t^j (b + (-1)^j b')
+                            are[j] = fma(v.x, tp, are[j]);
+                            aim[j] = fma(v.y, tp, aim[j]);
+                            if (j + 1 < R) tp *= t;
+                        }
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);  // stage s may be refilled
             }
-            // reduce over the 8 lanes of the row (fixed xor-butterfly order)
+            // unpaired columns l = 0 (t = 1: every j) and l = q/2 (t = 0: j = 0 only)
+            if (scol >= 0) {
+                double2 x = xs;
+                if constexpr (!MU0) x = cmul(x, li == 0 ? P.phase0 : P.phaseh);
+                are[0] += x.x;
+                aim[0] += x.y;
+                if (li == 0) {
+#pragma unroll
+                    for (int j = 1; j < R; ++j) {
+                        are[j] += x.x;
+                        aim[j] += x.y;
+                    }
+                }
+            }
+            // reduce over the 16 lanes of the row (fixed xor-butterfly order)
 #pragma unroll
             for (int j = 0; j < R; ++j) {
 #pragma unroll
-                for (int off = K1_GROUP / 2; off >= 1; off >>= 1) {
+                for (int off = K1_LANES_PER_ROW / 2; off >= 1; off >>= 1) {
                     are[j] += __shfl_xor_sync(0xffffffffu, are[j], off);
                     aim[j] += __shfl_xor_sync(0xffffffffu, aim[j], off);
                 }
             }
-            const uint32_t k1 = rb * K1_BOX_ROWS + grp;
 #pragma unroll
             for (int j = 0; j < R; ++j) {
-                if (k1 < P.P1 && (j % K1_GROUP) == gl)
+                if (k1 < P.P1 && (j % K1_LANES_PER_ROW) == li)
                     Cs[(size_t)j * P.P1 + k1] = cmul(make_double2(are[j], aim[j]), __ldg(P.w + j));  // C = w_j acc_j
             }
         }
     }
+    // All of A has been read: let K2 (launched with programmatic stream serialization)
+    // get scheduled and run its prologue while this grid finishes its FFT tail.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __syncthreads();
 
     // First FFT pass over k1 (length P1) for every column j, in shared memory; the ring is
     // idle now and serves as the Stockham scratch buffer.
     const double2* res = Cs;
-    if (P.P1 > 1) {
-        Twiddles tw{P.omega, P.P2};  // omega_P1^t = omega_p^{t P2}
-        res = fft_columns(Cs, ring, R, P.fft, tw);
-    }
+    if (P.P1 > 1) res = fft_columns(Cs, reinterpret_cast<double2*>(ring), R, P.fft, SmemTwiddles{tw1});
     // Y[b][m1][c][j]: the slab for one m1 is contiguous over (c, j) for K2.
     double2* __restrict__ Y = P.Y + (size_t)b * P.P1 * P.P2 * R;
     for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) {
@@ -149,38 +195,54 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
 template <int R>
 __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
     extern __shared__ __align__(16) double2 zs[];
-    double2* Z = zs;  // [R][P2]
-    double2* scratch = zs + (size_t)R * P.P2;
+    double2* Z = zs;                              // [R][P2]
+    double2* scratch = zs + (size_t)R * P.P2;     // [R][P2]
+    double2* tw2 = scratch + (size_t)R * P.P2;    // omega_P2^t
+    double2* pre = tw2 + P.P2;                    // omega_p^{m1 c}
     const uint32_t m1 = blockIdx.x, b = blockIdx.y;
     const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
     if (s0 >= P.W) return;  // no output slot maps to this m1 (block-uniform)
+
+    // ---- prologue (overlaps K1's tail under programmatic dependent launch): tables only
+    for (uint32_t c = threadIdx.x; c < P.P2; c += blockDim.x) {
+        tw2[c] = __ldg(P.omega + (size_t)c * P.P1);  // omega_P2^c = omega_p^{c P1}
+        pre[c] = __ldg(P.omega + (size_t)m1 * c);    // four-step twiddle; m1 c < p
+    }
+    const uint64_t s_first = s0 + (uint64_t)P.P1 * threadIdx.x;
+    double pw0[R];
+    double2 ptw0 = make_double2(0.0, 0.0);
+    if (s_first < P.W) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) pw0[j] = __ldg(P.post_powers + s_first * R + j);
+        ptw0 = __ldg(P.post_twiddles + s_first);
+    }
+    // ---- wait for K1's slab Y to be complete and visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __syncthreads();
     const double2* __restrict__ Y = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
     for (uint32_t idx = threadIdx.x; idx < P.P2 * (uint32_t)R; idx += blockDim.x) {
         const uint32_t c = idx / R, j = idx - c * R;
         const double2 y = Y[idx];
-        // four-step twiddle e^{-2 pi i m1 c / p}; m1 c < P1 P2 = p needs no reduction
-        Z[(size_t)j * P.P2 + c] = (m1 == 0 || c == 0) ? y : cmul(y, __ldg(P.omega + (size_t)m1 * c));
+        Z[(size_t)j * P.P2 + c] = (m1 == 0 || c == 0) ? y : cmul(y, pre[c]);
     }
     __syncthreads();
     const double2* res = Z;
-    if (P.P2 > 1) {
-        Twiddles tw{P.omega, P.P1};  // omega_P2^t = omega_p^{t P1}
-        res = fft_columns(Z, scratch, R, P.fft2, tw);
-    }
+    if (P.P2 > 1) res = fft_columns(Z, scratch, R, P.fft2, SmemTwiddles{tw2});
     double2* __restrict__ out = P.out + (size_t)b * P.W;
-    for (uint64_t s = s0 + (uint64_t)P.P1 * threadIdx.x; s < P.W; s += (uint64_t)P.P1 * blockDim.x) {
+    for (uint64_t s = s_first; s < P.W; s += (uint64_t)P.P1 * blockDim.x) {
         uint64_t mp = P.first_mod_p + s % P.p;
         if (mp >= P.p) mp -= P.p;
         const uint32_t m2 = (uint32_t)(mp / P.P1);
+        const bool first = s == s_first;
         double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
         for (int j = 0; j < R; ++j) {  // ascending j
-            const double pw = __ldg(P.post_powers + s * R + j);
+            const double pw = first ? pw0[j] : __ldg(P.post_powers + s * R + j);
             const double2 v = res[(size_t)j * P.P2 + m2];
             acc.x = fma(v.x, pw, acc.x);
             acc.y = fma(v.y, pw, acc.y);
         }
-        const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+        const double2 v = cmul(acc, first ? ptw0 : __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
         out[s] = v;
         if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
     }
@@ -198,6 +260,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_direct_post(K2Params P) {
     const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
     const double2* __restrict__ Y = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
     double2* __restrict__ out = P.out + (size_t)b * P.W;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     for (uint64_t s = s0 + (uint64_t)P.P1 * warp; s < P.W; s += (uint64_t)P.P1 * NW) {
         uint64_t mp = P.first_mod_p + s % P.p;
@@ -292,11 +355,20 @@ static cudaError_t configure_k1_r(size_t smem, bool mu0) {
 
 template <int R>
 static cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
-    if (P.use_fft)
-        k2_fft_post<R><<<grid, K2_THREADS, k2_smem_bytes(R, P.P2), st>>>(P);
-    else
-        k2_direct_post<R><<<grid, K2_THREADS, 0, st>>>(P);
-    return cudaGetLastError();
+    // Programmatic dependent launch: K2 may start its table prologue while K1 drains;
+    // griddepcontrol.wait in K2 orders its reads of Y after K1's completion.
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(K2_THREADS);
+    cfg.dynamicSmemBytes = P.use_fft ? k2_smem_bytes(R, P.P2) : 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (P.use_fft) return cudaLaunchKernelEx(&cfg, k2_fft_post<R>, P);
+    return cudaLaunchKernelEx(&cfg, k2_direct_post<R>, P);
 }
 
 template <int R>
@@ -332,7 +404,7 @@ cudaError_t configure_k2(int r, uint32_t P2) {
 
 cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t batch, bool mu0, cudaStream_t st) {
     const dim3 grid(P.P2, batch);
-    const size_t smem = k1_smem_bytes(r, P.P1);
+    const size_t smem = k1_smem_bytes(r, P.P1, P.stages);
     switch (r) {
 #define X(n) case n: return launch_k1_r<n>(map, P, grid, smem, st, mu0);
         PFT_R_CASES(X)

@@ -256,16 +256,32 @@ pft_status pft_plan_json(pft_hplan_t plan, char* buf, size_t cap, size_t* needed
     PFT_API_END
 }
 
-pft_status pft_shard_columns(uint64_t q, int world, int rank, uint64_t* l0, uint64_t* lq) {
+pft_status pft_shard_layout(uint64_t q, int world, int rank, pft_shard_info* info) {
     PFT_API_BEGIN
-    PFT_REQUIRE(world >= 1 && rank >= 0 && rank < world && l0 && lq, "shard_columns: bad arguments");
-    PFT_REQUIRE(q >= 1, "shard_columns: q must be >= 1");
-    // Contiguous near-equal split of the contraction axis [0, q): the first q % world
-    // ranks get one extra column.
-    const uint64_t base = q / world, extra = q % world;
-    const uint64_t r = static_cast<uint64_t>(rank);
-    *l0 = r * base + std::min<uint64_t>(r, extra);
-    *lq = base + (r < extra ? 1 : 0);
+    PFT_REQUIRE(info != nullptr, "info is null");
+    const ShardLayout v = shard_layout(q, world, rank);
+    info->pair_begin = v.pair_begin;
+    info->pair_end = v.pair_end;
+    info->row_len = v.row_len;
+    info->front_col = v.front_col;
+    info->mirror_col = v.mirror_col;
+    info->single0_col = v.single0_col;
+    info->singleh_col = v.singleh_col;
+    PFT_API_END
+}
+
+pft_status pft_shard_gather_host(uint64_t p, uint64_t q, int world, int rank, const pft_c128* a, pft_c128* local,
+                                 uint64_t row_stride) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(a && local && p >= 1, "shard_gather_host: bad arguments");
+    const ShardLayout v = shard_layout(q, world, rank);
+    if (row_stride == 0) row_stride = v.row_len;
+    PFT_REQUIRE(row_stride >= v.row_len, "shard_gather_host: row_stride < row_len");
+    std::vector<uint64_t> g(v.row_len);
+    for (uint64_t c = 0; c < v.row_len; ++c) g[c] = v.global_col(q, c);
+#pragma omp parallel for schedule(static)
+    for (long long k = 0; k < static_cast<long long>(p); ++k)
+        for (uint64_t c = 0; c < v.row_len; ++c) local[k * row_stride + c] = a[k * q + g[c]];
     PFT_API_END
 }
 

@@ -96,6 +96,19 @@ struct HostPlan {
 HostPlan build_plan(const Table& t, uint64_t N, uint64_t M, int64_t mu, uint64_t p, double eps);
 std::string plan_json(const HostPlan& plan);
 
+// Contraction-axis layout of one rank's slice of A (see pft_shard_info in pft_capi.h).
+// Columns are owned in mirror pairs (l, q-l), l in [1, L), L = ceil(q/2); the unpaired
+// columns l = 0 and (even q) l = q/2 belong to rank 0.  world == 1 is the natural
+// layout (local column == global column).
+struct ShardLayout {
+    uint64_t pair_begin = 1, pair_end = 1;
+    uint64_t row_len = 0;
+    int64_t front_col = 0, mirror_col = 0, single0_col = -1, singleh_col = -1;
+    // global column of local column c (c < row_len)
+    uint64_t global_col(uint64_t q, uint64_t c) const;
+};
+ShardLayout shard_layout(uint64_t q, int world, int rank);
+
 }  // namespace pft::detail
 
 struct pft_table_s {

@@ -187,6 +187,48 @@ HostPlan build_plan(const Table& t, uint64_t N, uint64_t M, int64_t mu, uint64_t
     return P;
 }
 
+ShardLayout shard_layout(uint64_t q, int world, int rank) {
+    if (q == 0) fail(PFT_ERR_INVALID_ARGUMENT, "shard_layout: q must be >= 1");
+    if (world < 1 || rank < 0 || rank >= world) fail(PFT_ERR_INVALID_ARGUMENT, "shard_layout: bad world/rank");
+    const uint64_t L = (q + 1) / 2;  // pairs (l, q-l) for l in [1, L)
+    const uint64_t npairs = L - 1;
+    ShardLayout v;
+    if (world == 1) {
+        v.pair_begin = 1;
+        v.pair_end = L;
+        v.row_len = q;
+        v.front_col = 1;
+        v.mirror_col = static_cast<int64_t>(q) - 1;
+        v.single0_col = 0;
+        v.singleh_col = (q % 2 == 0) ? static_cast<int64_t>(q / 2) : -1;
+        return v;
+    }
+    const uint64_t base = npairs / world, extra = npairs % world, r = static_cast<uint64_t>(rank);
+    v.pair_begin = 1 + r * base + std::min<uint64_t>(r, extra);
+    v.pair_end = v.pair_begin + base + (r < extra ? 1 : 0);
+    const uint64_t n = v.pair_end - v.pair_begin;
+    // local row: [front: l ascending | mirror: q-l ascending in global order | singles (rank 0)]
+    v.front_col = 0;
+    v.mirror_col = static_cast<int64_t>(2 * n) - 1;  // mirror of pair_begin is the last mirror column
+    v.row_len = 2 * n;
+    if (rank == 0) {
+        v.single0_col = static_cast<int64_t>(v.row_len++);
+        if (q % 2 == 0) v.singleh_col = static_cast<int64_t>(v.row_len++);
+    }
+    return v;
+}
+
+uint64_t ShardLayout::global_col(uint64_t q, uint64_t c) const {
+    const int64_t ci = static_cast<int64_t>(c);
+    if (ci == single0_col) return 0;
+    if (ci == singleh_col) return q / 2;
+    const uint64_t n = pair_end - pair_begin;
+    if (front_col == 1 && row_len == q) return c;  // natural layout
+    if (c < n) return pair_begin + c;              // front
+    if (c < 2 * n) return q - (pair_begin + static_cast<uint64_t>(mirror_col - ci));  // mirror
+    fail(PFT_ERR_INVALID_ARGUMENT, "shard layout: local column out of range");
+}
+
 std::string plan_json(const HostPlan& P) {
     char buf[512];
     std::snprintf(buf, sizeof buf,

@@ -122,3 +122,31 @@ def test_device_generator_matches_host(pft):
     torch.cuda.synchronize()
     host = pft.generate_signal(pft.KIND_UNIFORM, 7, N, offset=123)
     assert np.array_equal(x.cpu().numpy(), host)  # bit-identical uniforms
+
+
+@pytest.mark.parametrize("N,M,mu,p,world", [
+    (2 ** 20, 64, 0, 2 ** 14, 2),
+    (2 ** 20, 256, 12345, 2 ** 13, 4),
+    (3 * 5 * 7 * 64, 20, 11, 3 * 5 * 64, 3),       # odd q = 7
+    (2 ** 22, 2 ** 9, 2 ** 20, 2 ** 13, 8),
+])
+def test_sharded_partials_sum_to_unsharded(pft, oracle, N, M, mu, p, world):
+    """Contraction-axis sharding (BASELINE configs[4] layout): each rank's K1 partial slab
+    over its column pairs, summed (what the NCCL reduce does), finalized by K2, equals the
+    unsharded transform.  Ranks run one after another on this GPU (no inter-kernel waits)."""
+    import torch
+    plan = pft.build_plan(N, M, mu, p, 1e-12)
+    d = plan.device_plan()
+    a = pft.generate_signal(pft.KIND_UNIFORM, 5, N)
+    slab = torch.zeros(plan.p * plan.r, dtype=torch.complex128, device="cuda")
+    part = torch.empty_like(slab)
+    for rank in range(world):
+        local = torch.from_numpy(pft.shard_gather(a, plan.p, plan.q, world, rank)).cuda()
+        d.execute_partial_ptr(local.data_ptr(), part.data_ptr(), world=world, rank=rank)
+        torch.cuda.synchronize()
+        slab += part
+    out = torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda")
+    d.finalize_ptr(slab.data_ptr(), out.data_ptr())
+    torch.cuda.synchronize()
+    ref = oracle.execute(plan, a)
+    assert rel_l2(out.cpu().numpy(), ref) <= GATE

@@ -19,7 +19,7 @@ def check(N, M, mu, p, p2=0, seed=1):
     a = pft.generate_signal(pft.KIND_UNIFORM, seed, N)
     x = torch.from_numpy(a).cuda()
     Y = torch.zeros(P1 * P2 * r, dtype=torch.complex128, device="cuda")
-    d.execute_partial_ptr(x.data_ptr(), 0, q, q, Y.data_ptr())
+    d.execute_partial_ptr(x.data_ptr(), Y.data_ptr())
     out = torch.zeros(2 * M + 1, dtype=torch.complex128, device="cuda")
     d.finalize_ptr(Y.data_ptr(), out.data_ptr())
     torch.cuda.synchronize()
