@@ -411,12 +411,13 @@ class DevicePlan:
     """A plan uploaded to one B200 (pft_dplan_t).  Device buffers are passed as raw
     pointers (e.g. torch.Tensor.data_ptr() of complex128 CUDA tensors)."""
 
-    def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0, k1_stages: int = 0):
+    def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0, k1_stages: int = 0, k2_mode: int = 0):
         self.plan = plan
         opts = _capi.DPlanOpts()
         opts.device = device
         opts.p2 = p2
         opts.k1_stages = k1_stages
+        opts.reserved[0] = k2_mode  # 0 auto, 1 fft, 2 dot, 3 direct (A/B testing)
         h = C.c_void_p()
         _check(lib().pft_dplan_create(plan.handle, C.byref(opts), C.byref(h)))
         self._h = h

@@ -87,20 +87,32 @@ __device__ __forceinline__ void dft3(double2& v0, double2& v1, double2& v2) {
     v2 = csub(m, r);
 }
 
-// One Stockham stage with a radix known at compile time (2, 3, 4, 8).
-template <int R, class TW>
+// One Stockham stage with a radix known at compile time (2, 3, 4, 8).  When n is a power
+// of two (POW2) the index arithmetic uses shifts/masks (lg_nb = log2(n/R), lg_ns =
+// log2(Ns)); otherwise integer division.
+template <int R, bool POW2, class TW>
 __device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__ src, double2* __restrict__ dst,
-                                                     int ncols, int n, int Ns, const TW& tw) {
+                                                     int ncols, int n, int Ns, int lg_nb, int lg_ns, const TW& tw) {
     const int nb = n / R;
     const uint32_t tstride = (uint32_t)(n / (Ns * R));
     for (int idx = threadIdx.x; idx < ncols * nb; idx += blockDim.x) {
-        const int col = idx / nb, j = idx - col * nb;
+        int col, j, k, base;
+        if constexpr (POW2) {
+            col = idx >> lg_nb;
+            j = idx & (nb - 1);
+            k = j & (Ns - 1);
+            base = ((j >> lg_ns) << lg_ns) * R + k;
+        } else {
+            col = idx / nb;
+            j = idx - col * nb;
+            k = j % Ns;
+            base = (j / Ns) * Ns * R + k;
+        }
         const double2* s = src + (size_t)col * n;
         double2* d = dst + (size_t)col * n;
         double2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = s[j + r * nb];
-        const int k = j % Ns;
         if (k != 0) {
 #pragma unroll
             for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw((uint32_t)(k * r) * tstride));
@@ -109,7 +121,6 @@ __device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__
         if constexpr (R == 3) dft3(v[0], v[1], v[2]);
         if constexpr (R == 4) dft4(v[0], v[1], v[2], v[3]);
         if constexpr (R == 8) dft8(v);
-        const int base = (j / Ns) * Ns * R + k;
 #pragma unroll
         for (int r = 0; r < R; ++r) d[base + r * Ns] = v[r];
     }
@@ -146,16 +157,29 @@ __device__ __forceinline__ double2* fft_columns(double2* x, double2* y, int ncol
                                                 const TW& tw) {
     double2* src = x;
     double2* dst = y;
-    int Ns = 1;
+    int Ns = 1, lg_ns = 0;
     const int n = plan.n;
+    const bool pow2 = (n & (n - 1)) == 0;
+    const int lg_n = 31 - __clz(n);
     for (int st = 0; st < plan.count; ++st) {
         const int R = plan.radix[st];
-        switch (R) {
-            case 2: stockham_stage_fixed<2>(src, dst, ncols, n, Ns, tw); break;
-            case 3: stockham_stage_fixed<3>(src, dst, ncols, n, Ns, tw); break;
-            case 4: stockham_stage_fixed<4>(src, dst, ncols, n, Ns, tw); break;
-            case 8: stockham_stage_fixed<8>(src, dst, ncols, n, Ns, tw); break;
-            default: stockham_stage_generic(src, dst, ncols, n, Ns, R, tw); break;
+        const int lg_r = R == 2 ? 1 : R == 4 ? 2 : 3;
+        const int lg_nb = lg_n - lg_r;
+        if (pow2) {
+            switch (R) {
+                case 2: stockham_stage_fixed<2, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw); break;
+                case 4: stockham_stage_fixed<4, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw); break;
+                default: stockham_stage_fixed<8, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw); break;
+            }
+            lg_ns += lg_r;
+        } else {
+            switch (R) {
+                case 2: stockham_stage_fixed<2, false>(src, dst, ncols, n, Ns, 0, 0, tw); break;
+                case 3: stockham_stage_fixed<3, false>(src, dst, ncols, n, Ns, 0, 0, tw); break;
+                case 4: stockham_stage_fixed<4, false>(src, dst, ncols, n, Ns, 0, 0, tw); break;
+                case 8: stockham_stage_fixed<8, false>(src, dst, ncols, n, Ns, 0, 0, tw); break;
+                default: stockham_stage_generic(src, dst, ncols, n, Ns, R, tw); break;
+            }
         }
         __syncthreads();
         double2* t = src;

@@ -14,18 +14,28 @@ namespace pftdev {
 // {Re phase_l, Im phase_l, t_l, 0}.  Two K1 CTAs share an SM.
 constexpr int K1_CONSUMER_WARPS = 8;
 constexpr int K1_THREADS = 32 * (K1_CONSUMER_WARPS + 1);
-constexpr int K1_BR = 16;          // rows per box (2 per consumer warp, 16 lanes per row)
-constexpr int K1_CP = 32;          // column pairs per chunk
-constexpr int K1_LANES_PER_ROW = 16;
-constexpr uint32_t K1_BOX_BYTES = K1_BR * K1_CP * 16;  // 8 KiB
-constexpr uint32_t K1_TAB_BYTES = K1_CP * 32;           // 1 KiB
+#ifndef PFT_K1_BR
+#define PFT_K1_BR 32
+#endif
+#ifndef PFT_K1_CP
+#define PFT_K1_CP 16
+#endif
+constexpr int K1_BR = PFT_K1_BR;   // rows per box
+constexpr int K1_CP = PFT_K1_CP;   // column pairs per chunk
+constexpr int K1_LANES_PER_ROW = 32 * K1_CONSUMER_WARPS / K1_BR;  // consumer lanes sharing a row
+constexpr uint32_t K1_BOX_BYTES = K1_BR * K1_CP * 16;
+constexpr uint32_t K1_TAB_BYTES = K1_CP * 32;
 constexpr uint32_t K1_STAGE_BYTES = 2 * K1_BOX_BYTES + K1_TAB_BYTES;
-constexpr int K1_MIN_STAGES = 4, K1_MAX_STAGES = 8;
+#ifndef PFT_K1_MIN_STAGES
+#define PFT_K1_MIN_STAGES 4
+#endif
+constexpr int K1_MIN_STAGES = PFT_K1_MIN_STAGES, K1_MAX_STAGES = 8;
 constexpr size_t K1_MIN_RING_BYTES = (size_t)K1_MIN_STAGES * K1_STAGE_BYTES;
-static_assert(K1_BR == K1_CONSUMER_WARPS * (32 / K1_LANES_PER_ROW), "one row per half-warp");
+static_assert(K1_LANES_PER_ROW >= 1 && K1_LANES_PER_ROW <= 32 && K1_CP % K1_LANES_PER_ROW == 0, "row mapping");
 static_assert(K1_STAGE_BYTES % 128 == 0, "TMA destinations stay 128-byte aligned");
 
 constexpr int K2_THREADS = 256;
+enum K2Mode { K2_DIRECT = 0, K2_FFT = 1, K2_DOT = 2 };
 
 // Pair-table entry (host-built): phase_l = e^{-2 pi i mu (l - q/2)/N} and t_l = 1 - 2l/q.
 // The mirror column q-l uses conj(phase_l) and -t_l (exact identities of SPEC.md:126).
@@ -63,7 +73,7 @@ struct K2Params {
     uint64_t W;                    // 2M + 1
     uint64_t first_mod_p;          // (mu - M) mod p
     uint32_t first_mod_p1;         // (mu - M) mod P1
-    int use_fft;                   // k2_fft_post (1) or k2_direct_post (0)
+    int mode;                      // K2_DIRECT / K2_FFT / K2_DOT
     FftRadices fft2;               // radices of P2
     double2* out;                  // [batch][W]
     int* status;
@@ -94,6 +104,8 @@ inline uint32_t k1_pick_stages(int r, uint32_t P1) {
 }
 // Z + scratch (r x P2 each) + omega_P2 + four-step twiddles (P2 each)
 inline size_t k2_smem_bytes(int r, uint32_t P2) { return sizeof(double2) * (2 * (size_t)r * P2 + 2 * (size_t)P2); }
+// Z (r x P2) + omega_P2 + four-step twiddles
+inline size_t k2_dot_smem_bytes(int r, uint32_t P2) { return sizeof(double2) * ((size_t)r * P2 + 2 * (size_t)P2); }
 
 cudaError_t configure_k1(int r, uint32_t P1, bool mu0);
 cudaError_t configure_k2(int r, uint32_t P2);

@@ -109,7 +109,7 @@ struct pft_dplan_s {
     pftdev::FftRadices fft{};   // radices of P1 (K1)
     pftdev::FftRadices fft2{};  // radices of P2 (K2)
     uint32_t k1_stages = pftdev::K1_MIN_STAGES;
-    bool k2_fft = false;
+    int k2_mode = pftdev::K2_DIRECT;
     bool mu0 = false;
     uint64_t W = 0;
     // device allocations
@@ -175,7 +175,7 @@ struct pft_dplan_s {
         const int64_t first = host.mu - (int64_t)host.M;
         P.first_mod_p = mod_index(first, host.p);
         P.first_mod_p1 = (uint32_t)mod_index(first, P1);
-        P.use_fft = k2_fft ? 1 : 0;
+        P.mode = k2_mode;
         P.fft2 = fft2;
         P.out = out;
         P.status = d_status;
@@ -300,10 +300,22 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         fail(PFT_ERR_UNSUPPORTED, "dplan_create: P1 * r too large for K1 shared memory; choose a larger p2");
     d->k1_stages = (opts && opts->k1_stages) ? (uint32_t)opts->k1_stages : pftdev::k1_pick_stages(H.r, (uint32_t)d->P1);
     PFT_REQUIRE(d->k1_stages >= (uint32_t)pftdev::K1_MIN_STAGES && d->k1_stages <= (uint32_t)pftdev::K1_MAX_STAGES, "dplan_create: k1_stages out of [4, 8]");
-    d->k2_fft = k2_fft_feasible(d->P2, H.r);
-    if (d->k2_fft) {
-        if (d->P2 > 1) factor_radices((uint32_t)d->P2, d->fft2);
-        else d->fft2.n = 1;
+    // K2 form: length-P2 FFT when it fits shared memory (fastest measured), else the dot form,
+    // else the direct global form.
+    {
+        const bool fft_ok = k2_fft_feasible(d->P2, H.r);
+        const bool dot_ok = pftdev::k2_dot_smem_bytes(H.r, (uint32_t)d->P2) <= kK2SmemLimit;
+        const int forced = opts ? opts->reserved[0] : 0;  // 1 fft, 2 dot, 3 direct (A/B testing)
+        if (forced == 1 && fft_ok) d->k2_mode = pftdev::K2_FFT;
+        else if (forced == 2 && dot_ok) d->k2_mode = pftdev::K2_DOT;
+        else if (forced == 3) d->k2_mode = pftdev::K2_DIRECT;
+        else if (fft_ok) d->k2_mode = pftdev::K2_FFT;  // measured faster than dot at C2b/C4
+        else if (dot_ok) d->k2_mode = pftdev::K2_DOT;
+        else d->k2_mode = pftdev::K2_DIRECT;
+        if (d->k2_mode == pftdev::K2_FFT) {
+            if (d->P2 > 1) factor_radices((uint32_t)d->P2, d->fft2);
+            else d->fft2.n = 1;
+        }
     }
     d->mu0 = std::all_of(H.phase.begin(), H.phase.end(), [](const cplx& z) { return z == cplx(1.0, 0.0); });
 
@@ -346,7 +358,7 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     cuda_check(cudaMalloc(&d->d_status, sizeof(int)), "cudaMalloc(status)");
     cuda_check(cudaMemset(d->d_status, 0, sizeof(int)), "cudaMemset(status)");
     cuda_check(pftdev::configure_k1(H.r, (uint32_t)d->P1, d->mu0), "configure K1");
-    if (d->k2_fft) cuda_check(pftdev::configure_k2(H.r, (uint32_t)d->P2), "configure K2");
+    cuda_check(pftdev::configure_k2(H.r, (uint32_t)d->P2), "configure K2");
     *out = d.release();
     PFT_API_END
 }

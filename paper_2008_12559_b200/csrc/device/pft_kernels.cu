@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     } else {
         // ---- consumers: half-warp per row, lane li takes pairs li and li + 16 of each chunk
         const int li = lane & (K1_LANES_PER_ROW - 1);
-        const int rin = warp * 2 + (lane >> 4);  // row within the box
+        const int rin = (warp * 32 + lane) / K1_LANES_PER_ROW;  // row within the box
         for (uint32_t rb = 0; rb < nrb; ++rb) {
             double are[R], aim[R];
 #pragma unroll
@@ -113,9 +113,13 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
 #pragma unroll
                 for (int u = 0; u < K1_CP / K1_LANES_PER_ROW; ++u) {
                     const int i = li + u * K1_LANES_PER_ROW;
-                    if ((uint32_t)i < valid) {
-                        const double2 x1 = front[i];                   // column l
-                        const double2 x2 = mirror[K1_CP - 1 - i];      // column q - l
+                    // branch-free masking of pairs past the end of the view (keeps the
+                    // independent pairs in one basic block so their chains interleave)
+                    const bool ok = (uint32_t)i < valid;
+                    {
+                        const double2 z = make_double2(0.0, 0.0);
+                        const double2 x1 = ok ? front[i] : z;               // column l
+                        const double2 x2 = ok ? mirror[K1_CP - 1 - i] : z;  // column q - l
                         const double2 cs = *reinterpret_cast<const double2*>(&tab[i].c);
                         const double t = tab[i].t;
                         const double2 su = make_double2(x1.x + x2.x, x1.y + x2.y);
@@ -130,6 +134,9 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                         }
                         are[0] += Sv.x;
                         aim[0] += Sv.y;
+#ifdef PFT_DBG_NOCOMPUTE
+                        continue;
+#endif
                         double tp = t;
 #pragma unroll
                         for (int j = 1; j < R; ++j) {
@@ -181,7 +188,9 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     // First FFT pass over k1 (length P1) for every column j, in shared memory; the ring is
     // idle now and serves as the Stockham scratch buffer.
     const double2* res = Cs;
+#ifndef PFT_DBG_NOFFT
     if (P.P1 > 1) res = fft_columns(Cs, reinterpret_cast<double2*>(ring), R, P.fft, SmemTwiddles{tw1});
+#endif
     // Y[b][m1][c][j]: the slab for one m1 is contiguous over (c, j) for K2.
     double2* __restrict__ Y = P.Y + (size_t)b * P.P1 * P.P2 * R;
     for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) {
@@ -191,6 +200,32 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
 }
 
 // ----------------------------------------------------------------------------- K2
+
+// Z[j][c] = omega_p^{m1 c} Y[c][j] for the CTA's m1 slab: all of a thread's loads are
+// issued before any is consumed (the slab comes from L2 right after K1; a dependent
+// load per iteration made K2's time grow with r).
+template <int R>
+__device__ __forceinline__ void load_twiddled_slab(const double2* __restrict__ Y, uint32_t P2, uint32_t m1,
+                                                   const double2* pre, double2* Z) {
+    constexpr int U = 8;
+    const uint32_t n = P2 * (uint32_t)R;
+    for (uint32_t base = threadIdx.x; base < n; base += U * blockDim.x) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t idx = base + u * blockDim.x;
+            v[u] = idx < n ? Y[idx] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t idx = base + u * blockDim.x;
+            if (idx < n) {
+                const uint32_t c = idx / R, j = idx - c * R;
+                Z[(size_t)j * P2 + c] = (m1 == 0 || c == 0) ? v[u] : cmul(v[u], pre[c]);
+            }
+        }
+    }
+}
 
 template <int R>
 __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
@@ -220,11 +255,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     const double2* __restrict__ Y = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
-    for (uint32_t idx = threadIdx.x; idx < P.P2 * (uint32_t)R; idx += blockDim.x) {
-        const uint32_t c = idx / R, j = idx - c * R;
-        const double2 y = Y[idx];
-        Z[(size_t)j * P.P2 + c] = (m1 == 0 || c == 0) ? y : cmul(y, pre[c]);
-    }
+    load_twiddled_slab<R>(Y, P.P2, m1, pre, Z);
     __syncthreads();
     const double2* res = Z;
     if (P.P2 > 1) res = fft_columns(Z, scratch, R, P.fft2, SmemTwiddles{tw2});
@@ -245,6 +276,72 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
         const double2 v = cmul(acc, first ? ptw0 : __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
         out[s] = v;
         if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
+    }
+}
+
+// K2 (dot form, few outputs per m1): only the ~W/P1 bins this CTA owns are needed, so
+// instead of the full length-P2 FFT each warp evaluates
+//   out[s] = e^{-pi i m/p} sum_c omega_P2^{m2 c} (sum_j Z[j][c] ((m - mu)/p)^j)
+// directly from the twiddled slab Z in shared memory: one barrier instead of one per FFT
+// stage.  Lane-strided partial sums + xor-butterfly keep the order fixed.
+template <int R>
+__global__ void __launch_bounds__(K2_THREADS) k2_dot_post(K2Params P) {
+    extern __shared__ __align__(16) double2 zs[];
+    double2* Z = zs;                           // [R][P2]
+    double2* tw2 = zs + (size_t)R * P.P2;      // omega_P2^t
+    double2* pre = tw2 + P.P2;                 // omega_p^{m1 c}
+    const uint32_t m1 = blockIdx.x, b = blockIdx.y;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = K2_THREADS / 32;
+    const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
+    if (s0 >= P.W) return;  // block-uniform
+    // ---- prologue (overlaps K1's tail under PDL): twiddle tables and this warp's first powers
+    for (uint32_t c = threadIdx.x; c < P.P2; c += blockDim.x) {
+        tw2[c] = __ldg(P.omega + (size_t)c * P.P1);
+        pre[c] = __ldg(P.omega + (size_t)m1 * c);
+    }
+    const uint64_t s_first = s0 + (uint64_t)P.P1 * warp;
+    double pw0[R];
+    if (s_first < P.W) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) pw0[j] = __ldg(P.post_powers + s_first * R + j);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __syncthreads();
+    const double2* __restrict__ Y = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
+    load_twiddled_slab<R>(Y, P.P2, m1, pre, Z);
+    __syncthreads();
+    const bool p2_pow2 = (P.P2 & (P.P2 - 1)) == 0;
+    double2* __restrict__ out = P.out + (size_t)b * P.W;
+    for (uint64_t s = s_first; s < P.W; s += (uint64_t)P.P1 * NW) {
+        uint64_t mp = P.first_mod_p + s % P.p;
+        if (mp >= P.p) mp -= P.p;
+        const uint32_t m2 = (uint32_t)(mp / P.P1);
+        double pw[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) pw[j] = (s == s_first) ? pw0[j] : __ldg(P.post_powers + s * R + j);
+        double2 acc = make_double2(0.0, 0.0);
+        for (uint32_t c = lane; c < P.P2; c += 32) {
+            double2 S = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < R; ++j) {  // ascending j
+                const double2 z = Z[(size_t)j * P.P2 + c];
+                S.x = fma(z.x, pw[j], S.x);
+                S.y = fma(z.y, pw[j], S.y);
+            }
+            const uint32_t e = p2_pow2 ? ((m2 * c) & (P.P2 - 1)) : (uint32_t)(((uint64_t)m2 * c) % P.P2);
+            acc = cadd(acc, cmul(S, tw2[e]));  // omega_P2^{m2 c}
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+        }
+        if (lane == 0) {
+            const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+            out[s] = v;
+            if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
+        }
     }
 }
 
@@ -360,20 +457,23 @@ static cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(K2_THREADS);
-    cfg.dynamicSmemBytes = P.use_fft ? k2_smem_bytes(R, P.P2) : 0;
+    cfg.dynamicSmemBytes = P.mode == K2_FFT ? k2_smem_bytes(R, P.P2) : P.mode == K2_DOT ? k2_dot_smem_bytes(R, P.P2) : 0;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (P.use_fft) return cudaLaunchKernelEx(&cfg, k2_fft_post<R>, P);
+    if (P.mode == K2_FFT) return cudaLaunchKernelEx(&cfg, k2_fft_post<R>, P);
+    if (P.mode == K2_DOT) return cudaLaunchKernelEx(&cfg, k2_dot_post<R>, P);
     return cudaLaunchKernelEx(&cfg, k2_direct_post<R>, P);
 }
 
 template <int R>
 static cudaError_t configure_k2_r(size_t smem) {
-    return cudaFuncSetAttribute(k2_fft_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = cudaFuncSetAttribute(k2_fft_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k2_dot_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 // The attribute is only a cap (the launch's dynamic size decides occupancy), so set it to

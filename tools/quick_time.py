@@ -32,9 +32,9 @@ def graph_time(fn, reps, stream):
     return e0.elapsed_time(e1) / reps
 
 
-def time_plan(N, M, mu, p, p2=0, stages=0, reps=200, label=""):
+def time_plan(N, M, mu, p, p2=0, stages=0, reps=200, label="", k2_mode=0):
     plan = pft.build_plan(N, M, mu, p, 1e-12)
-    d = pft.DevicePlan(plan, p2=p2, k1_stages=stages)
+    d = pft.DevicePlan(plan, p2=p2, k1_stages=stages, k2_mode=k2_mode)
     bufs = [torch.empty(N, dtype=torch.complex128, device="cuda") for _ in range(2)]
     for i, b in enumerate(bufs):
         pft.generate_signal_device(b.data_ptr(), pft.KIND_UNIFORM, 1 + i, N)
@@ -44,7 +44,26 @@ def time_plan(N, M, mu, p, p2=0, stages=0, reps=200, label=""):
     sp = s.cuda_stream
     ms = graph_time(lambda i: d.execute_ptr(bufs[i % 2].data_ptr(), out.data_ptr(), stream=sp), reps, s)
     k1 = graph_time(lambda i: d.execute_partial_ptr(bufs[i % 2].data_ptr(), Y.data_ptr(), stream=sp), reps, s)
-    print(json.dumps({"label": label, "N": N, "M": M, "p": plan.p, "q": plan.q, "r": plan.r, "P1": d.P1,
+    # K2 alone (finalize of the same slab), and a 2-stream pipeline of independent transforms
+    k2 = graph_time(lambda i: d.finalize_ptr(Y.data_ptr(), out.data_ptr(), stream=sp), reps, s)
+    s2 = torch.cuda.Stream()
+    ws = [torch.empty(plan.p * plan.r, dtype=torch.complex128, device="cuda") for _ in range(2)]
+    outs = [torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda") for _ in range(2)]
+    ev = [torch.cuda.Event() for _ in range(2)]
+
+    def two_stream(i):
+        # fork s2 from s at the start of a pair, join back at the end (graph-capturable)
+        if i % 2 == 0:
+            ev[0].record(s)
+            s2.wait_event(ev[0])
+        st = s if i % 2 == 0 else s2
+        d.execute_ptr(bufs[i % 2].data_ptr(), outs[i % 2].data_ptr(), d_ws=ws[i % 2].data_ptr(),
+                      stream=st.cuda_stream)
+        if i % 2 == 1:
+            ev[1].record(s2)
+            s.wait_event(ev[1])
+    ms2 = graph_time(two_stream, reps, s)
+    print(json.dumps({"label": label, "k2_us": round(k2 * 1e3, 2), "pipelined_us": round(ms2 * 1e3, 2), "N": N, "M": M, "p": plan.p, "q": plan.q, "r": plan.r, "P1": d.P1,
                       "P2": d.P2, "stages": stages, "us": round(ms * 1e3, 2), "k1_us": round(k1 * 1e3, 2),
                       "GB/s": round(16 * N / (ms * 1e-3) / 1e9, 1),
                       "k1_GB/s": round(16 * N / (k1 * 1e-3) / 1e9, 1)}), flush=True)
@@ -53,6 +72,16 @@ def time_plan(N, M, mu, p, p2=0, stages=0, reps=200, label=""):
 if __name__ == "__main__":
     import os
     which = os.environ.get("QT", "main")
+    if which == "k2":
+        for mode in (1, 2, 3):
+            time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label=f"C2b k2_mode={mode}", k2_mode=mode)
+            time_plan(2 ** 24, 2 ** 14, 2 ** 22, 2 ** 16, label=f"C2c k2_mode={mode}", k2_mode=mode)
+            time_plan(6220800, 1000, -12345, 62208, label=f"C4 k2_mode={mode}", k2_mode=mode)
+    if which == "k1":
+        time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label="C2b p=2^15")
+        time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 14, label="C2b p=2^14")
+        time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 16, label="C2b p=2^16")
+        time_plan(2 ** 24, 0, 2 ** 22, 2 ** 15, label="C2b-shape r=1")
     if which == "main":
         time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label="C2b p=2^15")
         time_plan(2 ** 24, 0, 2 ** 22, 2 ** 15, label="C2b-shape r=1 (memory-pattern ceiling)")
