@@ -330,7 +330,7 @@ double oracle_certify(const oracle_c128* w, int r, double xi, double u) {
         probe(0.0L);
         return static_cast<double>(worst);
     }
-    const long n = 4096L * r;
+    const long n = 4096L * r + 1;  // symmetric grid including x = 0
     for (long i = 0; i < n; ++i) probe(-X + 2.0L * X * i / (n - 1));
     for (int k = 0; k < 8 * r; ++k) probe(X * cosl(PI_L * (2.0L * k + 1.0L) / (16.0L * r)));
     return static_cast<double>(worst);

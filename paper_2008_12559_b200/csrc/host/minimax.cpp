@@ -101,7 +101,7 @@ double certify(const std::vector<cplx>& coeffs, double xi, double u) {
         const long double e = std::abs(eval_poly_l(coeffs, x) - target);
         if (e > worst || std::isnan(static_cast<double>(e))) worst = std::isnan((double)e) ? INFINITY : e;
     };
-    const long n_eq = 4096L * r;
+    const long n_eq = 4096L * r + 1;  // odd and symmetric: includes x = 0
     for (long i = 0; i < n_eq; ++i) {
         const long double x = -X + 2.0L * X * static_cast<long double>(i) / static_cast<long double>(n_eq - 1);
         probe(x);

@@ -1,0 +1,79 @@
+"""Multi-GPU execution of one huge transform (BASELINE.json configs[4]: N = 2^30 split along
+the contraction axis over 2/4/8 B200s) and batch sharding (configs[2]).
+
+One process per GPU (torchrun); torch.distributed is the plumbing (NCCL over NVLink on GPUs,
+gloo in the CPU tests).  For a single transform each rank owns, for every row k of A, the
+column pairs of pft_shard_layout(q, world, rank); the only exchange is one reduction of the
+p x r partial slab (8.4 MB at p = 2^16, r = 8 -- SURVEY.md §8(e)):
+
+    K1 (local slice) -> dist.reduce(slab, SUM, dst=root) -> K2 on root
+
+The slab is the K1 output Y (the contraction fused with the first FFT pass); both steps are
+linear, so the sum over ranks of the partial slabs equals the unsharded slab.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import PftPlan, ShardLayout, shard_gather, shard_layout
+
+
+class ShardedTransform:
+    """Contraction-axis sharded execute of `plan` on this rank."""
+
+    def __init__(self, plan: PftPlan, world: int, rank: int, root: int = 0, group=None, device: int = 0,
+                 p2: int = 0):
+        self.plan, self.world, self.rank, self.root, self.group = plan, world, rank, root, group
+        self.layout: ShardLayout = shard_layout(plan.q, world, rank)
+        self.device = device
+        self._p2 = p2
+        self._dplan = None
+
+    # --------------------------------------------------------------- host helpers
+    def gather_local(self, a) -> np.ndarray:
+        """This rank's slice (p x row_len) of the global signal, in the shard layout."""
+        return shard_gather(a, self.plan.p, self.plan.q, self.world, self.rank)
+
+    def slab_elems(self) -> int:
+        return self.plan.p * self.plan.r
+
+    # --------------------------------------------------------------- device steps
+    @property
+    def dplan(self):
+        if self._dplan is None:
+            from . import DevicePlan
+            self._dplan = DevicePlan(self.plan, device=self.device, p2=self._p2)
+        return self._dplan
+
+    def partial(self, d_local: int, d_slab: int, stream: int = 0) -> None:
+        """K1 on the local slice: writes this rank's partial slab (p*r complex128)."""
+        self.dplan.execute_partial_ptr(d_local, d_slab, world=self.world, rank=self.rank,
+                                       row_stride=self.layout.row_len, stream=stream)
+
+    def reduce(self, slab) -> None:
+        """Sum the partial slabs onto the root (torch tensor, complex128, any backend)."""
+        import torch
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.reduce(torch.view_as_real(slab), dst=self.root, op=dist.ReduceOp.SUM, group=self.group)
+
+    def finalize(self, d_slab: int, d_out: int, stream: int = 0) -> None:
+        """K2 on the root: the remaining FFT pass + Eq. (7) post-process."""
+        if self.rank == self.root:
+            self.dplan.finalize_ptr(d_slab, d_out, stream=stream)
+
+    def execute(self, local, slab, out) -> None:
+        """Full sharded transform on CUDA tensors: local (p*row_len), slab (p*r), out (2M+1)."""
+        import torch
+        stream = torch.cuda.current_stream().cuda_stream
+        self.partial(local.data_ptr(), slab.data_ptr(), stream)
+        self.reduce(slab)
+        self.finalize(slab.data_ptr(), out.data_ptr(), stream)
+
+
+def batch_shard(n_signals: int, world: int, rank: int) -> tuple[int, int]:
+    """Signals [start, start + count) of rank `rank` when a batch is sharded by signal
+    (BASELINE configs[2]); contiguous near-equal split, no communication."""
+    base, extra = divmod(n_signals, world)
+    start = rank * base + min(rank, extra)
+    return start, base + (1 if rank < extra else 0)
