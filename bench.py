@@ -195,7 +195,7 @@ def run_ours(args):
     N, M, mu, p, kind, desc = CONFIGS[args.config]
     W = 2 * M + 1
     plan = pft.build_plan(N, M, mu, p, EPS)
-    d = pft.DevicePlan(plan, device=local, p2=args.p2)
+    d = pft.DevicePlan(plan, device=local, p2=args.p2, pdl=not args.no_pdl, fuse=args.fuse)
     launches = d.launches_per_execute()
 
     # inputs: >= 2 buffers, together > 2x L2, rotated so no step re-reads a cached input
@@ -210,7 +210,8 @@ def run_ours(args):
     # output (pft_execute is re-entrant on distinct (stream, workspace) pairs), so one
     # transform's K2 and K1 FFT tail overlap the next transform's streaming K1.
     side = torch.cuda.Stream(device=dev)
-    ws = [torch.empty(plan.p * plan.r, dtype=torch.complex128, device=dev) for _ in range(2)]
+    ws_elems = -(-d.workspace_bytes(1) // 16)
+    ws = [torch.zeros(ws_elems, dtype=torch.complex128, device=dev) for _ in range(2)]  # zeroed once
     outs = [out, torch.empty(W, dtype=torch.complex128, device=dev)]
     fork, join = torch.cuda.Event(), torch.cuda.Event()
 
@@ -331,9 +332,11 @@ def run_ours(args):
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "l2": f"{nbuf} rotating inputs of {16 * N / 2**20:.0f} MiB (> L2 126 MiB)",
                        "timing": "CUDA graph of K steps, CUDA events on the launch stream",
-                       "streams": args.streams,
+                       "streams": args.streams, "pdl": not args.no_pdl, "fused_k2": args.fuse,
                        "pipelining": "independent transforms alternate over 2 streams with separate "
-                                     "workspaces" if args.streams == 2 else "none"},
+                                     "workspaces" if args.streams == 2 else
+                                     "single stream; K1 of transform i+1 overlaps K2 of transform i via "
+                                     "programmatic dependent launch"},
             "latency_us_single_stream": latency_us,
             "input_gbs": value * 16 * N / 1e9,
             "input_gbs_frac_of_peak": value * 16 * N / 1e9 / world / peak,
@@ -362,8 +365,11 @@ def main():
     ap.add_argument("--config", default="c2b", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--p2", type=int, default=0, help="override K1 residue classes (0 = planner)")
-    ap.add_argument("--streams", type=int, default=2, choices=[1, 2],
-                    help="2 = pipeline independent transforms over two streams (default)")
+    ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
+                    help="1 (default): one stream; consecutive transforms overlap through programmatic "
+                         "dependent launch (K2 releases the next K1).  2: alternate two streams")
+    ap.add_argument("--no-pdl", action="store_true", help="plain stream order between kernels")
+    ap.add_argument("--fuse", action="store_true", help="fuse K2 into K1's tail (grid barrier)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

@@ -153,7 +153,8 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
 void pft_dplan_destroy(pft_dplan_t d);
 /* Chosen decomposition p = P1 * P2 (P1 = local FFT length per residue class). */
 pft_status pft_dplan_layout(pft_dplan_t d, uint64_t* p1, uint64_t* p2);
-/* Device workspace bytes for `batch` independent transforms. */
+/* Device workspace bytes for `batch` independent transforms (zero it once before first use;
+ * the library leaves it in a reusable state). */
 pft_status pft_workspace_bytes(pft_dplan_t d, size_t batch, size_t* bytes);
 /* Bytes of one partial slab (the reducible intermediate, p*r complex128 per transform). */
 pft_status pft_partial_bytes(pft_dplan_t d, size_t batch, size_t* bytes);

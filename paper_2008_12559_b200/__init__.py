@@ -411,13 +411,17 @@ class DevicePlan:
     """A plan uploaded to one B200 (pft_dplan_t).  Device buffers are passed as raw
     pointers (e.g. torch.Tensor.data_ptr() of complex128 CUDA tensors)."""
 
-    def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0, k1_stages: int = 0, k2_mode: int = 0):
+    def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0, k1_stages: int = 0, k2_mode: int = 0,
+                 k2_ctas: int = 0, pdl: bool = True, fuse: bool = False):
         self.plan = plan
         opts = _capi.DPlanOpts()
         opts.device = device
         opts.p2 = p2
         opts.k1_stages = k1_stages
-        opts.reserved[0] = k2_mode  # 0 auto, 1 fft, 2 dot, 3 direct (A/B testing)
+        opts.reserved[0] = k2_mode  # 0 auto, 1 fft, 2 dot, 3 direct, 4 l2, 5 sum tail (A/B testing)
+        opts.reserved[1] = k2_ctas  # K2 grid width for the L2 form (0 = default)
+        opts.reserved[2] = 0 if pdl else 1  # PDL chaining of consecutive transforms
+        opts.reserved[3] = 2 if fuse else 0  # K2 fused into K1's tail (grid barrier, opt-in)
         h = C.c_void_p()
         _check(lib().pft_dplan_create(plan.handle, C.byref(opts), C.byref(h)))
         self._h = h

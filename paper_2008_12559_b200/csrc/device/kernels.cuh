@@ -35,7 +35,26 @@ static_assert(K1_LANES_PER_ROW >= 1 && K1_LANES_PER_ROW <= 32 && K1_CP % K1_LANE
 static_assert(K1_STAGE_BYTES % 128 == 0, "TMA destinations stay 128-byte aligned");
 
 constexpr int K2_THREADS = 256;
-enum K2Mode { K2_DIRECT = 0, K2_FFT = 1, K2_DOT = 2 };
+constexpr int K2L_THREADS = 128;
+enum K2Mode { K2_DIRECT = 0, K2_FFT = 1, K2_DOT = 2, K2_L2 = 3, K2_SUM = 4 };
+
+struct K2Params {
+    const double2* Y;              // [batch][P1][P2][r]
+    const double* post_powers;     // [W][r]
+    const double2* post_twiddles;  // [W]
+    const double2* omega;          // [p]
+    uint64_t p;
+    uint32_t P1, P2;
+    uint64_t W;                    // 2M + 1
+    uint64_t first_mod_p;          // (mu - M) mod p
+    uint32_t first_mod_p1;         // (mu - M) mod P1
+    int mode;                      // K2_DIRECT / K2_FFT / K2_DOT
+    uint32_t k2_ctas;              // K2_L2 grid width (0 = 148)
+    int release_next;              // trigger the next launch at K2 start (PDL chaining)
+    FftRadices fft2;               // radices of P2
+    double2* out;                  // [batch][W]
+    int* status;
+};
 
 // Pair-table entry (host-built): phase_l = e^{-2 pi i mu (l - q/2)/N} and t_l = 1 - 2l/q.
 // The mirror column q-l uses conj(phase_l) and -t_l (exact identities of SPEC.md:126).
@@ -60,24 +79,14 @@ struct K1Params {
     uint32_t P1, P2;            // p = P1 * P2
     FftRadices fft;             // radices of P1
     uint32_t stages;            // ring depth (K1_MIN_STAGES..K1_MAX_STAGES)
-    double2* Y;                 // [batch][P1][P2][r]
+    int pdl;                    // launched with programmatic stream serialization
+    double2* Y;                 // [batch][P1][P2][r] slab, or [batch][W][P2] partial sums (sum_tail)
+    int sum_tail;               // write per-output partial sums S'_c(s) instead of the slab
+    int fused;                  // run K2 in K1's tail behind a grid barrier (cooperative launch)
+    unsigned* bar;              // grid-barrier state {count, generation} (workspace tail, zeroed once)
+    K2Params k2;                // K2 parameters for the fused tail
 };
 
-struct K2Params {
-    const double2* Y;              // [batch][P1][P2][r]
-    const double* post_powers;     // [W][r]
-    const double2* post_twiddles;  // [W]
-    const double2* omega;          // [p]
-    uint64_t p;
-    uint32_t P1, P2;
-    uint64_t W;                    // 2M + 1
-    uint64_t first_mod_p;          // (mu - M) mod p
-    uint32_t first_mod_p1;         // (mu - M) mod P1
-    int mode;                      // K2_DIRECT / K2_FFT / K2_DOT
-    FftRadices fft2;               // radices of P2
-    double2* out;                  // [batch][W]
-    int* status;
-};
 
 struct GenParams {
     int kind;
@@ -108,6 +117,8 @@ inline size_t k2_smem_bytes(int r, uint32_t P2) { return sizeof(double2) * (2 * 
 inline size_t k2_dot_smem_bytes(int r, uint32_t P2) { return sizeof(double2) * ((size_t)r * P2 + 2 * (size_t)P2); }
 
 cudaError_t configure_k1(int r, uint32_t P1, bool mu0);
+int k1_max_active_per_sm(int r, uint32_t P1, uint32_t stages, bool mu0);
+constexpr size_t kBarrierBytes = 256;  // grid-barrier words at the end of a workspace
 cudaError_t configure_k2(int r, uint32_t P2);
 cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t batch, bool mu0, cudaStream_t st);
 cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st);

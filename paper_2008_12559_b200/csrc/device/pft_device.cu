@@ -110,6 +110,11 @@ struct pft_dplan_s {
     pftdev::FftRadices fft2{};  // radices of P2 (K2)
     uint32_t k1_stages = pftdev::K1_MIN_STAGES;
     int k2_mode = pftdev::K2_DIRECT;
+    uint32_t k2_ctas = 0;
+    bool pdl_chain = true;  // K2 releases the next K1 early (programmatic dependent launch)
+    bool allow_fuse = false; // K2 fused into K1's tail (opt-in; measured slower at C2b/C4)
+    bool sum_tail = false;   // unsharded execute: K1 writes per-output partial sums, K2 = sum form
+    uint64_t k1_capacity = 0;  // co-resident K1 CTAs on the device
     bool mu0 = false;
     uint64_t W = 0;
     // device allocations
@@ -136,6 +141,15 @@ struct pft_dplan_s {
     }
 
     size_t slab_elems() const { return (size_t)host.p * host.r; }
+    size_t workspace_bytes(size_t batch) const {
+        const size_t per = sum_tail ? std::max<size_t>(slab_elems(), (size_t)W * P2) : slab_elems();
+        return per * sizeof(double2) * batch + pftdev::kBarrierBytes;
+    }
+    bool fused(size_t batch) const {
+        return allow_fuse && !sum_tail && k2_mode == pftdev::K2_FFT &&
+               pftdev::k2_smem_bytes(host.r, (uint32_t)P2) <= (size_t)k1_stages * pftdev::K1_STAGE_BYTES &&
+               P2 * batch <= k1_capacity;
+    }
 
     pftdev::K1Params k1_params(const ShardLayout& v, const double2* a, uint64_t row_stride, size_t batch_stride,
                                double2* Y) const {
@@ -158,6 +172,7 @@ struct pft_dplan_s {
         P.P2 = (uint32_t)P2;
         P.fft = fft;
         P.stages = k1_stages;
+        P.pdl = pdl_chain ? 1 : 0;
         P.Y = Y;
         return P;
     }
@@ -176,6 +191,8 @@ struct pft_dplan_s {
         P.first_mod_p = mod_index(first, host.p);
         P.first_mod_p1 = (uint32_t)mod_index(first, P1);
         P.mode = k2_mode;
+        P.k2_ctas = k2_ctas;
+        P.release_next = pdl_chain ? 1 : 0;
         P.fft2 = fft2;
         P.out = out;
         P.status = d_status;
@@ -237,13 +254,29 @@ CUtensorMap make_input_map(const pft_dplan_s* d, const void* base, uint64_t row_
     return map;
 }
 
+// Y: workspace of workspace_bytes(batch) (slab then the zero-initialised barrier words).
 void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stride, double2* out, double2* Y,
                  cudaStream_t st) {
     const ShardLayout v = shard_layout(d->host.q, 1, 0);
     const CUtensorMap map = make_input_map(d, in, v.row_len, d->host.q, batch, in_stride);
-    const auto P1 = d->k1_params(v, in, d->host.q, in_stride, Y);
+    auto P1 = d->k1_params(v, in, d->host.q, in_stride, Y);
+    auto P2 = d->k2_params(Y, out);
+    if (d->sum_tail) {
+        P2.mode = pftdev::K2_SUM;
+        P1.sum_tail = 1;
+        P1.k2 = P2;
+        cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
+        cuda_check(pftdev::launch_k2(P2, d->host.r, (uint32_t)batch, st), "K2 launch");
+        return;
+    }
+    if (d->fused(batch)) {
+        P1.fused = 1;
+        P1.bar = reinterpret_cast<unsigned*>(Y + d->slab_elems() * batch);
+        P1.k2 = P2;
+        cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 (fused) launch");
+        return;
+    }
     cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
-    const auto P2 = d->k2_params(Y, out);
     cuda_check(pftdev::launch_k2(P2, d->host.r, (uint32_t)batch, st), "K2 launch");
 }
 
@@ -305,17 +338,32 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     {
         const bool fft_ok = k2_fft_feasible(d->P2, H.r);
         const bool dot_ok = pftdev::k2_dot_smem_bytes(H.r, (uint32_t)d->P2) <= kK2SmemLimit;
-        const int forced = opts ? opts->reserved[0] : 0;  // 1 fft, 2 dot, 3 direct (A/B testing)
+        const int forced = opts ? opts->reserved[0] : 0;  // 1 fft, 2 dot, 3 direct, 4 l2 (A/B testing)
+        // L2 form when there are few output bins per m1 (W <= 2 P1, e.g. C1); it needs no shared
+        // memory and parks beside K1 under PDL.  Otherwise the FFT form (measured fastest at
+        // C2b/C4: 2049 / 2001 bins; the L2 form is latency-bound there).
+        const bool l2_ok = d->P2 <= 1024 && double(d->W) * d->P2 <= 64.0 * 1024 * 1024;
         if (forced == 1 && fft_ok) d->k2_mode = pftdev::K2_FFT;
         else if (forced == 2 && dot_ok) d->k2_mode = pftdev::K2_DOT;
         else if (forced == 3) d->k2_mode = pftdev::K2_DIRECT;
-        else if (fft_ok) d->k2_mode = pftdev::K2_FFT;  // measured faster than dot at C2b/C4
+        else if (forced == 4) d->k2_mode = pftdev::K2_L2;
+        else if (forced == 5) d->k2_mode = pftdev::K2_FFT;  // with the sum tail below
+        else if (l2_ok && d->W <= 2 * d->P1) d->k2_mode = pftdev::K2_L2;  // few bins per m1 (C1)
+        else if (fft_ok) d->k2_mode = pftdev::K2_FFT;
         else if (dot_ok) d->k2_mode = pftdev::K2_DOT;
         else d->k2_mode = pftdev::K2_DIRECT;
         if (d->k2_mode == pftdev::K2_FFT) {
             if (d->P2 > 1) factor_radices((uint32_t)d->P2, d->fft2);
             else d->fft2.n = 1;
         }
+        // K2 CTAs (each loops over m1): few enough to all be resident beside K1 (opts override)
+        d->k2_ctas = opts && opts->reserved[1] > 0 ? (uint32_t)opts->reserved[1] : 0;
+        d->pdl_chain = !(opts && opts->reserved[2] == 1);  // reserved[2] == 1: plain stream order
+        d->allow_fuse = opts && opts->reserved[3] == 2;    // reserved[3] == 2: fuse K2 into K1's tail
+        // Sum tail when the outputs are few relative to p (W <= p/4) and the partial-sum
+        // buffer is small: K2 becomes a dot product per output (no FFT).  Forced off by modes 1-4.
+        d->sum_tail = (forced == 0 || forced == 5) && 4 * d->W <= H.p &&
+                      (double)d->W * d->P2 * sizeof(double2) <= 256.0 * 1024 * 1024;
     }
     d->mu0 = std::all_of(H.phase.begin(), H.phase.end(), [](const cplx& z) { return z == cplx(1.0, 0.0); });
 
@@ -354,11 +402,15 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
                "upload post_powers");
     cuda_check(cudaMemcpy(d->d_post_twiddles, H.post_twiddles.data(), d->W * sizeof(double2), cudaMemcpyHostToDevice),
                "upload post_twiddles");
-    cuda_check(cudaMalloc(&d->d_ws, d->slab_elems() * sizeof(double2)), "cudaMalloc(workspace)");
+    cuda_check(pftdev::configure_k1(H.r, (uint32_t)d->P1, d->mu0), "configure K1 (early)");
+    cuda_check(cudaMalloc(&d->d_ws, d->workspace_bytes(1)), "cudaMalloc(workspace)");
+    cuda_check(cudaMemset(d->d_ws, 0, d->workspace_bytes(1)), "cudaMemset(workspace)");
     cuda_check(cudaMalloc(&d->d_status, sizeof(int)), "cudaMalloc(status)");
     cuda_check(cudaMemset(d->d_status, 0, sizeof(int)), "cudaMemset(status)");
     cuda_check(pftdev::configure_k1(H.r, (uint32_t)d->P1, d->mu0), "configure K1");
     cuda_check(pftdev::configure_k2(H.r, (uint32_t)d->P2), "configure K2");
+    d->k1_capacity = (uint64_t)pftdev::k1_max_active_per_sm(H.r, (uint32_t)d->P1, d->k1_stages, d->mu0) *
+                     (uint64_t)prop.multiProcessorCount;
     *out = d.release();
     PFT_API_END
 }
@@ -375,19 +427,22 @@ pft_status pft_dplan_layout(pft_dplan_t d, uint64_t* p1, uint64_t* p2) {
 pft_status pft_workspace_bytes(pft_dplan_t d, size_t batch, size_t* bytes) {
     PFT_API_BEGIN
     PFT_REQUIRE(bytes != nullptr, "bytes is null");
-    *bytes = dp(d)->slab_elems() * sizeof(double2) * batch;
+    *bytes = dp(d)->workspace_bytes(batch);
     PFT_API_END
 }
 
 pft_status pft_partial_bytes(pft_dplan_t d, size_t batch, size_t* bytes) {
-    return pft_workspace_bytes(d, batch, bytes);
+    PFT_API_BEGIN
+    PFT_REQUIRE(bytes != nullptr, "bytes is null");
+    *bytes = dp(d)->slab_elems() * sizeof(double2) * batch;
+    PFT_API_END
 }
 
 pft_status pft_launches_per_execute(pft_dplan_t d, int* launches) {
     PFT_API_BEGIN
     dp(d);
     PFT_REQUIRE(launches != nullptr, "launches is null");
-    *launches = 2;
+    *launches = dp(d)->fused(1) ? 1 : 2;
     PFT_API_END
 }
 
@@ -481,7 +536,8 @@ pft_status pft_execute_host(pft_dplan_t dh, const pft_c128* h_in, size_t batch, 
     }
     double2* Y = d->d_ws;
     if (batch > 1) {
-        cuda_check(cudaMalloc(&ws, d->slab_elems() * sizeof(double2) * batch), "cudaMalloc(workspace)");
+        cuda_check(cudaMalloc(&ws, d->workspace_bytes(batch)), "cudaMalloc(workspace)");
+        cuda_check(cudaMemsetAsync(ws, 0, d->workspace_bytes(batch), st), "cudaMemset(workspace)");
         Y = ws;
     }
     cuda_check(cudaMemcpyAsync(din, h_in, n_in * sizeof(pft_c128), cudaMemcpyHostToDevice, st), "H2D input");

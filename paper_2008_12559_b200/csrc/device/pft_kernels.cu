@@ -32,7 +32,55 @@
 
 namespace pftdev {
 
+#ifdef PFT_TIMELINE
+// Development instrumentation: per-CTA %globaltimer stamps at K1 phase boundaries.
+__device__ unsigned long long g_pft_timeline[65536][6];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define PFT_STAMP(slot) \
+    if (threadIdx.x == 0 && blockIdx.x + blockIdx.y * gridDim.x < 65536) \
+        g_pft_timeline[blockIdx.x + blockIdx.y * gridDim.x][slot] = gtimer();
+__device__ unsigned long long g_pft_timeline2[65536][6];
+#define PFT_STAMP2(slot) \
+    if (threadIdx.x == 0 && blockIdx.x + blockIdx.y * gridDim.x < 65536) \
+        g_pft_timeline2[blockIdx.x + blockIdx.y * gridDim.x][slot] = gtimer();
+#else
+#define PFT_STAMP(slot)
+#define PFT_STAMP2(slot)
+#endif
+
+// Grid-wide barrier for K1's fused K2 tail (all CTAs are co-resident: cooperative launch).
+// Self-resetting: the last arriver zeroes the count and bumps the generation, so the state
+// (two words at the end of the workspace, zeroed once) is reusable by the next launch.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = ld_acquire_u32(gen);
+        __threadfence();
+        if (atomicAdd(count, 1u) == nblocks - 1) {
+            atomicExch(count, 0u);
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (ld_acquire_u32(gen) == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 // ----------------------------------------------------------------------------- K1
+
+template <int R>
+__device__ __forceinline__ void k2_fft_block(const K2Params& P, uint32_t m1, uint32_t b, double2* zs);
 
 template <int R, bool MU0>
 __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_constant__ CUtensorMap tmap,
@@ -46,6 +94,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     uint64_t* empty = full + S;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    PFT_STAMP(0)
     if (tid == 0) {
         for (uint32_t s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -53,9 +102,11 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         }
         fence_barrier_init();
     }
-    // stage the FFT twiddles omega_P1^t = omega_p^{t P2} once (read in every FFT stage)
-    for (uint32_t t = tid; t < P.P1; t += blockDim.x) tw1[t] = __ldg(P.omega + (size_t)t * P.P2);
-    __syncthreads();
+    __syncthreads();  // barriers initialised: the producer starts streaming immediately
+#ifdef PFT_K1_TRIGGER_EARLY
+    // (experiment) release the dependent K2 at the start of K1 instead of after its main loop
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
 
     const uint32_t c = blockIdx.x;  // residue class k = c (mod P2)
     const uint32_t b = blockIdx.y;  // signal
@@ -83,7 +134,10 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
             }
         }
     } else {
-        // ---- consumers: half-warp per row, lane li takes pairs li and li + 16 of each chunk
+        // ---- consumers: K1_LANES_PER_ROW lanes per row, each taking pairs li + k*LANES_PER_ROW
+        // FFT twiddles omega_P1^t = omega_p^{t P2} for the tail, staged while the first
+        // TMA boxes are in flight (read after the __syncthreads that ends the main loop)
+        for (uint32_t t = tid; t < P.P1; t += K1_CONSUMER_WARPS * 32) tw1[t] = __ldg(P.omega + (size_t)t * P.P2);
         const int li = lane & (K1_LANES_PER_ROW - 1);
         const int rin = (warp * 32 + lane) / K1_LANES_PER_ROW;  // row within the box
         for (uint32_t rb = 0; rb < nrb; ++rb) {
@@ -101,6 +155,9 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                 const uint32_t it = rb * nch + ch;
                 const uint32_t s = it % S, n = it / S;
                 mbar_wait(&full[s], n & 1);
+#ifdef PFT_TIMELINE
+                if (it == 0) PFT_STAMP(1)
+#endif
                 // Reconverge before touching the stage: lane 0's `empty` arrive below leaves
                 // the warp diverged, and reading a stage from a diverged warp was observed to
                 // return corrupt rows on B200 when two K1 CTAs share an SM.
@@ -134,9 +191,6 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                         }
                         are[0] += Sv.x;
                         aim[0] += Sv.y;
-#ifdef PFT_DBG_NOCOMPUTE
-                        continue;
-#endif
                         double tp = t;
 #pragma unroll
                         for (int j = 1; j < R; ++j) {
@@ -182,20 +236,66 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     }
     // All of A has been read: let K2 (launched with programmatic stream serialization)
     // get scheduled and run its prologue while this grid finishes its FFT tail.
+    PFT_STAMP(2)
+#ifndef PFT_K1_TRIGGER_EARLY
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
     __syncthreads();
+    PFT_STAMP(3)
 
     // First FFT pass over k1 (length P1) for every column j, in shared memory; the ring is
     // idle now and serves as the Stockham scratch buffer.
     const double2* res = Cs;
-#ifndef PFT_DBG_NOFFT
     if (P.P1 > 1) res = fft_columns(Cs, reinterpret_cast<double2*>(ring), R, P.fft, SmemTwiddles{tw1});
-#endif
-    // Y[b][m1][c][j]: the slab for one m1 is contiguous over (c, j) for K2.
-    double2* __restrict__ Y = P.Y + (size_t)b * P.P1 * P.P2 * R;
-    for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) {
-        const uint32_t m1 = idx / R, j = idx - m1 * R;
-        Y[((size_t)m1 * P.P2 + c) * R + j] = res[(size_t)j * P.P1 + m1];
+    PFT_STAMP(4)
+    // K1 is launched with programmatic stream serialization, so it may run while the previous
+    // kernel of the stream (K2 of the previous transform, which may still read this
+    // workspace) drains: wait for it only here, right before overwriting the slab.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (P.sum_tail) {
+        // Sum tail (few output bins, W << p): this CTA's share of every output slot s,
+        //   S'_c(s) = e^{-2 pi i m1 c / p} sum_j Y_c[m1][j] x_s^j,  m1 = (m mod p) mod P1,
+        // with x_s = (m - mu)/p and its powers formed exactly as the planner forms
+        // post_powers (repeated multiplication, ascending j).  K2 then only sums over c.
+        const K2Params& Q = P.k2;
+        for (uint32_t t = tid; t < P.P1; t += blockDim.x) tw1[t] = __ldg(P.omega + (size_t)t * c);  // m1 c < p
+        __syncthreads();
+        const int64_t Mh = (int64_t)((Q.W - 1) / 2);
+        const double pd = (double)Q.p;
+        const bool p1_pow2 = (P.P1 & (P.P1 - 1)) == 0;
+        double2* __restrict__ Sout = P.Y + (size_t)b * Q.W * P.P2;  // [s][c]
+        for (uint64_t s = tid; s < Q.W; s += blockDim.x) {
+            uint64_t mp = Q.first_mod_p + s % Q.p;
+            if (mp >= Q.p) mp -= Q.p;
+            const uint32_t m1 = p1_pow2 ? (uint32_t)(mp & (P.P1 - 1)) : (uint32_t)(mp % P.P1);
+            const double x = (double)((int64_t)s - Mh) / pd;
+            double2 S = res[m1];
+            double tp = x;
+#pragma unroll
+            for (int j = 1; j < R; ++j) {  // ascending j
+                const double2 v = res[(size_t)j * P.P1 + m1];
+                S.x = fma(v.x, tp, S.x);
+                S.y = fma(v.y, tp, S.y);
+                if (j + 1 < R) tp *= x;
+            }
+            Sout[s * P.P2 + c] = cmul(S, tw1[m1]);
+        }
+    } else {
+        // Y[b][m1][c][j]: the slab for one m1 is contiguous over (c, j) for K2.
+        double2* __restrict__ Y = P.Y + (size_t)b * P.P1 * P.P2 * R;
+        for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) {
+            const uint32_t m1 = idx / R, j = idx - m1 * R;
+            Y[((size_t)m1 * P.P2 + c) * R + j] = res[(size_t)j * P.P1 + m1];
+        }
+    }
+    PFT_STAMP(5)
+    if (P.fused) {
+        // Fused K2: once every residue's slab is in L2, CTA (c, b) finishes bins m1 = c,
+        // c + P2, ... of signal b; the other CTAs exit and free their SM slots for the next
+        // transform's K1 (already launched under PDL).
+        grid_barrier(P.bar, P.bar + 1, gridDim.x * gridDim.y);
+        for (uint32_t m1 = c; m1 < P.P1; m1 += P.P2)
+            k2_fft_block<R>(P.k2, m1, b, reinterpret_cast<double2*>(ring));
     }
 }
 
@@ -227,6 +327,47 @@ __device__ __forceinline__ void load_twiddled_slab(const double2* __restrict__ Y
     }
 }
 
+// K2 body for one (m1, signal): four-step twiddle, length-P2 FFT over c in shared memory,
+// Eq. (7) at the output slots owned by m1.  smem: Z, scratch (r x P2 each), tw2, pre (P2).
+// `prologue_done`: tw2/pre already staged.  Shared by the standalone K2 and K1's fused tail.
+template <int R>
+__device__ __forceinline__ void k2_fft_block(const K2Params& P, uint32_t m1, uint32_t b, double2* zs) {
+    double2* Z = zs;                              // [R][P2]
+    double2* scratch = zs + (size_t)R * P.P2;     // [R][P2]
+    double2* tw2 = scratch + (size_t)R * P.P2;    // omega_P2^t
+    double2* pre = tw2 + P.P2;                    // omega_p^{m1 c}
+    const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
+    if (s0 >= P.W) return;  // no output slot maps to this m1 (block-uniform)
+    for (uint32_t c = threadIdx.x; c < P.P2; c += blockDim.x) {
+        tw2[c] = __ldg(P.omega + (size_t)c * P.P1);  // omega_P2^c = omega_p^{c P1}
+        pre[c] = __ldg(P.omega + (size_t)m1 * c);    // four-step twiddle; m1 c < p
+    }
+    __syncthreads();
+    const double2* __restrict__ Y = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
+    load_twiddled_slab<R>(Y, P.P2, m1, pre, Z);
+    __syncthreads();
+    const double2* res = Z;
+    if (P.P2 > 1) res = fft_columns(Z, scratch, R, P.fft2, SmemTwiddles{tw2});
+    double2* __restrict__ out = P.out + (size_t)b * P.W;
+    for (uint64_t s = s0 + (uint64_t)P.P1 * threadIdx.x; s < P.W; s += (uint64_t)P.P1 * blockDim.x) {
+        uint64_t mp = P.first_mod_p + s % P.p;
+        if (mp >= P.p) mp -= P.p;
+        const uint32_t m2 = (uint32_t)(mp / P.P1);
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < R; ++j) {  // ascending j
+            const double pw = __ldg(P.post_powers + s * R + j);
+            const double2 v = res[(size_t)j * P.P2 + m2];
+            acc.x = fma(v.x, pw, acc.x);
+            acc.y = fma(v.y, pw, acc.y);
+        }
+        const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+        out[s] = v;
+        if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
+    }
+    __syncthreads();  // smem reuse by a following m1
+}
+
 template <int R>
 __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
     extern __shared__ __align__(16) double2 zs[];
@@ -235,6 +376,10 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
     double2* tw2 = scratch + (size_t)R * P.P2;    // omega_P2^t
     double2* pre = tw2 + P.P2;                    // omega_p^{m1 c}
     const uint32_t m1 = blockIdx.x, b = blockIdx.y;
+    PFT_STAMP2(0)
+    // the next transform's K1 may launch now: it only touches this workspace after its own
+    // griddepcontrol.wait (which waits for this grid to complete)
+    if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
     if (s0 >= P.W) return;  // no output slot maps to this m1 (block-uniform)
 
@@ -251,14 +396,18 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
         for (int j = 0; j < R; ++j) pw0[j] = __ldg(P.post_powers + s_first * R + j);
         ptw0 = __ldg(P.post_twiddles + s_first);
     }
+    PFT_STAMP2(1)
     // ---- wait for K1's slab Y to be complete and visible
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
+    PFT_STAMP2(2)
     const double2* __restrict__ Y = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
     load_twiddled_slab<R>(Y, P.P2, m1, pre, Z);
     __syncthreads();
+    PFT_STAMP2(3)
     const double2* res = Z;
     if (P.P2 > 1) res = fft_columns(Z, scratch, R, P.fft2, SmemTwiddles{tw2});
+    PFT_STAMP2(4)
     double2* __restrict__ out = P.out + (size_t)b * P.W;
     for (uint64_t s = s_first; s < P.W; s += (uint64_t)P.P1 * blockDim.x) {
         uint64_t mp = P.first_mod_p + s % P.p;
@@ -277,6 +426,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
         out[s] = v;
         if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
     }
+    PFT_STAMP2(5)
 }
 
 // K2 (dot form, few outputs per m1): only the ~W/P1 bins this CTA owns are needed, so
@@ -293,6 +443,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_dot_post(K2Params P) {
     const uint32_t m1 = blockIdx.x, b = blockIdx.y;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int NW = K2_THREADS / 32;
+    if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
     if (s0 >= P.W) return;  // block-uniform
     // ---- prologue (overlaps K1's tail under PDL): twiddle tables and this warp's first powers
@@ -345,6 +496,93 @@ __global__ void __launch_bounds__(K2_THREADS) k2_dot_post(K2Params P) {
     }
 }
 
+// K2 (L2 form, default): no shared memory and a small register footprint, so its CTAs
+// can park beside two K1 CTAs on every SM while K1 streams (programmatic dependent launch).
+// One warp per output slot reads the m1 slice of the L2-resident slab directly:
+//   out[s] = e^{-pi i m/p} sum_c e^{-2 pi i m' c / p} (sum_j Y[m1][c][j] ((m - mu)/p)^j)
+// (m' = m mod p, m1 = m' mod P1).  Lane-strided partial sums + xor-butterfly: fixed order.
+template <int R>
+__global__ void __launch_bounds__(K2L_THREADS) k2_l2_post(K2Params P) {
+    // the next transform's K1 may launch now (it waits for this grid before touching Y)
+    if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint32_t b = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const bool p_pow2 = (P.p & (P.p - 1)) == 0;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's slab complete and visible
+    const double2* __restrict__ Yb = P.Y + (size_t)b * P.P1 * P.P2 * R;
+    double2* __restrict__ out = P.out + (size_t)b * P.W;
+    for (uint64_t s = gwarp; s < P.W; s += nwarps) {
+        uint64_t mp = P.first_mod_p + s % P.p;
+        if (mp >= P.p) mp -= P.p;
+        const uint32_t m1 = (uint32_t)(mp % P.P1);
+        const double2* __restrict__ Y = Yb + (size_t)m1 * P.P2 * R;
+        double pw[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) pw[j] = __ldg(P.post_powers + s * R + j);
+        double2 acc = make_double2(0.0, 0.0);
+        for (uint32_t c = lane; c < P.P2; c += 32) {
+            const double2* yc = Y + (size_t)c * R;
+            const uint64_t e = p_pow2 ? ((mp * c) & (P.p - 1)) : ((mp * c) % P.p);
+            const double2 tw = __ldg(P.omega + e);  // e^{-2 pi i m' c / p}
+            double2 S = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < R; ++j) {  // ascending j
+                const double2 y = yc[j];
+                S.x = fma(y.x, pw[j], S.x);
+                S.y = fma(y.y, pw[j], S.y);
+            }
+            acc = cadd(acc, cmul(S, tw));
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+        }
+        if (lane == 0) {
+            const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+            out[s] = v;
+            if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
+        }
+    }
+}
+
+// K2 (sum form, with K1's sum tail): out[s] = e^{-pi i m/p} sum_c omega_P2^{m2 c} S'_c(s),
+// one warp per output slot reading the contiguous row S'[s][0..P2) -- no FFT, a 4 KB table
+// in shared memory, so it is resident at once and releases the next transform's K1.
+__global__ void __launch_bounds__(K2_THREADS) k2_sum_post(K2Params P) {
+    extern __shared__ __align__(16) double2 tw2s[];  // omega_P2^t
+    if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    for (uint32_t c = threadIdx.x; c < P.P2; c += blockDim.x) tw2s[c] = __ldg(P.omega + (size_t)c * P.P1);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's partial sums complete and visible
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t s = (uint64_t)blockIdx.x * (K2_THREADS / 32) + warp;
+    if (s >= P.W) return;
+    const uint32_t b = blockIdx.y;
+    uint64_t mp = P.first_mod_p + s % P.p;
+    if (mp >= P.p) mp -= P.p;
+    const uint32_t m2 = (uint32_t)(mp / P.P1);
+    const bool p2_pow2 = (P.P2 & (P.P2 - 1)) == 0;
+    const double2* __restrict__ row = P.Y + ((size_t)b * P.W + s) * P.P2;
+    double2 acc = make_double2(0.0, 0.0);
+    for (uint32_t c = lane; c < P.P2; c += 32) {
+        const uint32_t e = p2_pow2 ? ((m2 * c) & (P.P2 - 1)) : (uint32_t)(((uint64_t)m2 * c) % P.P2);
+        acc = cadd(acc, cmul(row[c], tw2s[e]));
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    }
+    if (lane == 0) {
+        const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+        P.out[(size_t)b * P.W + s] = v;
+        if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
+    }
+}
+
 // Direct form for any P2 (P2 with a prime factor > 64, or too large for shared memory):
 // Chat[m'][j] = sum_c e^{-2 pi i m' c / p} Y[m1][c][j], one warp per output slot.
 template <int R>
@@ -357,6 +595,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_direct_post(K2Params P) {
     const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
     const double2* __restrict__ Y = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
     double2* __restrict__ out = P.out + (size_t)b * P.W;
+    if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
     for (uint64_t s = s0 + (uint64_t)P.P1 * warp; s < P.W; s += (uint64_t)P.P1 * NW) {
@@ -436,11 +675,32 @@ __global__ void k0_generate(GenParams G) {
 template <int R>
 static cudaError_t launch_k1_r(const CUtensorMap& map, const K1Params& P, dim3 grid, size_t smem, cudaStream_t st,
                                bool mu0) {
-    if (mu0)
-        k1_contract_fft<R, true><<<grid, K1_THREADS, smem, st>>>(map, P);
-    else
-        k1_contract_fft<R, false><<<grid, K1_THREADS, smem, st>>>(map, P);
-    return cudaGetLastError();
+    // Programmatic dependent launch: when the previous kernel in the stream is a K2 (which
+    // triggers at its start), this K1 starts streaming its input while that K2 finishes;
+    // any other predecessor does not trigger, so ordinary stream order applies.
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(K1_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    unsigned n = 0;
+    if (P.pdl) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+#ifndef PFT_NO_COOP
+    if (P.fused) {  // the grid barrier needs every CTA resident
+        attr[n].id = cudaLaunchAttributeCooperative;
+        attr[n].val.cooperative = 1;
+        ++n;
+    }
+#endif
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    if (mu0) return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, true>, map, P);
+    return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, false>, map, P);
 }
 
 template <int R>
@@ -464,6 +724,14 @@ static cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (P.mode == K2_L2) {
+        cfg.blockDim = dim3(K2L_THREADS);
+        return cudaLaunchKernelEx(&cfg, k2_l2_post<R>, P);
+    }
+    if (P.mode == K2_SUM) {
+        cfg.dynamicSmemBytes = sizeof(double2) * P.P2;
+        return cudaLaunchKernelEx(&cfg, k2_sum_post, P);
+    }
     if (P.mode == K2_FFT) return cudaLaunchKernelEx(&cfg, k2_fft_post<R>, P);
     if (P.mode == K2_DOT) return cudaLaunchKernelEx(&cfg, k2_dot_post<R>, P);
     return cudaLaunchKernelEx(&cfg, k2_direct_post<R>, P);
@@ -471,7 +739,9 @@ static cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
 
 template <int R>
 static cudaError_t configure_k2_r(size_t smem) {
-    const cudaError_t e = cudaFuncSetAttribute(k2_fft_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k2_fft_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k2_sum_post, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k2_dot_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
@@ -489,6 +759,26 @@ cudaError_t configure_k1(int r, uint32_t P1, bool mu0) {
 #undef X
     }
     return cudaErrorInvalidValue;
+}
+
+template <int R>
+static int k1_active_r(size_t smem, bool mu0) {
+    int n = 0;
+    if (mu0)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_contract_fft<R, true>, K1_THREADS, smem);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_contract_fft<R, false>, K1_THREADS, smem);
+    return n;
+}
+
+int k1_max_active_per_sm(int r, uint32_t P1, uint32_t stages, bool mu0) {
+    const size_t smem = k1_smem_bytes(r, P1, stages);
+    switch (r) {
+#define X(n) case n: return k1_active_r<n>(smem, mu0);
+        PFT_R_CASES(X)
+#undef X
+    }
+    return 0;
 }
 
 cudaError_t configure_k2(int r, uint32_t P2) {
@@ -514,7 +804,9 @@ cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t
 }
 
 cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st) {
-    const dim3 grid(P.P1, batch);
+    const uint32_t gx = P.mode == K2_L2 ? (P.k2_ctas ? P.k2_ctas : 148u)
+                        : P.mode == K2_SUM ? (uint32_t)((P.W + K2_THREADS / 32 - 1) / (K2_THREADS / 32)) : P.P1;
+    const dim3 grid(gx, batch);
     switch (r) {
 #define X(n) case n: return launch_k2_r<n>(P, grid, st);
         PFT_R_CASES(X)
@@ -522,6 +814,15 @@ cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st)
     }
     return cudaErrorInvalidValue;
 }
+
+#ifdef PFT_TIMELINE
+extern "C" int pft_debug_timeline(unsigned long long* host, int n_ctas) {
+    return (int)cudaMemcpyFromSymbol(host, g_pft_timeline, sizeof(unsigned long long) * 6 * n_ctas);
+}
+extern "C" int pft_debug_timeline2(unsigned long long* host, int n_ctas) {
+    return (int)cudaMemcpyFromSymbol(host, g_pft_timeline2, sizeof(unsigned long long) * 6 * n_ctas);
+}
+#endif
 
 cudaError_t launch_k0(const GenParams& G, cudaStream_t st) {
     const int threads = 256;

@@ -150,3 +150,37 @@ def test_sharded_partials_sum_to_unsharded(pft, oracle, N, M, mu, p, world):
     torch.cuda.synchronize()
     ref = oracle.execute(plan, a)
     assert rel_l2(out.cpu().numpy(), ref) <= GATE
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+def test_batched_workspace_and_fused_tail(pft, oracle, fuse):
+    """Batched execute through a caller workspace (zeroed once, reused), with K2 fused into
+    K1's tail (grid barrier) or launched separately: identical to per-signal oracle runs."""
+    import torch
+    N, M, mu, batch = 2 ** 16, 128, 77, 3
+    plan = pft.build_plan(N, M, mu, None, 1e-12)
+    d = pft.DevicePlan(plan, fuse=fuse)
+    a = pft.generate_signal(pft.KIND_UNIFORM, 9, N * batch)
+    x = torch.from_numpy(a).cuda()
+    ws = torch.zeros(-(-d.workspace_bytes(batch) // 16), dtype=torch.complex128, device="cuda")
+    out = torch.empty(batch * (2 * M + 1), dtype=torch.complex128, device="cuda")
+    for _ in range(3):  # the workspace is left reusable
+        d.execute_ptr(x.data_ptr(), out.data_ptr(), batch=batch, in_stride=N, d_ws=ws.data_ptr())
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().reshape(batch, 2 * M + 1)
+    for b in range(batch):
+        ref = oracle.execute(plan, a[b * N:(b + 1) * N])
+        assert rel_l2(got[b], ref) <= GATE, (b, fuse)
+
+
+def test_nonfinite_input_is_reported(pft):
+    """non-finite input entries are an error (reported via the status word)."""
+    N = 2 ** 14
+    plan = pft.build_plan(N, 32, 0, None, 1e-12)
+    a = pft.generate_signal(pft.KIND_UNIFORM, 3, N)
+    a[1234] = np.nan
+    with pytest.raises(ValueError) as e:
+        pft.execute(plan, a)
+    assert e.value.status == 7
+    a[1234] = 0.5  # the plan stays usable afterwards
+    assert np.all(np.isfinite(pft.execute(plan, a).values))

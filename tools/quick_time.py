@@ -32,9 +32,9 @@ def graph_time(fn, reps, stream):
     return e0.elapsed_time(e1) / reps
 
 
-def time_plan(N, M, mu, p, p2=0, stages=0, reps=200, label="", k2_mode=0):
+def time_plan(N, M, mu, p, p2=0, stages=0, reps=200, label="", k2_mode=0, k2_ctas=0, fuse=True):
     plan = pft.build_plan(N, M, mu, p, 1e-12)
-    d = pft.DevicePlan(plan, p2=p2, k1_stages=stages, k2_mode=k2_mode)
+    d = pft.DevicePlan(plan, p2=p2, k1_stages=stages, k2_mode=k2_mode, k2_ctas=k2_ctas, fuse=fuse)
     bufs = [torch.empty(N, dtype=torch.complex128, device="cuda") for _ in range(2)]
     for i, b in enumerate(bufs):
         pft.generate_signal_device(b.data_ptr(), pft.KIND_UNIFORM, 1 + i, N)
@@ -47,7 +47,7 @@ def time_plan(N, M, mu, p, p2=0, stages=0, reps=200, label="", k2_mode=0):
     # K2 alone (finalize of the same slab), and a 2-stream pipeline of independent transforms
     k2 = graph_time(lambda i: d.finalize_ptr(Y.data_ptr(), out.data_ptr(), stream=sp), reps, s)
     s2 = torch.cuda.Stream()
-    ws = [torch.empty(plan.p * plan.r, dtype=torch.complex128, device="cuda") for _ in range(2)]
+    ws = [torch.zeros(-(-d.workspace_bytes(1) // 16), dtype=torch.complex128, device="cuda") for _ in range(2)]
     outs = [torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda") for _ in range(2)]
     ev = [torch.cuda.Event() for _ in range(2)]
 
@@ -63,7 +63,23 @@ def time_plan(N, M, mu, p, p2=0, stages=0, reps=200, label="", k2_mode=0):
             ev[1].record(s2)
             s.wait_event(ev[1])
     ms2 = graph_time(two_stream, reps, s)
-    print(json.dumps({"label": label, "k2_us": round(k2 * 1e3, 2), "pipelined_us": round(ms2 * 1e3, 2), "N": N, "M": M, "p": plan.p, "q": plan.q, "r": plan.r, "P1": d.P1,
+
+    # split: the K1 chain stays on stream s (PDL back-to-back), each transform's K2 runs on s2
+    evk = [torch.cuda.Event() for _ in range(reps + 8)]
+    evf = [torch.cuda.Event() for _ in range(reps + 8)]
+
+    def split(i):
+        if i >= 2:
+            s.wait_event(evf[i - 2])  # K2(i-2) done reading workspace i % 2
+        d.execute_partial_ptr(bufs[i % 2].data_ptr(), ws[i % 2].data_ptr(), stream=s.cuda_stream)
+        evk[i].record(s)
+        s2.wait_event(evk[i])
+        d.finalize_ptr(ws[i % 2].data_ptr(), outs[i % 2].data_ptr(), stream=s2.cuda_stream)
+        evf[i].record(s2)
+        if i == reps - 1 or i == 2:
+            s.wait_event(evf[i])
+    ms3 = graph_time(split, reps, s)
+    print(json.dumps({"label": label, "k2_us": round(k2 * 1e3, 2), "pipelined_us": round(ms2 * 1e3, 2), "split_us": round(ms3 * 1e3, 2), "N": N, "M": M, "p": plan.p, "q": plan.q, "r": plan.r, "P1": d.P1,
                       "P2": d.P2, "stages": stages, "us": round(ms * 1e3, 2), "k1_us": round(k1 * 1e3, 2),
                       "GB/s": round(16 * N / (ms * 1e-3) / 1e9, 1),
                       "k1_GB/s": round(16 * N / (k1 * 1e-3) / 1e9, 1)}), flush=True)
@@ -72,6 +88,38 @@ def time_plan(N, M, mu, p, p2=0, stages=0, reps=200, label="", k2_mode=0):
 if __name__ == "__main__":
     import os
     which = os.environ.get("QT", "main")
+    if which == "split":
+        for rep in range(2):
+            time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label="C2b", reps=500)
+            time_plan(6220800, 1000, -12345, 62208, label="C4", reps=500)
+            time_plan(2 ** 20, 64, 0, None, label="C1", reps=500)
+    if which == "sum":
+        for rep in range(2):
+            for mode in (5, 1):
+                time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label=f"C2b k2_mode={mode}", k2_mode=mode, reps=500)
+                time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 14, label=f"C2b p=2^14 k2_mode={mode}", k2_mode=mode, reps=500)
+                time_plan(6220800, 1000, -12345, 62208, label=f"C4 k2_mode={mode}", k2_mode=mode, reps=500)
+                time_plan(2 ** 20, 64, 0, None, label=f"C1 k2_mode={mode}", k2_mode=mode, reps=500)
+    if which == "fuse":
+        for rep in range(2):
+            for fz in (True, False):
+                time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label=f"C2b fuse={fz}", fuse=fz, reps=500)
+                time_plan(6220800, 1000, -12345, 62208, label=f"C4 fuse={fz}", fuse=fz, reps=500)
+    if which == "rep":
+        for _ in range(3):
+            time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label="C2b", reps=1000)
+            time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 14, label="C2b p=2^14", reps=1000)
+    if which == "l2":
+        for mode in (4, 1):
+            time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label=f"C2b k2_mode={mode}", k2_mode=mode)
+            time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 14, label=f"C2b p=2^14 k2_mode={mode}", k2_mode=mode)
+            time_plan(6220800, 1000, -12345, 62208, label=f"C4 k2_mode={mode}", k2_mode=mode)
+            time_plan(2 ** 20, 64, 0, None, label=f"C1 k2_mode={mode}", k2_mode=mode)
+    if which == "k2c":
+        for kc in (16, 32, 64, 128):
+            time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label=f"C2b k2_ctas={kc}", k2_ctas=kc)
+        time_plan(6220800, 1000, -12345, 62208, label="C4")
+        time_plan(2 ** 24, 2 ** 14, 2 ** 22, 2 ** 16, label="C2c p=2^16")
     if which == "k2":
         for mode in (1, 2, 3):
             time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label=f"C2b k2_mode={mode}", k2_mode=mode)
