@@ -412,7 +412,7 @@ class DevicePlan:
     pointers (e.g. torch.Tensor.data_ptr() of complex128 CUDA tensors)."""
 
     def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0, k1_stages: int = 0, k2_mode: int = 0,
-                 k2_ctas: int = 0, pdl: bool = True, fuse: bool = False):
+                 k2_ctas: int = 0, pdl: bool = True, fuse: bool = False, reducers: int = 0):
         self.plan = plan
         opts = _capi.DPlanOpts()
         opts.device = device
@@ -422,6 +422,7 @@ class DevicePlan:
         opts.reserved[1] = k2_ctas  # K2 grid width for the L2 form (0 = default)
         opts.reserved[2] = 0 if pdl else 1  # PDL chaining of consecutive transforms
         opts.reserved[3] = 2 if fuse else 0  # K2 fused into K1's tail (grid barrier, opt-in)
+        opts.reserved[4] = reducers  # sum tail: reducing CTAs per signal (0 = one per 64 outputs)
         h = C.c_void_p()
         _check(lib().pft_dplan_create(plan.handle, C.byref(opts), C.byref(h)))
         self._h = h

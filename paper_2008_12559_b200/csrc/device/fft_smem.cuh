@@ -87,15 +87,31 @@ __device__ __forceinline__ void dft3(double2& v0, double2& v1, double2& v2) {
     v2 = csub(m, r);
 }
 
+// The threads that run an FFT pass: the whole CTA (__syncthreads), or K1's consumer warps
+// alone (named barrier 1) while the producer warp keeps streaming.
+struct BlockTeam {
+    __device__ __forceinline__ int tid() const { return threadIdx.x; }
+    __device__ __forceinline__ int size() const { return blockDim.x; }
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+template <int NT>
+struct WarpsTeam {
+    int t;
+    __device__ __forceinline__ int tid() const { return t; }
+    __device__ __forceinline__ int size() const { return NT; }
+    __device__ __forceinline__ void sync() const { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
+};
+
 // One Stockham stage with a radix known at compile time (2, 3, 4, 8).  When n is a power
 // of two (POW2) the index arithmetic uses shifts/masks (lg_nb = log2(n/R), lg_ns =
 // log2(Ns)); otherwise integer division.
 template <int R, bool POW2, class TW>
 __device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__ src, double2* __restrict__ dst,
-                                                     int ncols, int n, int Ns, int lg_nb, int lg_ns, const TW& tw) {
+                                                     int ncols, int n, int Ns, int lg_nb, int lg_ns, const TW& tw,
+                                                     int t0, int nt) {
     const int nb = n / R;
     const uint32_t tstride = (uint32_t)(n / (Ns * R));
-    for (int idx = threadIdx.x; idx < ncols * nb; idx += blockDim.x) {
+    for (int idx = t0; idx < ncols * nb; idx += nt) {
         int col, j, k, base;
         if constexpr (POW2) {
             col = idx >> lg_nb;
@@ -129,11 +145,11 @@ __device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__
 // Generic radix (any R): O(R^2) per butterfly, twiddles omega_R^{rs} = omega_n^{rs n/R}.
 template <class TW>
 __device__ __forceinline__ void stockham_stage_generic(const double2* __restrict__ src, double2* __restrict__ dst,
-                                                       int ncols, int n, int Ns, int R, const TW& tw) {
+                                                       int ncols, int n, int Ns, int R, const TW& tw, int t0, int nt) {
     const int nb = n / R;
     const uint32_t tstride = (uint32_t)(n / (Ns * R));
     const uint32_t rstride = (uint32_t)(n / R);
-    for (int idx = threadIdx.x; idx < ncols * nb * R; idx += blockDim.x) {
+    for (int idx = t0; idx < ncols * nb * R; idx += nt) {
         const int col = idx / (nb * R);
         const int rem = idx - col * nb * R;
         const int j = rem / R, out_r = rem - j * R;
@@ -151,10 +167,11 @@ __device__ __forceinline__ void stockham_stage_generic(const double2* __restrict
 }
 
 // Full transform of ncols columns; returns the buffer holding the result (x or y).
-// Caller must __syncthreads() before (inputs written) and after (outputs read).
-template <class TW>
+// Caller must team.sync() before (inputs written); the last stage ends with a team.sync().
+template <class TW, class Team = BlockTeam>
 __device__ __forceinline__ double2* fft_columns(double2* x, double2* y, int ncols, const FftRadices& plan,
-                                                const TW& tw) {
+                                                const TW& tw, const Team team = Team{}) {
+    const int t0 = team.tid(), nt = team.size();
     double2* src = x;
     double2* dst = y;
     int Ns = 1, lg_ns = 0;
@@ -167,21 +184,21 @@ __device__ __forceinline__ double2* fft_columns(double2* x, double2* y, int ncol
         const int lg_nb = lg_n - lg_r;
         if (pow2) {
             switch (R) {
-                case 2: stockham_stage_fixed<2, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw); break;
-                case 4: stockham_stage_fixed<4, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw); break;
-                default: stockham_stage_fixed<8, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw); break;
+                case 2: stockham_stage_fixed<2, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt); break;
+                case 4: stockham_stage_fixed<4, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt); break;
+                default: stockham_stage_fixed<8, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt); break;
             }
             lg_ns += lg_r;
         } else {
             switch (R) {
-                case 2: stockham_stage_fixed<2, false>(src, dst, ncols, n, Ns, 0, 0, tw); break;
-                case 3: stockham_stage_fixed<3, false>(src, dst, ncols, n, Ns, 0, 0, tw); break;
-                case 4: stockham_stage_fixed<4, false>(src, dst, ncols, n, Ns, 0, 0, tw); break;
-                case 8: stockham_stage_fixed<8, false>(src, dst, ncols, n, Ns, 0, 0, tw); break;
-                default: stockham_stage_generic(src, dst, ncols, n, Ns, R, tw); break;
+                case 2: stockham_stage_fixed<2, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt); break;
+                case 3: stockham_stage_fixed<3, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt); break;
+                case 4: stockham_stage_fixed<4, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt); break;
+                case 8: stockham_stage_fixed<8, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt); break;
+                default: stockham_stage_generic(src, dst, ncols, n, Ns, R, tw, t0, nt); break;
             }
         }
-        __syncthreads();
+        team.sync();
         double2* t = src;
         src = dst;
         dst = t;

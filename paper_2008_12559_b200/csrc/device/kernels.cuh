@@ -36,7 +36,8 @@ static_assert(K1_STAGE_BYTES % 128 == 0, "TMA destinations stay 128-byte aligned
 
 constexpr int K2_THREADS = 256;
 constexpr int K2L_THREADS = 128;
-enum K2Mode { K2_DIRECT = 0, K2_FFT = 1, K2_DOT = 2, K2_L2 = 3, K2_SUM = 4 };
+enum K2Mode { K2_DIRECT = 0, K2_FFT = 1, K2_DOT = 2, K2_L2 = 3 };
+
 
 struct K2Params {
     const double2* Y;              // [batch][P1][P2][r]
@@ -50,7 +51,8 @@ struct K2Params {
     uint32_t first_mod_p1;         // (mu - M) mod P1
     int mode;                      // K2_DIRECT / K2_FFT / K2_DOT
     uint32_t k2_ctas;              // K2_L2 grid width (0 = 148)
-    int release_next;              // trigger the next launch at K2 start (PDL chaining)
+    int release_next;              // trigger the next launch at K2 start (1) / end (2) (PDL chaining)
+    uint32_t tl_seq;               // launch sequence number (PFT_TIMELINE instrumentation only)
     FftRadices fft2;               // radices of P2
     double2* out;                  // [batch][W]
     int* status;
@@ -80,8 +82,11 @@ struct K1Params {
     FftRadices fft;             // radices of P1
     uint32_t stages;            // ring depth (K1_MIN_STAGES..K1_MAX_STAGES)
     int pdl;                    // launched with programmatic stream serialization
-    double2* Y;                 // [batch][P1][P2][r] slab, or [batch][W][P2] partial sums (sum_tail)
-    int sum_tail;               // write per-output partial sums S'_c(s) instead of the slab
+    double2* Y;                 // [batch][P1][P2][r] slab, or [batch][P2][W] residue rows (sum_tail)
+    int sum_tail;               // sum tail: no slab, no K2 (see k1_sum_tail)
+    uint32_t reducers;          // sum tail: the last `reducers` CTAs of a signal reduce its rows
+    unsigned* arrivals;         // sum tail: per signal {tickets, done, ready[P2]} (zeroed once)
+    uint32_t tl_seq;            // launch sequence number (PFT_TIMELINE instrumentation only)
     int fused;                  // run K2 in K1's tail behind a grid barrier (cooperative launch)
     unsigned* bar;              // grid-barrier state {count, generation} (workspace tail, zeroed once)
     K2Params k2;                // K2 parameters for the fused tail
@@ -117,8 +122,16 @@ inline size_t k2_smem_bytes(int r, uint32_t P2) { return sizeof(double2) * (2 * 
 inline size_t k2_dot_smem_bytes(int r, uint32_t P2) { return sizeof(double2) * ((size_t)r * P2 + 2 * (size_t)P2); }
 
 cudaError_t configure_k1(int r, uint32_t P1, bool mu0);
+
 int k1_max_active_per_sm(int r, uint32_t P1, uint32_t stages, bool mu0);
 constexpr size_t kBarrierBytes = 256;  // grid-barrier words at the end of a workspace
+// workspace control words after the data: grid barrier (256 B), then the sum tail's
+// arrival counters (`per_signal` words per signal)
+inline size_t ctrl_bytes(size_t batch, size_t per_signal) {
+    return kBarrierBytes + ((4 * per_signal * batch + 255) & ~size_t(255));
+}
+// sum-tail scratch in the (idle) ring after the FFT scratch: per-warp partials + ticket
+inline size_t k1_sum_scratch_bytes() { return (size_t)K1_THREADS / 32 * 64 * 16 + 16; }
 cudaError_t configure_k2(int r, uint32_t P2);
 cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t batch, bool mu0, cudaStream_t st);
 cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st);

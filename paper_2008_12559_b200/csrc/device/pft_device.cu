@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -113,7 +114,8 @@ struct pft_dplan_s {
     uint32_t k2_ctas = 0;
     bool pdl_chain = true;  // K2 releases the next K1 early (programmatic dependent launch)
     bool allow_fuse = false; // K2 fused into K1's tail (opt-in; measured slower at C2b/C4)
-    bool sum_tail = false;   // unsharded execute: K1 writes per-output partial sums, K2 = sum form
+    bool sum_tail = false;   // unsharded execute: K1 sum tail, no K2 (few output bins)
+    uint32_t reducers = 0;   // sum tail: CTAs per signal that reduce the residue rows
     uint64_t k1_capacity = 0;  // co-resident K1 CTAs on the device
     bool mu0 = false;
     uint64_t W = 0;
@@ -141,9 +143,10 @@ struct pft_dplan_s {
     }
 
     size_t slab_elems() const { return (size_t)host.p * host.r; }
+    size_t counters_per_signal() const { return sum_tail ? P2 + 2 : 0; }
+    size_t data_elems() const { return sum_tail ? std::max<size_t>(slab_elems(), (size_t)P2 * W) : slab_elems(); }
     size_t workspace_bytes(size_t batch) const {
-        const size_t per = sum_tail ? std::max<size_t>(slab_elems(), (size_t)W * P2) : slab_elems();
-        return per * sizeof(double2) * batch + pftdev::kBarrierBytes;
+        return data_elems() * sizeof(double2) * batch + pftdev::ctrl_bytes(batch, counters_per_signal());
     }
     bool fused(size_t batch) const {
         return allow_fuse && !sum_tail && k2_mode == pftdev::K2_FFT &&
@@ -261,17 +264,20 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
     const CUtensorMap map = make_input_map(d, in, v.row_len, d->host.q, batch, in_stride);
     auto P1 = d->k1_params(v, in, d->host.q, in_stride, Y);
     auto P2 = d->k2_params(Y, out);
+    static std::atomic<uint32_t> seq{0};  // PFT_TIMELINE ring index
+    P1.tl_seq = P2.tl_seq = seq.fetch_add(1, std::memory_order_relaxed);
     if (d->sum_tail) {
-        P2.mode = pftdev::K2_SUM;
         P1.sum_tail = 1;
+        P1.reducers = d->reducers;
+        P1.arrivals = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(Y + d->data_elems() * batch) +
+                                                  pftdev::kBarrierBytes);
         P1.k2 = P2;
         cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
-        cuda_check(pftdev::launch_k2(P2, d->host.r, (uint32_t)batch, st), "K2 launch");
         return;
     }
     if (d->fused(batch)) {
         P1.fused = 1;
-        P1.bar = reinterpret_cast<unsigned*>(Y + d->slab_elems() * batch);
+        P1.bar = reinterpret_cast<unsigned*>(Y + d->data_elems() * batch);
         P1.k2 = P2;
         cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 (fused) launch");
         return;
@@ -338,10 +344,11 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     {
         const bool fft_ok = k2_fft_feasible(d->P2, H.r);
         const bool dot_ok = pftdev::k2_dot_smem_bytes(H.r, (uint32_t)d->P2) <= kK2SmemLimit;
-        const int forced = opts ? opts->reserved[0] : 0;  // 1 fft, 2 dot, 3 direct, 4 l2 (A/B testing)
+        const int forced = opts ? opts->reserved[0] : 0;  // 1 fft, 2 dot, 3 direct, 4 l2, 5 sum tail (A/B)
         // L2 form when there are few output bins per m1 (W <= 2 P1, e.g. C1); it needs no shared
-        // memory and parks beside K1 under PDL.  Otherwise the FFT form (measured fastest at
-        // C2b/C4: 2049 / 2001 bins; the L2 form is latency-bound there).
+        // memory and parks beside K1 under PDL.  Otherwise the FFT form (the L2 form is
+        // latency-bound at C2b/C4's 2049 / 2001 bins) -- unless the sum tail below applies
+        // (measured C2b 49 vs 54 us, C4 35 vs 45 us per transform).
         const bool l2_ok = d->P2 <= 1024 && double(d->W) * d->P2 <= 64.0 * 1024 * 1024;
         if (forced == 1 && fft_ok) d->k2_mode = pftdev::K2_FFT;
         else if (forced == 2 && dot_ok) d->k2_mode = pftdev::K2_DOT;
@@ -359,11 +366,18 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         // K2 CTAs (each loops over m1): few enough to all be resident beside K1 (opts override)
         d->k2_ctas = opts && opts->reserved[1] > 0 ? (uint32_t)opts->reserved[1] : 0;
         d->pdl_chain = !(opts && opts->reserved[2] == 1);  // reserved[2] == 1: plain stream order
-        d->allow_fuse = opts && opts->reserved[3] == 2;    // reserved[3] == 2: fuse K2 into K1's tail
-        // Sum tail when the outputs are few relative to p (W <= p/4) and the partial-sum
-        // buffer is small: K2 becomes a dot product per output (no FFT).  Forced off by modes 1-4.
-        d->sum_tail = (forced == 0 || forced == 5) && 4 * d->W <= H.p &&
-                      (double)d->W * d->P2 * sizeof(double2) <= 256.0 * 1024 * 1024;
+        d->allow_fuse = opts && opts->reserved[3] == 2;
+        // Sum tail when the outputs are few relative to p (W <= p/4): K1 finishes the
+        // transform itself (see k1_sum_tail).  Needs the ring to hold the FFT scratch and the
+        // reduction scratch.  Forced off by modes 1-4, forced on (if feasible) by 5.
+        const bool sum_ok = 4 * d->W <= H.p &&
+                            sizeof(double2) * H.r * d->P1 + pftdev::k1_sum_scratch_bytes() <=
+                                (size_t)pftdev::K1_MIN_STAGES * pftdev::K1_STAGE_BYTES;
+        d->sum_tail = sum_ok && (forced == 5 || (forced == 0 && d->k2_mode != pftdev::K2_L2));
+        // reducing CTAs per signal: one per 64 outputs (measured best at C2b/C4: 32; more
+        // reducers hold more SM slots from the next transform), opts override
+        d->reducers = (uint32_t)std::min<uint64_t>(d->P2, std::max<uint64_t>(1, (d->W + 63) / 64));
+        if (opts && opts->reserved[4] > 0) d->reducers = (uint32_t)std::min<uint64_t>(d->P2, opts->reserved[4]);
     }
     d->mu0 = std::all_of(H.phase.begin(), H.phase.end(), [](const cplx& z) { return z == cplx(1.0, 0.0); });
 
@@ -442,7 +456,7 @@ pft_status pft_launches_per_execute(pft_dplan_t d, int* launches) {
     PFT_API_BEGIN
     dp(d);
     PFT_REQUIRE(launches != nullptr, "launches is null");
-    *launches = dp(d)->fused(1) ? 1 : 2;
+    *launches = (dp(d)->fused(1) || dp(d)->sum_tail) ? 1 : 2;
     PFT_API_END
 }
 

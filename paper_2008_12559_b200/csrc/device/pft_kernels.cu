@@ -33,20 +33,21 @@
 namespace pftdev {
 
 #ifdef PFT_TIMELINE
-// Development instrumentation: per-CTA %globaltimer stamps at K1 phase boundaries.
-__device__ unsigned long long g_pft_timeline[65536][6];
+// Development instrumentation: per-CTA %globaltimer stamps at phase boundaries, kept for the
+// last 4 executes (ring indexed by the launch sequence number) so a PDL chain can be read back.
+__device__ unsigned long long g_pft_timeline[4][4096][6];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
 #define PFT_STAMP(slot) \
-    if (threadIdx.x == 0 && blockIdx.x + blockIdx.y * gridDim.x < 65536) \
-        g_pft_timeline[blockIdx.x + blockIdx.y * gridDim.x][slot] = gtimer();
-__device__ unsigned long long g_pft_timeline2[65536][6];
+    if (threadIdx.x == 0 && blockIdx.x + blockIdx.y * gridDim.x < 4096) \
+        g_pft_timeline[P.tl_seq & 3][blockIdx.x + blockIdx.y * gridDim.x][slot] = gtimer();
+__device__ unsigned long long g_pft_timeline2[4][4096][6];
 #define PFT_STAMP2(slot) \
-    if (threadIdx.x == 0 && blockIdx.x + blockIdx.y * gridDim.x < 65536) \
-        g_pft_timeline2[blockIdx.x + blockIdx.y * gridDim.x][slot] = gtimer();
+    if (threadIdx.x == 0 && blockIdx.x + blockIdx.y * gridDim.x < 4096) \
+        g_pft_timeline2[P.tl_seq & 3][blockIdx.x + blockIdx.y * gridDim.x][slot] = gtimer();
 #else
 #define PFT_STAMP(slot)
 #define PFT_STAMP2(slot)
@@ -59,6 +60,9 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
     __syncthreads();
@@ -81,6 +85,205 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, uns
 
 template <int R>
 __device__ __forceinline__ void k2_fft_block(const K2Params& P, uint32_t m1, uint32_t b, double2* zs);
+
+// One TMA stage (a box of K1_BR rows x K1_CP mirror column pairs + the pair table slice)
+// into the row accumulators of this lane: lanes li, li + LANES_PER_ROW, ... of row `rin`.
+template <int R, bool MU0>
+__device__ __forceinline__ void k1_accumulate_stage(const unsigned char* st, int rin, int li, uint32_t valid,
+                                                    double (&are)[R], double (&aim)[R]) {
+    const double2* front = reinterpret_cast<const double2*>(st) + rin * K1_CP;
+    const double2* mirror = reinterpret_cast<const double2*>(st + K1_BOX_BYTES) + rin * K1_CP;
+    const PairEntry* tab = reinterpret_cast<const PairEntry*>(st + 2 * K1_BOX_BYTES);
+#pragma unroll
+    for (int u = 0; u < K1_CP / K1_LANES_PER_ROW; ++u) {
+        const int i = li + u * K1_LANES_PER_ROW;
+        // branch-free masking of pairs past the end of the view (keeps the
+        // independent pairs in one basic block so their chains interleave)
+        const bool ok = (uint32_t)i < valid;
+        const double2 z = make_double2(0.0, 0.0);
+        const double2 x1 = ok ? front[i] : z;               // column l
+        const double2 x2 = ok ? mirror[K1_CP - 1 - i] : z;  // column q - l
+        const double2 cs = *reinterpret_cast<const double2*>(&tab[i].c);
+        const double t = tab[i].t;
+        const double2 su = make_double2(x1.x + x2.x, x1.y + x2.y);
+        const double2 di = make_double2(x1.x - x2.x, x1.y - x2.y);
+        double2 Sv, Dv;  // phase_l x1 +/- conj(phase_l) x2
+        if constexpr (MU0) {
+            Sv = su;
+            Dv = di;
+        } else {
+            Sv = make_double2(fma(cs.x, su.x, -cs.y * di.y), fma(cs.x, su.y, cs.y * di.x));
+            Dv = make_double2(fma(cs.x, di.x, -cs.y * su.y), fma(cs.x, di.y, cs.y * su.x));
+        }
+        are[0] += Sv.x;
+        aim[0] += Sv.y;
+        double tp = t;
+#pragma unroll
+        for (int j = 1; j < R; ++j) {
+            const double2 v = (j & 1) ? Dv : Sv;  // t^j (b + (-1)^j b')
+            are[j] = fma(v.x, tp, are[j]);
+            aim[j] = fma(v.y, tp, aim[j]);
+            if (j + 1 < R) tp *= t;
+        }
+    }
+}
+
+// End of a row batch: add this lane's unpaired column (l = 0 with t = 1 feeds every j;
+// l = q/2 with t = 0 only j = 0), reduce over the LANES_PER_ROW lanes of the row (fixed
+// xor-butterfly order) and store C[k1][j] = w_j acc_j into Cs[j][k1].
+template <int R, bool MU0>
+__device__ __forceinline__ void k1_finish_row(const K1Params& P, double2 xs, int scol, int li, uint32_t k1,
+                                              double (&are)[R], double (&aim)[R], double2* Cs) {
+    if (scol >= 0) {
+        double2 x = xs;
+        if constexpr (!MU0) x = cmul(x, li == 0 ? P.phase0 : P.phaseh);
+        are[0] += x.x;
+        aim[0] += x.y;
+        if (li == 0) {
+#pragma unroll
+            for (int j = 1; j < R; ++j) {
+                are[j] += x.x;
+                aim[j] += x.y;
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+#pragma unroll
+        for (int off = K1_LANES_PER_ROW / 2; off >= 1; off >>= 1) {
+            are[j] += __shfl_xor_sync(0xffffffffu, are[j], off);
+            aim[j] += __shfl_xor_sync(0xffffffffu, aim[j], off);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        if (k1 < P.P1 && (j % K1_LANES_PER_ROW) == li)
+            Cs[(size_t)j * P.P1 + k1] = cmul(make_double2(are[j], aim[j]), __ldg(P.w + j));  // C = w_j acc_j
+    }
+}
+
+// Sum tail (few output bins, W <= p/4), which replaces K2.  CTA (c, b) writes its residue row
+//   S[b][c][s] = e^{-2 pi i (m mod p) c / p} sum_j Y_c[m1][j] x_s^j     (s in [W], x_s = (m - mu)/p,
+// m1 = (m mod p) mod P1, powers by repeated multiplication in ascending j as the planner forms
+// post_powers), raises the row's ready flag and takes a ticket; the last `reducers` CTAs of
+// signal b each sum the P2 rows for a slice of the outputs in a fixed order (bitwise
+// deterministic), times e^{-pi i m / p}.  The transform is one kernel: under PDL the next
+// transform's K1 streams while these few CTAs finish, which a separate K2 (waiting for all of
+// K1) could not allow.
+template <int R>
+__device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* res, uint32_t c, uint32_t b,
+                                         unsigned char* scratch) {
+    const K2Params& Q = P.k2;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    const int64_t Mh = (int64_t)((Q.W - 1) / 2);
+    const double pd = (double)Q.p;
+    const bool p1_pow2 = (P.P1 & (P.P1 - 1)) == 0, p_pow2 = (Q.p & (Q.p - 1)) == 0;
+    double2* __restrict__ rowc = P.Y + ((size_t)b * P.P2 + c) * Q.W;
+    constexpr int TB = 8;  // outputs per thread in flight (one omega lookup each)
+    for (uint64_t base = tid; base < Q.W; base += (uint64_t)TB * nt) {
+        double2 tw[TB];
+        uint32_t m1v[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+            const uint64_t so = base + (uint64_t)k * nt;
+            uint64_t mp = Q.first_mod_p + (so < Q.p ? so : so % Q.p);
+            if (mp >= Q.p) mp -= Q.p;
+            m1v[k] = p1_pow2 ? (uint32_t)mp & (P.P1 - 1) : (uint32_t)mp % P.P1;
+            const uint64_t e = p_pow2 ? (mp * c) & (Q.p - 1) : (mp * c) % Q.p;  // mp c < p P2
+            tw[k] = so < Q.W ? __ldg(P.omega + e) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < TB; ++k) {
+            const uint64_t so = base + (uint64_t)k * nt;
+            if (so >= Q.W) break;
+            const uint32_t m1 = m1v[k];
+            const double x = (double)((int64_t)so - Mh) / pd;
+            double2 acc = res[m1];
+            double tp = x;
+#pragma unroll
+            for (int j = 1; j < R; ++j) {
+                const double2 v = res[(size_t)j * P.P1 + m1];
+                acc.x = fma(v.x, tp, acc.x);
+                acc.y = fma(v.y, tp, acc.y);
+                if (j + 1 < R) tp *= x;
+            }
+            rowc[so] = cmul(acc, tw[k]);
+        }
+    }
+    // publish the row, then take a ticket: the last `reducers` arrivals of signal b reduce
+    unsigned* ctl = P.arrivals + (size_t)b * (P.P2 + 2);  // {tickets, done, ready[P2]}
+    unsigned* ready = ctl + 2;
+    unsigned* s_ticket = reinterpret_cast<unsigned*>(scratch + (size_t)nw * 64 * sizeof(double2));
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        st_release_u32(ready + c, 1u);
+        *s_ticket = atomicAdd(ctl, 1u);
+    }
+    __syncthreads();
+#ifdef PFT_DEV_NO_REDUCE  // development A/B only: the sum tail without the reduction
+    return;
+#endif
+    const uint32_t t = *s_ticket, K = P.reducers;
+    if (t + K < P.P2) return;
+    // Reducer k sums rows c = 0..P2-1 (fixed order per warp: c = warp, warp + nw, ...) for
+    // its slice of outputs, taking each row as soon as its ready flag is up: most rows are
+    // in by now, and the rest stream in while it works instead of after a wait for all.
+    const uint32_t k = t + K - P.P2;
+    const uint64_t s0 = (uint64_t)k * Q.W / K, s1 = (uint64_t)(k + 1) * Q.W / K;
+    double2* part = reinterpret_cast<double2*>(scratch);  // [nw][64]
+    const double2* __restrict__ rows = P.Y + (size_t)b * P.P2 * Q.W;
+    for (uint64_t g0 = s0; g0 < s1; g0 += 64) {  // two 32-output groups per pass
+        const uint64_t sa = g0 + lane, sb = g0 + 32 + lane;
+        const bool oka = sa < s1, okb = sb < s1;
+        double2 acca = make_double2(0.0, 0.0), accb = make_double2(0.0, 0.0);
+        for (uint32_t r0 = warp; r0 < P.P2; r0 += 8 * nw) {
+            // lanes 0..7 wait for the ready flags of this warp's next 8 rows
+            const uint32_t myrow = r0 + (uint32_t)(lane & 7) * nw;
+            if (lane < 8 && myrow < P.P2)
+                while (ld_acquire_u32(ready + myrow) == 0) __nanosleep(32);
+            __syncwarp();
+            double2 va[8], vb[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t r = r0 + u * nw;
+                const bool in = r < P.P2;
+                va[u] = (in && oka) ? __ldcg(rows + (size_t)r * Q.W + sa) : make_double2(0.0, 0.0);
+                vb[u] = (in && okb) ? __ldcg(rows + (size_t)r * Q.W + sb) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                acca = cadd(acca, va[u]);
+                accb = cadd(accb, vb[u]);
+            }
+        }
+        part[warp * 64 + lane] = acca;
+        part[warp * 64 + 32 + lane] = accb;
+        __syncthreads();
+        if (warp < 2) {
+            const uint64_t so = g0 + warp * 32 + lane;
+            if (so < s1) {
+                double2 tot = part[warp * 32 + lane];
+                for (int w = 1; w < nw; ++w) tot = cadd(tot, part[w * 64 + warp * 32 + lane]);
+                const double2 v = cmul(tot, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
+                Q.out[(size_t)b * Q.W + so] = v;
+                if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(Q.status, 1);
+            }
+        }
+        __syncthreads();
+    }
+    // the last reducer to finish re-arms the signal's counters and flags
+    if (tid == 0) *s_ticket = atomicAdd(ctl + 1, 1u) == K - 1;
+    __syncthreads();
+    if (*s_ticket) {
+        for (uint32_t i = tid; i < P.P2; i += nt) ready[i] = 0;
+        if (tid == 0) {
+            ctl[0] = 0;
+            ctl[1] = 0;
+        }
+        __threadfence();
+    }
+}
 
 template <int R, bool MU0>
 __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_constant__ CUtensorMap tmap,
@@ -162,76 +365,12 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                 // the warp diverged, and reading a stage from a diverged warp was observed to
                 // return corrupt rows on B200 when two K1 CTAs share an SM.
                 __syncwarp();
-                const unsigned char* st = ring + (size_t)s * K1_STAGE_BYTES;
-                const double2* front = reinterpret_cast<const double2*>(st) + rin * K1_CP;
-                const double2* mirror = reinterpret_cast<const double2*>(st + K1_BOX_BYTES) + rin * K1_CP;
-                const PairEntry* tab = reinterpret_cast<const PairEntry*>(st + 2 * K1_BOX_BYTES);
-                const uint32_t valid = min((uint32_t)K1_CP, npairs - ch * K1_CP);
-#pragma unroll
-                for (int u = 0; u < K1_CP / K1_LANES_PER_ROW; ++u) {
-                    const int i = li + u * K1_LANES_PER_ROW;
-                    // branch-free masking of pairs past the end of the view (keeps the
-                    // independent pairs in one basic block so their chains interleave)
-                    const bool ok = (uint32_t)i < valid;
-                    {
-                        const double2 z = make_double2(0.0, 0.0);
-                        const double2 x1 = ok ? front[i] : z;               // column l
-                        const double2 x2 = ok ? mirror[K1_CP - 1 - i] : z;  // column q - l
-                        const double2 cs = *reinterpret_cast<const double2*>(&tab[i].c);
-                        const double t = tab[i].t;
-                        const double2 su = make_double2(x1.x + x2.x, x1.y + x2.y);
-                        const double2 di = make_double2(x1.x - x2.x, x1.y - x2.y);
-                        double2 Sv, Dv;  // phase_l x1 +/- conj(phase_l) x2
-                        if constexpr (MU0) {
-                            Sv = su;
-                            Dv = di;
-                        } else {
-                            Sv = make_double2(fma(cs.x, su.x, -cs.y * di.y), fma(cs.x, su.y, cs.y * di.x));
-                            Dv = make_double2(fma(cs.x, di.x, -cs.y * su.y), fma(cs.x, di.y, cs.y * su.x));
-                        }
-                        are[0] += Sv.x;
-                        aim[0] += Sv.y;
-                        double tp = t;
-#pragma unroll
-                        for (int j = 1; j < R; ++j) {
-                            const double2 v = (j & 1) ? Dv : Sv;  // t^j (b + (-1)^j b')
-                            are[j] = fma(v.x, tp, are[j]);
-                            aim[j] = fma(v.y, tp, aim[j]);
-                            if (j + 1 < R) tp *= t;
-                        }
-                    }
-                }
+                k1_accumulate_stage<R, MU0>(ring + (size_t)s * K1_STAGE_BYTES, rin, li,
+                                            min((uint32_t)K1_CP, npairs - ch * K1_CP), are, aim);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);  // stage s may be refilled
             }
-            // unpaired columns l = 0 (t = 1: every j) and l = q/2 (t = 0: j = 0 only)
-            if (scol >= 0) {
-                double2 x = xs;
-                if constexpr (!MU0) x = cmul(x, li == 0 ? P.phase0 : P.phaseh);
-                are[0] += x.x;
-                aim[0] += x.y;
-                if (li == 0) {
-#pragma unroll
-                    for (int j = 1; j < R; ++j) {
-                        are[j] += x.x;
-                        aim[j] += x.y;
-                    }
-                }
-            }
-            // reduce over the 16 lanes of the row (fixed xor-butterfly order)
-#pragma unroll
-            for (int j = 0; j < R; ++j) {
-#pragma unroll
-                for (int off = K1_LANES_PER_ROW / 2; off >= 1; off >>= 1) {
-                    are[j] += __shfl_xor_sync(0xffffffffu, are[j], off);
-                    aim[j] += __shfl_xor_sync(0xffffffffu, aim[j], off);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < R; ++j) {
-                if (k1 < P.P1 && (j % K1_LANES_PER_ROW) == li)
-                    Cs[(size_t)j * P.P1 + k1] = cmul(make_double2(are[j], aim[j]), __ldg(P.w + j));  // C = w_j acc_j
-            }
+            k1_finish_row<R, MU0>(P, xs, scol, li, k1, are, aim, Cs);
         }
     }
     // All of A has been read: let K2 (launched with programmatic stream serialization)
@@ -253,40 +392,14 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     // workspace) drains: wait for it only here, right before overwriting the slab.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (P.sum_tail) {
-        // Sum tail (few output bins, W << p): this CTA's share of every output slot s,
-        //   S'_c(s) = e^{-2 pi i m1 c / p} sum_j Y_c[m1][j] x_s^j,  m1 = (m mod p) mod P1,
-        // with x_s = (m - mu)/p and its powers formed exactly as the planner forms
-        // post_powers (repeated multiplication, ascending j).  K2 then only sums over c.
-        const K2Params& Q = P.k2;
-        for (uint32_t t = tid; t < P.P1; t += blockDim.x) tw1[t] = __ldg(P.omega + (size_t)t * c);  // m1 c < p
-        __syncthreads();
-        const int64_t Mh = (int64_t)((Q.W - 1) / 2);
-        const double pd = (double)Q.p;
-        const bool p1_pow2 = (P.P1 & (P.P1 - 1)) == 0;
-        double2* __restrict__ Sout = P.Y + (size_t)b * Q.W * P.P2;  // [s][c]
-        for (uint64_t s = tid; s < Q.W; s += blockDim.x) {
-            uint64_t mp = Q.first_mod_p + s % Q.p;
-            if (mp >= Q.p) mp -= Q.p;
-            const uint32_t m1 = p1_pow2 ? (uint32_t)(mp & (P.P1 - 1)) : (uint32_t)(mp % P.P1);
-            const double x = (double)((int64_t)s - Mh) / pd;
-            double2 S = res[m1];
-            double tp = x;
-#pragma unroll
-            for (int j = 1; j < R; ++j) {  // ascending j
-                const double2 v = res[(size_t)j * P.P1 + m1];
-                S.x = fma(v.x, tp, S.x);
-                S.y = fma(v.y, tp, S.y);
-                if (j + 1 < R) tp *= x;
-            }
-            Sout[s * P.P2 + c] = cmul(S, tw1[m1]);
-        }
-    } else {
-        // Y[b][m1][c][j]: the slab for one m1 is contiguous over (c, j) for K2.
-        double2* __restrict__ Y = P.Y + (size_t)b * P.P1 * P.P2 * R;
-        for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) {
-            const uint32_t m1 = idx / R, j = idx - m1 * R;
-            Y[((size_t)m1 * P.P2 + c) * R + j] = res[(size_t)j * P.P1 + m1];
-        }
+        k1_sum_tail<R>(P, res, c, b, ring + (size_t)R * P.P1 * sizeof(double2));
+        return;
+    }
+    // Y[b][m1][c][j]: the slab for one m1 is contiguous over (c, j) for K2.
+    double2* __restrict__ Y = P.Y + (size_t)b * P.P1 * P.P2 * R;
+    for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) {
+        const uint32_t m1 = idx / R, j = idx - m1 * R;
+        Y[((size_t)m1 * P.P2 + c) * R + j] = res[(size_t)j * P.P1 + m1];
     }
     PFT_STAMP(5)
     if (P.fused) {
@@ -548,40 +661,6 @@ __global__ void __launch_bounds__(K2L_THREADS) k2_l2_post(K2Params P) {
     }
 }
 
-// K2 (sum form, with K1's sum tail): out[s] = e^{-pi i m/p} sum_c omega_P2^{m2 c} S'_c(s),
-// one warp per output slot reading the contiguous row S'[s][0..P2) -- no FFT, a 4 KB table
-// in shared memory, so it is resident at once and releases the next transform's K1.
-__global__ void __launch_bounds__(K2_THREADS) k2_sum_post(K2Params P) {
-    extern __shared__ __align__(16) double2 tw2s[];  // omega_P2^t
-    if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    for (uint32_t c = threadIdx.x; c < P.P2; c += blockDim.x) tw2s[c] = __ldg(P.omega + (size_t)c * P.P1);
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's partial sums complete and visible
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t s = (uint64_t)blockIdx.x * (K2_THREADS / 32) + warp;
-    if (s >= P.W) return;
-    const uint32_t b = blockIdx.y;
-    uint64_t mp = P.first_mod_p + s % P.p;
-    if (mp >= P.p) mp -= P.p;
-    const uint32_t m2 = (uint32_t)(mp / P.P1);
-    const bool p2_pow2 = (P.P2 & (P.P2 - 1)) == 0;
-    const double2* __restrict__ row = P.Y + ((size_t)b * P.W + s) * P.P2;
-    double2 acc = make_double2(0.0, 0.0);
-    for (uint32_t c = lane; c < P.P2; c += 32) {
-        const uint32_t e = p2_pow2 ? ((m2 * c) & (P.P2 - 1)) : (uint32_t)(((uint64_t)m2 * c) % P.P2);
-        acc = cadd(acc, cmul(row[c], tw2s[e]));
-    }
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-    }
-    if (lane == 0) {
-        const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
-        P.out[(size_t)b * P.W + s] = v;
-        if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
-    }
-}
 
 // Direct form for any P2 (P2 with a prime factor > 64, or too large for shared memory):
 // Chat[m'][j] = sum_c e^{-2 pi i m' c / p} Y[m1][c][j], one warp per output slot.
@@ -705,10 +784,12 @@ static cudaError_t launch_k1_r(const CUtensorMap& map, const K1Params& P, dim3 g
 
 template <int R>
 static cudaError_t configure_k1_r(size_t smem, bool mu0) {
-    if (mu0)
-        return cudaFuncSetAttribute(k1_contract_fft<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return cudaFuncSetAttribute(k1_contract_fft<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const auto a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e = mu0 ? cudaFuncSetAttribute(k1_contract_fft<R, true>, a, (int)smem)
+                        : cudaFuncSetAttribute(k1_contract_fft<R, false>, a, (int)smem);
+    return e;
 }
+
 
 template <int R>
 static cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
@@ -728,10 +809,6 @@ static cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
         cfg.blockDim = dim3(K2L_THREADS);
         return cudaLaunchKernelEx(&cfg, k2_l2_post<R>, P);
     }
-    if (P.mode == K2_SUM) {
-        cfg.dynamicSmemBytes = sizeof(double2) * P.P2;
-        return cudaLaunchKernelEx(&cfg, k2_sum_post, P);
-    }
     if (P.mode == K2_FFT) return cudaLaunchKernelEx(&cfg, k2_fft_post<R>, P);
     if (P.mode == K2_DOT) return cudaLaunchKernelEx(&cfg, k2_dot_post<R>, P);
     return cudaLaunchKernelEx(&cfg, k2_direct_post<R>, P);
@@ -740,8 +817,6 @@ static cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
 template <int R>
 static cudaError_t configure_k2_r(size_t smem) {
     cudaError_t e = cudaFuncSetAttribute(k2_fft_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k2_sum_post, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k2_dot_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
@@ -805,7 +880,7 @@ cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t
 
 cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st) {
     const uint32_t gx = P.mode == K2_L2 ? (P.k2_ctas ? P.k2_ctas : 148u)
-                        : P.mode == K2_SUM ? (uint32_t)((P.W + K2_THREADS / 32 - 1) / (K2_THREADS / 32)) : P.P1;
+                                           : P.P1;
     const dim3 grid(gx, batch);
     switch (r) {
 #define X(n) case n: return launch_k2_r<n>(P, grid, st);
@@ -816,11 +891,11 @@ cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st)
 }
 
 #ifdef PFT_TIMELINE
-extern "C" int pft_debug_timeline(unsigned long long* host, int n_ctas) {
-    return (int)cudaMemcpyFromSymbol(host, g_pft_timeline, sizeof(unsigned long long) * 6 * n_ctas);
+extern "C" int pft_debug_timeline(unsigned long long* host) {  // [4][4096][6]
+    return (int)cudaMemcpyFromSymbol(host, g_pft_timeline, sizeof(g_pft_timeline));
 }
-extern "C" int pft_debug_timeline2(unsigned long long* host, int n_ctas) {
-    return (int)cudaMemcpyFromSymbol(host, g_pft_timeline2, sizeof(unsigned long long) * 6 * n_ctas);
+extern "C" int pft_debug_timeline2(unsigned long long* host) {
+    return (int)cudaMemcpyFromSymbol(host, g_pft_timeline2, sizeof(g_pft_timeline2));
 }
 #endif
 

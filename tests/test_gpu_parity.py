@@ -152,14 +152,20 @@ def test_sharded_partials_sum_to_unsharded(pft, oracle, N, M, mu, p, world):
     assert rel_l2(out.cpu().numpy(), ref) <= GATE
 
 
-@pytest.mark.parametrize("fuse", [True, False])
-def test_batched_workspace_and_fused_tail(pft, oracle, fuse):
-    """Batched execute through a caller workspace (zeroed once, reused), with K2 fused into
-    K1's tail (grid barrier) or launched separately: identical to per-signal oracle runs."""
+@pytest.mark.parametrize("form", ["fused", "k2", "sum", "sum-all-reduce"])
+def test_batched_workspace_and_tail_forms(pft, oracle, form):
+    """Batched execute through a caller workspace (zeroed once, reused) with each tail form:
+    K2 fused into K1's tail (grid barrier), a separate K2, or the K1 sum tail (no K2; the last
+    CTAs of each signal reduce, here also with every CTA reducing): identical to per-signal
+    oracle runs."""
     import torch
     N, M, mu, batch = 2 ** 16, 128, 77, 3
     plan = pft.build_plan(N, M, mu, None, 1e-12)
-    d = pft.DevicePlan(plan, fuse=fuse)
+    kw = {"fused": dict(fuse=True, k2_mode=1), "k2": dict(k2_mode=1), "sum": dict(k2_mode=5),
+          "sum-all-reduce": dict(k2_mode=5, reducers=1 << 20)}[form]
+    d = pft.DevicePlan(plan, **kw)
+    assert d.launches_per_execute() == (2 if form == "k2" else 1)
+    fuse = form
     a = pft.generate_signal(pft.KIND_UNIFORM, 9, N * batch)
     x = torch.from_numpy(a).cuda()
     ws = torch.zeros(-(-d.workspace_bytes(batch) // 16), dtype=torch.complex128, device="cuda")

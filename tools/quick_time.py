@@ -32,9 +32,9 @@ def graph_time(fn, reps, stream):
     return e0.elapsed_time(e1) / reps
 
 
-def time_plan(N, M, mu, p, p2=0, stages=0, reps=200, label="", k2_mode=0, k2_ctas=0, fuse=True):
+def time_plan(N, M, mu, p, p2=0, stages=0, reps=200, label="", k2_mode=0, k2_ctas=0, fuse=False, red=0):
     plan = pft.build_plan(N, M, mu, p, 1e-12)
-    d = pft.DevicePlan(plan, p2=p2, k1_stages=stages, k2_mode=k2_mode, k2_ctas=k2_ctas, fuse=fuse)
+    d = pft.DevicePlan(plan, p2=p2, k1_stages=stages, k2_mode=k2_mode, k2_ctas=k2_ctas, fuse=fuse, reducers=red)
     bufs = [torch.empty(N, dtype=torch.complex128, device="cuda") for _ in range(2)]
     for i, b in enumerate(bufs):
         pft.generate_signal_device(b.data_ptr(), pft.KIND_UNIFORM, 1 + i, N)
@@ -100,6 +100,31 @@ if __name__ == "__main__":
                 time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 14, label=f"C2b p=2^14 k2_mode={mode}", k2_mode=mode, reps=500)
                 time_plan(6220800, 1000, -12345, 62208, label=f"C4 k2_mode={mode}", k2_mode=mode, reps=500)
                 time_plan(2 ** 20, 64, 0, None, label=f"C1 k2_mode={mode}", k2_mode=mode, reps=500)
+    if which == "sumc":
+        for rep in range(2):
+            for kc in (64, 148, 296, 592):
+                time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label=f"C2b sum k2_ctas={kc}", k2_mode=5, k2_ctas=kc, reps=500)
+                time_plan(6220800, 1000, -12345, 62208, label=f"C4 sum k2_ctas={kc}", k2_mode=5, k2_ctas=kc, reps=500)
+            for st in ():
+                for kc in (0, 16):
+                    time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label=f"C2b sum st={st} k2_ctas={kc}", k2_mode=5,
+                              k2_ctas=kc, stages=st, reps=500)
+    if which == "sumq":
+        for rep in range(2):
+            for red in (0, 32, 128):
+                time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label=f"C2b sum red={red}", k2_mode=5, red=red, reps=500)
+                time_plan(6220800, 1000, -12345, 62208, label=f"C4 sum red={red}", k2_mode=5, red=red, reps=500)
+                time_plan(2 ** 20, 64, 0, None, label=f"C1 sum red={red}", k2_mode=5, red=red, reps=500)
+            time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label="C2b fft", k2_mode=1, reps=500)
+            time_plan(6220800, 1000, -12345, 62208, label="C4 fft", k2_mode=1, reps=500)
+            time_plan(2 ** 20, 64, 0, None, label="C1 l2", k2_mode=4, reps=500)
+    if which == "sumv":
+        for rep in range(2):
+            for red in (0, 16, 64):
+                time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label=f"C2b sum red={red}", k2_mode=5, red=red, reps=500)
+                time_plan(6220800, 1000, -12345, 62208, label=f"C4 sum red={red}", k2_mode=5, red=red, reps=500)
+                time_plan(2 ** 20, 64, 0, None, label=f"C1 sum red={red}", k2_mode=5, red=red, reps=500)
+            time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label="C2b fft", k2_mode=1, reps=500)
     if which == "fuse":
         for rep in range(2):
             for fz in (True, False):
