@@ -48,6 +48,7 @@ struct K2Params {
     uint32_t P1, P2;
     uint64_t W;                    // 2M + 1
     uint64_t first_mod_p;          // (mu - M) mod p
+    double inv_p;                  // 1 / p
     uint32_t first_mod_p1;         // (mu - M) mod P1
     int mode;                      // K2_DIRECT / K2_FFT / K2_DOT
     uint32_t k2_ctas;              // K2_L2 grid width (0 = 148)
@@ -130,8 +131,11 @@ constexpr size_t kBarrierBytes = 256;  // grid-barrier words at the end of a wor
 inline size_t ctrl_bytes(size_t batch, size_t per_signal) {
     return kBarrierBytes + ((4 * per_signal * batch + 255) & ~size_t(255));
 }
-// sum-tail scratch in the (idle) ring after the FFT scratch: per-warp partials + ticket
-inline size_t k1_sum_scratch_bytes() { return (size_t)K1_THREADS / 32 * 64 * 16 + 16; }
+// sum-tail scratch in the (idle) ring after the FFT scratch: twiddle tables, per-warp
+// reducer partials, ticket
+inline size_t k1_sum_scratch_bytes(uint32_t P1, uint32_t P2) {
+    return 16 * ((size_t)P1 + P2) + (size_t)K1_THREADS / 32 * 64 * 16 + 16;
+}
 cudaError_t configure_k2(int r, uint32_t P2);
 cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t batch, bool mu0, cudaStream_t st);
 cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st);

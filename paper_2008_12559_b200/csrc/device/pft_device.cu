@@ -193,6 +193,7 @@ struct pft_dplan_s {
         const int64_t first = host.mu - (int64_t)host.M;
         P.first_mod_p = mod_index(first, host.p);
         P.first_mod_p1 = (uint32_t)mod_index(first, P1);
+        P.inv_p = 1.0 / (double)host.p;
         P.mode = k2_mode;
         P.k2_ctas = k2_ctas;
         P.release_next = pdl_chain ? 1 : 0;
@@ -371,7 +372,7 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         // transform itself (see k1_sum_tail).  Needs the ring to hold the FFT scratch and the
         // reduction scratch.  Forced off by modes 1-4, forced on (if feasible) by 5.
         const bool sum_ok = 4 * d->W <= H.p &&
-                            sizeof(double2) * H.r * d->P1 + pftdev::k1_sum_scratch_bytes() <=
+                            sizeof(double2) * H.r * d->P1 + pftdev::k1_sum_scratch_bytes((uint32_t)d->P1, (uint32_t)d->P2) <=
                                 (size_t)pftdev::K1_MIN_STAGES * pftdev::K1_STAGE_BYTES;
         d->sum_tail = sum_ok && (forced == 5 || (forced == 0 && d->k2_mode != pftdev::K2_L2));
         // reducing CTAs per signal: one per 64 outputs (measured best at C2b/C4: 32; more

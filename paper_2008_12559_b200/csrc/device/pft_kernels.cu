@@ -176,44 +176,40 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     const K2Params& Q = P.k2;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
     const int64_t Mh = (int64_t)((Q.W - 1) / 2);
-    const double pd = (double)Q.p;
-    const bool p1_pow2 = (P.P1 & (P.P1 - 1)) == 0, p_pow2 = (Q.p & (Q.p - 1)) == 0;
+    const bool p1_pow2 = (P.P1 & (P.P1 - 1)) == 0, p2_pow2 = (P.P2 & (P.P2 - 1)) == 0;
+    const int lg_p1 = 31 - __clz(P.P1);
+    // omega_p^{(m mod p) c} = omega_p^{m1 c} omega_P2^{m2 c}: both factors from tables in the idle ring
+    double2* twc = reinterpret_cast<double2*>(scratch);  // [P1] omega_p^{m1 c}
+    double2* tw2 = twc + P.P1;                            // [P2] omega_P2^t
+    for (uint32_t t = tid; t < P.P1; t += nt) twc[t] = __ldg(P.omega + (size_t)t * c);  // m1 c < p
+    for (uint32_t t = tid; t < P.P2; t += nt) tw2[t] = __ldg(P.omega + (size_t)t * P.P1);
+    __syncthreads();
     double2* __restrict__ rowc = P.Y + ((size_t)b * P.P2 + c) * Q.W;
-    constexpr int TB = 8;  // outputs per thread in flight (one omega lookup each)
-    for (uint64_t base = tid; base < Q.W; base += (uint64_t)TB * nt) {
-        double2 tw[TB];
-        uint32_t m1v[TB];
+    for (uint64_t so = tid; so < Q.W; so += nt) {
+        uint32_t mp = (uint32_t)(Q.first_mod_p + (so < Q.p ? so : so % Q.p));
+        if (mp >= Q.p) mp -= (uint32_t)Q.p;
+        const uint32_t m1 = p1_pow2 ? mp & (P.P1 - 1) : mp % P.P1;
+        const uint32_t m2 = p1_pow2 ? mp >> lg_p1 : mp / P.P1;
+        const uint32_t e2 = p2_pow2 ? (m2 * c) & (P.P2 - 1) : (m2 * c) % P.P2;  // m2 c < p
+        // x = (m - mu)/p; 1/p is exact for power-of-two p (then x^j is bit-identical to the
+        // planner's post_powers), else within an ulp
+        const double x = (double)((int64_t)so - Mh) * Q.inv_p;
+        double2 acc = res[m1];
+        double tp = x;
 #pragma unroll
-        for (int k = 0; k < TB; ++k) {
-            const uint64_t so = base + (uint64_t)k * nt;
-            uint64_t mp = Q.first_mod_p + (so < Q.p ? so : so % Q.p);
-            if (mp >= Q.p) mp -= Q.p;
-            m1v[k] = p1_pow2 ? (uint32_t)mp & (P.P1 - 1) : (uint32_t)mp % P.P1;
-            const uint64_t e = p_pow2 ? (mp * c) & (Q.p - 1) : (mp * c) % Q.p;  // mp c < p P2
-            tw[k] = so < Q.W ? __ldg(P.omega + e) : make_double2(0.0, 0.0);
+        for (int j = 1; j < R; ++j) {  // ascending j, powers by repeated multiplication
+            const double2 v = res[(size_t)j * P.P1 + m1];
+            acc.x = fma(v.x, tp, acc.x);
+            acc.y = fma(v.y, tp, acc.y);
+            if (j + 1 < R) tp *= x;
         }
-#pragma unroll
-        for (int k = 0; k < TB; ++k) {
-            const uint64_t so = base + (uint64_t)k * nt;
-            if (so >= Q.W) break;
-            const uint32_t m1 = m1v[k];
-            const double x = (double)((int64_t)so - Mh) / pd;
-            double2 acc = res[m1];
-            double tp = x;
-#pragma unroll
-            for (int j = 1; j < R; ++j) {
-                const double2 v = res[(size_t)j * P.P1 + m1];
-                acc.x = fma(v.x, tp, acc.x);
-                acc.y = fma(v.y, tp, acc.y);
-                if (j + 1 < R) tp *= x;
-            }
-            rowc[so] = cmul(acc, tw[k]);
-        }
+        rowc[so] = cmul(cmul(acc, twc[m1]), tw2[e2]);
     }
     // publish the row, then take a ticket: the last `reducers` arrivals of signal b reduce
     unsigned* ctl = P.arrivals + (size_t)b * (P.P2 + 2);  // {tickets, done, ready[P2]}
     unsigned* ready = ctl + 2;
-    unsigned* s_ticket = reinterpret_cast<unsigned*>(scratch + (size_t)nw * 64 * sizeof(double2));
+    double2* part = tw2 + P.P2;                           // [nw][64] reducer partials
+    unsigned* s_ticket = reinterpret_cast<unsigned*>(part + (size_t)nw * 64);
     __threadfence();
     __syncthreads();
     if (tid == 0) {
@@ -227,22 +223,19 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     const uint32_t t = *s_ticket, K = P.reducers;
     if (t + K < P.P2) return;
     // Reducer k sums rows c = 0..P2-1 (fixed order per warp: c = warp, warp + nw, ...) for
-    // its slice of outputs, taking each row as soon as its ready flag is up: most rows are
-    // in by now, and the rest stream in while it works instead of after a wait for all.
+    // its slice of outputs once the warp's rows are flagged ready (most are by now).
     const uint32_t k = t + K - P.P2;
     const uint64_t s0 = (uint64_t)k * Q.W / K, s1 = (uint64_t)(k + 1) * Q.W / K;
-    double2* part = reinterpret_cast<double2*>(scratch);  // [nw][64]
     const double2* __restrict__ rows = P.Y + (size_t)b * P.P2 * Q.W;
+    // this warp's rows c = warp, warp + nw, ...: all flags checked at once (one lane per row)
+    for (uint32_t r = warp + (uint32_t)lane * nw; r < P.P2; r += 32u * nw)
+        while (ld_acquire_u32(ready + r) == 0) __nanosleep(32);
+    __syncwarp();
     for (uint64_t g0 = s0; g0 < s1; g0 += 64) {  // two 32-output groups per pass
         const uint64_t sa = g0 + lane, sb = g0 + 32 + lane;
         const bool oka = sa < s1, okb = sb < s1;
         double2 acca = make_double2(0.0, 0.0), accb = make_double2(0.0, 0.0);
         for (uint32_t r0 = warp; r0 < P.P2; r0 += 8 * nw) {
-            // lanes 0..7 wait for the ready flags of this warp's next 8 rows
-            const uint32_t myrow = r0 + (uint32_t)(lane & 7) * nw;
-            if (lane < 8 && myrow < P.P2)
-                while (ld_acquire_u32(ready + myrow) == 0) __nanosleep(32);
-            __syncwarp();
             double2 va[8], vb[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {

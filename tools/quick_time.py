@@ -125,6 +125,10 @@ if __name__ == "__main__":
                 time_plan(6220800, 1000, -12345, 62208, label=f"C4 sum red={red}", k2_mode=5, red=red, reps=500)
                 time_plan(2 ** 20, 64, 0, None, label=f"C1 sum red={red}", k2_mode=5, red=red, reps=500)
             time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label="C2b fft", k2_mode=1, reps=500)
+    if which == "sum1":
+        for rep in range(2):
+            time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label="C2b sum", reps=500)
+            time_plan(6220800, 1000, -12345, 62208, label="C4 sum", reps=500)
     if which == "fuse":
         for rep in range(2):
             for fz in (True, False):
