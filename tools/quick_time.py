@@ -129,6 +129,11 @@ if __name__ == "__main__":
         for rep in range(2):
             time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label="C2b sum", reps=500)
             time_plan(6220800, 1000, -12345, 62208, label="C4 sum", reps=500)
+    if which == "redsweep":
+        for rep in range(2):
+            for red in (0, 20, 24, 40, 48):
+                time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label=f"C2b sum red={red}", red=red, reps=500)
+                time_plan(6220800, 1000, -12345, 62208, label=f"C4 sum red={red}", red=red, reps=500)
     if which == "fuse":
         for rep in range(2):
             for fz in (True, False):
