@@ -28,12 +28,13 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
-    # name: (N, M, mu, p, kind, description)
-    "c1": (2 ** 20, 64, 0, 2 ** 14, "uniform", "BASELINE configs[0]: N=2^20, M=64, mu=0, U[-1,1] re/im"),
-    "c2a": (2 ** 24, 2 ** 6, 2 ** 22, 2 ** 16, "sparse", "BASELINE configs[1]: N=2^24, M=2^6, mu=N/4, 32 tones + CN noise"),
-    "c2b": (2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, "sparse", "BASELINE configs[1]: N=2^24, M=2^10, mu=N/4, 32 tones + CN noise"),
-    "c2c": (2 ** 24, 2 ** 14, 2 ** 22, 2 ** 16, "sparse", "BASELINE configs[1]: N=2^24, M=2^14, mu=N/4, 32 tones + CN noise"),
-    "c4": (6220800, 1000, -12345, 62208, "normal", "BASELINE configs[3]: N=2^10 3^5 5^2, M=1000, mu=-12345, CN(0,1)"),
+    # name: (N, M, mu, p, kind, description); p None: our arm autotunes p on the device
+    # (pft_autotune_divisor), the reference arm uses SPEC's CPU cost model (select_divisor)
+    "c1": (2 ** 20, 64, 0, None, "uniform", "BASELINE configs[0]: N=2^20, M=64, mu=0, U[-1,1] re/im"),
+    "c2a": (2 ** 24, 2 ** 6, 2 ** 22, None, "sparse", "BASELINE configs[1]: N=2^24, M=2^6, mu=N/4, 32 tones + CN noise"),
+    "c2b": (2 ** 24, 2 ** 10, 2 ** 22, None, "sparse", "BASELINE configs[1]: N=2^24, M=2^10, mu=N/4, 32 tones + CN noise"),
+    "c2c": (2 ** 24, 2 ** 14, 2 ** 22, None, "sparse", "BASELINE configs[1]: N=2^24, M=2^14, mu=N/4, 32 tones + CN noise"),
+    "c4": (6220800, 1000, -12345, None, "normal", "BASELINE configs[3]: N=2^10 3^5 5^2, M=1000, mu=-12345, CN(0,1)"),
 }
 SEEDS = {"c1": 1, "c2a": 2, "c2b": 2, "c2c": 2, "c4": 4}
 EPS = 1e-12
@@ -194,15 +195,23 @@ def run_ours(args):
 
     N, M, mu, p, kind, desc = CONFIGS[args.config]
     W = 2 * M + 1
-    plan = pft.build_plan(N, M, mu, p, EPS)
-    d = pft.DevicePlan(plan, device=local, p2=args.p2, pdl=not args.no_pdl, fuse=args.fuse)
-    launches = d.launches_per_execute()
 
     # inputs: >= 2 buffers, together > 2x L2, rotated so no step re-reads a cached input
     nbuf = max(2, -(-2 * L2_BYTES // (16 * N)))
     bufs = [torch.empty(N, dtype=torch.complex128, device=dev) for _ in range(nbuf)]
     for i, b in enumerate(bufs):
         make_input_device(pft, b, N, mu, M, SEEDS[args.config] + 100 * rank, kind, offset=i * N)
+    p_src = "--p"
+    if args.p:
+        p = args.p
+    elif p is None:  # device-aware planner: model-ranked candidates, timed on this GPU
+        p, tuned_us = pft.autotune_divisor(N, M, mu, bufs[0].data_ptr(), epsilon=EPS, device=local)
+        p_src = f"pft_autotune_divisor ({tuned_us:.1f} us/transform in the tuning run)"
+    else:
+        p_src = "config"
+    plan = pft.build_plan(N, M, mu, p, EPS)
+    d = pft.DevicePlan(plan, device=local, p2=args.p2, pdl=not args.no_pdl, fuse=args.fuse)
+    launches = d.launches_per_execute()
     out = torch.empty(W, dtype=torch.complex128, device=dev)
     stream = torch.cuda.Stream(device=dev)
     sp = stream.cuda_stream
@@ -331,7 +340,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
             "config": {"workload": f"{args.config}: {desc}", "N": N, "M": M, "mu": mu, "epsilon": EPS,
-                       "p": plan.p, "q": plan.q, "r": plan.r, "P1": d.P1, "P2": d.P2,
+                       "p": plan.p, "q": plan.q, "r": plan.r, "P1": d.P1, "P2": d.P2, "p_choice": p_src,
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "l2": f"{nbuf} rotating inputs of {16 * N / 2**20:.0f} MiB (> L2 126 MiB)",
                        "timing": "CUDA graph of K steps, CUDA events on the launch stream",
@@ -372,6 +381,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2b", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--p", type=int, default=0, help="override p (0 = autotune on the device)")
     ap.add_argument("--p2", type=int, default=0, help="override K1 residue classes (0 = planner)")
     ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
                     help="1 (default): one stream; consecutive transforms overlap through programmatic "

@@ -99,6 +99,15 @@ pft_status pft_min_terms(pft_table_t t, double epsilon, uint64_t M, uint64_t p, 
  *                                                                   */
 pft_status pft_select_divisor(pft_table_t t, uint64_t N, uint64_t M, double epsilon,
                               uint64_t* p, int* r, double* cost);
+/* Device-aware choice of p for the B200 path (not in the reference):
+ * argmin_p of a calibrated HBM / FP64 / row-length / tail time model, n_sms = SM count (148).
+ * est_us = modelled microseconds per transform.  Pass the result to pft_plan_build.       */
+pft_status pft_select_divisor_device(pft_table_t t, uint64_t N, uint64_t M, double epsilon, int n_sms,
+                                     uint64_t* p, int* r, double* est_us);
+/* Measured choice: times the n_candidates best modelled p on `device` with the caller's input
+ * d_in (N complex128 on that device); returns the fastest p and its microseconds/transform. */
+pft_status pft_autotune_divisor(pft_table_t t, uint64_t N, uint64_t M, int64_t mu, double epsilon, int device,
+                                const pft_c128* d_in, int n_candidates, uint64_t* p, double* us);
 
 typedef struct pft_hplan_s* pft_hplan_t;
 

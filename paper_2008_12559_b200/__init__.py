@@ -20,7 +20,7 @@ from ._capi import c128
 
 __all__ = [
     "PftError", "ApproxPoly", "ScopeTable", "CostEstimate", "TargetRange", "PartialSpectrum", "PftPlan",
-    "DevicePlan", "best_approx", "scope_xi", "translate_poly", "divisors", "min_terms", "select_divisor",
+    "DevicePlan", "best_approx", "scope_xi", "translate_poly", "divisors", "min_terms", "select_divisor", "select_divisor_device", "autotune_divisor",
     "build_plan", "execute", "mod_index", "l1_norm", "generate_signal", "sparse_tones", "shard_layout",
     "shard_gather",
     "device_count", "lib",
@@ -306,6 +306,29 @@ def select_divisor(N: int, M: int, table: Optional[ScopeTable] = None,
     _check(lib().pft_select_divisor(_table(table).handle, int(N), int(M), float(epsilon), C.byref(p),
                                     C.byref(r), C.byref(cost)))
     return p.value, CostEstimate(p.value, r.value, cost.value)
+
+
+def select_divisor_device(N: int, M: int, table: Optional[ScopeTable] = None,
+                          epsilon: float = DEFAULT_EPSILON, n_sms: int = 148) -> tuple[int, int, float]:
+    """Device-aware choice of p for the B200 path (not in the reference):
+    returns (p, r, modelled microseconds per transform).  Pass p to build_plan."""
+    p = C.c_uint64()
+    r = C.c_int()
+    est = C.c_double()
+    _check(lib().pft_select_divisor_device(_table(table).handle, int(N), int(M), float(epsilon), int(n_sms),
+                                           C.byref(p), C.byref(r), C.byref(est)))
+    return p.value, r.value, est.value
+
+
+def autotune_divisor(N: int, M: int, mu: int, d_in: int, table: Optional[ScopeTable] = None,
+                     epsilon: float = DEFAULT_EPSILON, device: int = 0, candidates: int = 4) -> tuple[int, float]:
+    """Measured choice of p: times the `candidates` best modelled divisors on the device with the
+    caller's input (device pointer to N complex128); returns (p, microseconds per transform)."""
+    p = C.c_uint64()
+    us = C.c_double()
+    _check(lib().pft_autotune_divisor(_table(table).handle, int(N), int(M), int(mu), float(epsilon), int(device),
+                                      C.c_void_p(int(d_in)), int(candidates), C.byref(p), C.byref(us)))
+    return p.value, us.value
 
 
 class PftPlan:

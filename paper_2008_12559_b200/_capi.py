@@ -70,6 +70,8 @@ SIGNATURES: dict[str, tuple] = {
     "pft_divisors": (ST, [U64, P, SZ, C.POINTER(SZ)]),
     "pft_min_terms": (ST, [P, D, U64, U64, C.POINTER(I)]),
     "pft_select_divisor": (ST, [P, U64, U64, D, C.POINTER(U64), C.POINTER(I), PD]),
+    "pft_select_divisor_device": (ST, [P, U64, U64, D, I, C.POINTER(U64), C.POINTER(I), PD]),
+    "pft_autotune_divisor": (ST, [P, U64, U64, I64, D, I, P, I, C.POINTER(U64), PD]),
     "pft_plan_build": (ST, [P, U64, U64, I64, U64, D, C.POINTER(P)]),
     "pft_plan_destroy": (None, [P]),
     "pft_plan_info_get": (ST, [P, C.POINTER(PlanInfo)]),

@@ -82,6 +82,35 @@ bool k2_fft_feasible(uint64_t P2, int r) {
     return pftdev::k2_smem_bytes(r, (uint32_t)P2) <= kK2SmemLimit;
 }
 
+// P2 for the sum tail: at most one K1 CTA per SM per transform, so under PDL two transforms
+// stream side by side (measured C2b p = 2^14: P2 = 128 42.5 us vs P2 = 256 46.5 us; C4
+// p = 27648: 128 21.7 us, 144 22.9 us, 256 27.7 us).  Among divisors P2 <= n_sms whose
+// P1 = p / P2 keeps two K1 CTAs per SM and fits the tail scratch: prefer P1 >= K1_BR (a
+// box's 32 rows all belong to the CTA; P1 = 16 measured 62 vs 38 us at C2a), then the
+// largest P2, taking a power of two if within 15% of it.  0 = none.
+bool sum_p1_ok(uint64_t P1, int r, uint64_t P2) {
+    if (!k1_feasible(P1, r)) return false;
+    if (pftdev::k1_smem_bytes(r, (uint32_t)P1, pftdev::K1_MIN_STAGES) > (228 * 1024) / 2 - 1024) return false;
+    return sizeof(double2) * r * P1 + pftdev::k1_sum_scratch_bytes((uint32_t)P1, (uint32_t)P2) <=
+           (size_t)pftdev::K1_MIN_STAGES * pftdev::K1_STAGE_BYTES;
+}
+
+uint64_t choose_p2_sum(uint64_t p, int r, int n_sms) {
+    for (int pass = 0; pass < 2; ++pass) {  // pass 0: P1 >= K1_BR only
+        uint64_t any = 0, pow2 = 0;
+        for (uint64_t d : divisors(p)) {
+            if (d > (uint64_t)n_sms) break;
+            const uint64_t P1 = p / d;
+            if (pass == 0 && P1 < (uint64_t)pftdev::K1_BR) continue;
+            if (!sum_p1_ok(P1, r, d)) continue;
+            any = d;
+            if ((d & (d - 1)) == 0) pow2 = d;
+        }
+        if (any) return (pow2 && 100 * pow2 >= 85 * any) ? pow2 : any;
+    }
+    return 0;
+}
+
 // Choose P2 | p (K1 grid = P2 x batch CTAs; P1 = p / P2 is K1's in-CTA FFT length, P2 is
 // K2's).  Prefer decompositions where both FFT passes fit shared memory, then the
 // smallest P2 that still gives >= kTargetCtas CTAs (fewer residue classes = less K2 work).
@@ -99,6 +128,72 @@ uint64_t choose_p2(uint64_t p, int r, size_t batch) {
         if (best) return best;
     }
     return p;
+}
+
+// Device-aware choice of p (not in the reference).  SPEC's cost
+// r (N + p log p + M) models a CPU; here the transform is one streaming pass whose time is set
+// by HBM and by the FP64 issue rate of the paired contraction, with the decomposition the
+// device plan would pick for that p:
+//   t_mem  = 16 N / bw * pad(q) * (1 + 48 / q) / rows(P1)   pad: TMA chunks of 16 column pairs;
+//                                                           bw = min(BW, 55 GB/s per K1 CTA)
+//   t_fp   = N (3r + 10) / 2 / F / rows(P1)                 rows: P1 / (32 ceil(P1 / 32)), the
+//                                                           used share of a box's 32 rows
+//   t_tail = 32 W P2 / BW                if W <= p/4 (sum tail: rows written + reduced in L2)
+//          = 8 us + 32 p r / BW          otherwise (slab + K2)
+//   t      = 2 us + max(t_mem, t_fp) + t_tail
+// BW = F = 6.6e12 (bytes/s, element-ops/s), calibrated on one B200 at N = 2^24, M = 2^10 where
+// p = 2^13 (r = 10) is FP64-bound and p = 2^14..2^16 follow the row term (measured 51.8, 42.5,
+// 45.1, 48.4 us; model 51.6, 44.6, 46.3, 51.0).
+std::vector<DivisorChoice> rank_divisors_device(const Table& t, uint64_t N, uint64_t M, double eps, int n_sms) {
+    if (N <= 1) fail(PFT_ERR_INVALID_ARGUMENT, "select_divisor_device: N = 1 has no non-trivial split");
+    if (M > N) fail(PFT_ERR_INVALID_ARGUMENT, "select_divisor_device: M > N");
+    if (!t.has_eps(eps)) fail(PFT_ERR_EPSILON_NOT_IN_TABLE, "select_divisor_device: table has no entries for epsilon");
+    constexpr double BW = 6.6e12, F = 6.6e12;
+    const uint64_t W = 2 * M + 1;
+    const double n = static_cast<double>(N);
+    std::vector<DivisorChoice> all;
+    for (uint64_t p : divisors(N)) {
+        if (p <= 1) continue;
+        int r;
+        try {
+            r = min_terms(t, eps, M, p);
+        } catch (const Error& e) {
+            if (e.status == PFT_ERR_RATIO_OUT_OF_RANGE) continue;
+            throw;
+        }
+        const uint64_t q = N / p;
+        if (q < 2) continue;
+        const bool sum = 4 * W <= p;
+        uint64_t P2 = sum ? choose_p2_sum(p, r, n_sms) : 0;
+        if (!P2) P2 = choose_p2(p, r, 1);
+        const uint64_t P1 = p / P2;
+        if (!k1_feasible(P1, r)) continue;
+        const double rows = static_cast<double>(P1) / (32.0 * static_cast<double>((P1 + 31) / 32));
+        const uint64_t pairs = q / 2, chunks = (pairs + 15) / 16;
+        const double pad = pairs ? 16.0 * static_cast<double>(chunks) / static_cast<double>(pairs) : 1.0;
+        // a K1 CTA streams at most ~55 GB/s (ring depth / latency); with the sum tail two
+        // transforms' grids are in flight under PDL
+        const double ctas = static_cast<double>(sum ? 2 * P2 : std::min<uint64_t>(P2, 2ull * n_sms));
+        const double bw = std::min(BW, 55e9 * ctas);
+        const double t_mem = 16.0 * n / bw * pad * (1.0 + 48.0 / static_cast<double>(q)) / rows;
+        const double t_fp = n * (3.0 * r + 10.0) / 2.0 / F / rows;
+        const double t_tail = (sum && choose_p2_sum(p, r, n_sms)) ? 32.0 * static_cast<double>(W * P2) / BW
+                                                                 : 8e-6 + 32.0 * static_cast<double>(p) * r / BW;
+        const double cost = 2e-6 + std::max(t_mem, t_fp) + t_tail;
+        DivisorChoice c;
+        c.p = p;
+        c.r = r;
+        c.cost = cost * 1e6;  // microseconds
+        all.push_back(c);
+    }
+    if (all.empty()) fail(PFT_ERR_RATIO_OUT_OF_RANGE, "select_divisor_device: no feasible divisor p");
+    std::stable_sort(all.begin(), all.end(),
+                     [](const DivisorChoice& a, const DivisorChoice& b) { return a.cost < b.cost; });
+    return all;
+}
+
+DivisorChoice select_divisor_device(const Table& t, uint64_t N, uint64_t M, double eps, int n_sms) {
+    return rank_divisors_device(t, N, M, eps, n_sms).front();
 }
 
 }  // namespace
@@ -293,6 +388,79 @@ extern "C" {
 
 const char* pft_version(void) { return "pft-b200 " PFT_BUILD_DESC " sm_100a"; }
 
+pft_status pft_select_divisor_device(pft_table_t t, uint64_t N, uint64_t M, double eps, int n_sms, uint64_t* p,
+                                     int* r, double* est_us) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(t != nullptr, "null table handle");
+    PFT_REQUIRE(n_sms > 0, "n_sms must be positive");
+    const DivisorChoice c = select_divisor_device(t->table, N, M, eps, n_sms);
+    if (p) *p = c.p;
+    if (r) *r = c.r;
+    if (est_us) *est_us = c.cost;
+    PFT_API_END
+}
+
+// Measured choice among the model's best candidates ("measured rather
+// than modelled"): each candidate p is planned, uploaded and timed over `reps` back-to-back
+// executes of the caller's device input on a private stream (after 3 warm-up executes).
+pft_status pft_autotune_divisor(pft_table_t t, uint64_t N, uint64_t M, int64_t mu, double eps, int device,
+                                const pft_c128* d_in, int n_candidates, uint64_t* p, double* us) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(t != nullptr && d_in != nullptr && p != nullptr, "autotune_divisor: bad arguments");
+    PFT_REQUIRE(n_candidates >= 1, "autotune_divisor: n_candidates < 1");
+    const int ndev = usable_device_count();
+    if (ndev == 0) fail(PFT_ERR_NO_DEVICE, "no CUDA device visible (this library has no CPU fallback)");
+    PFT_REQUIRE(device >= 0 && device < ndev, "autotune_divisor: device ordinal out of range");
+    DeviceGuard guard(device);
+    cudaDeviceProp prop{};
+    cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    const auto ranked = rank_divisors_device(t->table, N, M, eps, prop.multiProcessorCount);
+    struct Res {
+        cudaStream_t st = nullptr;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        double2* out = nullptr;
+        ~Res() {
+            if (out) cudaFree(out);
+            if (e0) cudaEventDestroy(e0);
+            if (e1) cudaEventDestroy(e1);
+            if (st) cudaStreamDestroy(st);
+        }
+    } res;
+    cuda_check(cudaStreamCreateWithFlags(&res.st, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreate(&res.e0), "cudaEventCreate");
+    cuda_check(cudaEventCreate(&res.e1), "cudaEventCreate");
+    cuda_check(cudaMalloc(&res.out, (2 * M + 1) * sizeof(double2)), "cudaMalloc(out)");
+    constexpr int reps = 20;
+    double best_us = 0.0;
+    uint64_t best_p = 0;
+    const size_t n = std::min<size_t>((size_t)n_candidates, ranked.size());
+    for (size_t i = 0; i < n; ++i) {
+        pft_hplan_s hp{build_plan(t->table, N, M, mu, ranked[i].p, eps)};
+        pft_dplan_opts o{};
+        o.device = device;
+        pft_dplan_t dpl = nullptr;
+        if (pft_dplan_create(&hp, &o, &dpl) != PFT_OK) continue;  // infeasible decomposition
+        std::unique_ptr<pft_dplan_s> guard_plan(dpl);
+        const auto* in = reinterpret_cast<const double2*>(d_in);
+        for (int w = 0; w < 3; ++w) run_execute(dpl, in, 1, N, res.out, dpl->d_ws, res.st);
+        cuda_check(cudaEventRecord(res.e0, res.st), "cudaEventRecord");
+        for (int k = 0; k < reps; ++k) run_execute(dpl, in, 1, N, res.out, dpl->d_ws, res.st);
+        cuda_check(cudaEventRecord(res.e1, res.st), "cudaEventRecord");
+        cuda_check(cudaEventSynchronize(res.e1), "cudaEventSynchronize");
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, res.e0, res.e1), "cudaEventElapsedTime");
+        const double per = 1e3 * ms / reps;
+        if (best_p == 0 || per < best_us) {
+            best_us = per;
+            best_p = ranked[i].p;
+        }
+    }
+    if (best_p == 0) fail(PFT_ERR_UNSUPPORTED, "autotune_divisor: no candidate could be planned on the device");
+    *p = best_p;
+    if (us) *us = best_us;
+    PFT_API_END
+}
+
 pft_status pft_device_count(int* n) {
     PFT_API_BEGIN
     PFT_REQUIRE(n != nullptr, "n is null");
@@ -329,7 +497,11 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     d->host.achieved_epsilon = H.achieved_epsilon;
     d->host.plan_id = H.plan_id;
     d->W = 2 * H.M + 1;
-    const uint64_t p2 = (opts && opts->p2) ? opts->p2 : choose_p2(H.p, H.r, 1);
+    const int forced_mode = opts ? opts->reserved[0] : 0;
+    uint64_t p2 = opts && opts->p2 ? opts->p2 : 0;
+    if (!p2 && (forced_mode == 0 || forced_mode == 5) && 4 * d->W <= H.p)
+        p2 = choose_p2_sum(H.p, H.r, prop.multiProcessorCount);  // sum tail
+    if (!p2) p2 = choose_p2(H.p, H.r, 1);
     if (p2 == 0 || H.p % p2 != 0) fail(PFT_ERR_INVALID_ARGUMENT, "dplan_create: p2 must divide p");
     d->P2 = p2;
     d->P1 = H.p / p2;
@@ -374,7 +546,7 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         const bool sum_ok = 4 * d->W <= H.p &&
                             sizeof(double2) * H.r * d->P1 + pftdev::k1_sum_scratch_bytes((uint32_t)d->P1, (uint32_t)d->P2) <=
                                 (size_t)pftdev::K1_MIN_STAGES * pftdev::K1_STAGE_BYTES;
-        d->sum_tail = sum_ok && (forced == 5 || (forced == 0 && d->k2_mode != pftdev::K2_L2));
+        d->sum_tail = sum_ok && (forced == 5 || forced == 0);
         // reducing CTAs per signal: one per 64 outputs (measured best at C2b/C4: 32; more
         // reducers hold more SM slots from the next transform), opts override
         d->reducers = (uint32_t)std::min<uint64_t>(d->P2, std::max<uint64_t>(1, (d->W + 63) / 64));

@@ -190,3 +190,17 @@ def test_nonfinite_input_is_reported(pft):
     assert e.value.status == 7
     a[1234] = 0.5  # the plan stays usable afterwards
     assert np.all(np.isfinite(pft.execute(plan, a).values))
+
+
+def test_autotuned_divisor_plan_parity(pft, oracle):
+    """pft_autotune_divisor times the model's best candidates on the device and returns one of
+    them; the plan it picks passes the parity gate like any other."""
+    import torch
+    N, M, mu = 2 ** 20, 200, -999
+    a = pft.generate_signal(pft.KIND_UNIFORM, 21, N)
+    x = torch.from_numpy(a).cuda()
+    p, us = pft.autotune_divisor(N, M, mu, x.data_ptr(), candidates=3)
+    assert N % p == 0 and us > 0
+    plan = pft.build_plan(N, M, mu, p, 1e-12)
+    got = pft.execute(plan, a).values
+    assert rel_l2(got, oracle.execute(plan, a)) <= GATE

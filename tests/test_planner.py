@@ -89,6 +89,21 @@ def test_spec_cost_model_picks_match_survey(pft):
         assert (got, est.r) == (p, r), (N, M)
 
 
+def test_device_divisor_model(pft):
+    """pft_select_divisor_device (B200 time model, DESIGN.md §2 'Plan choice'): a valid divisor
+    whose r is min_terms(p); at the calibration point (C2b) it picks the measured-best p = 2^14
+    (SPEC's CPU model picks 2^16)."""
+    for N, M in [(2 ** 20, 64), (2 ** 24, 64), (2 ** 24, 1024), (2 ** 24, 16384), (2 ** 16, 256),
+                 (6220800, 1000), (2 ** 30, 4096), (32000, 100)]:
+        p, r, est = pft.select_divisor_device(N, M)
+        assert N % p == 0 and 1 < p < N
+        assert r == pft.min_terms(1e-12, M, p)
+        assert est > 0
+    assert pft.select_divisor_device(2 ** 24, 1024)[0] == 2 ** 14
+    with pytest.raises(ValueError):
+        pft.select_divisor_device(2 ** 20, 64, n_sms=0)
+
+
 def test_cost_model_sanity(pft):
     """the selected p minimises r (N + p log2 p + M) over all valid divisors."""
     for N, M in [(2 ** 20, 512), (32000, 100), (6220800, 1000)]:

@@ -134,6 +134,32 @@ if __name__ == "__main__":
             for red in (0, 20, 24, 40, 48):
                 time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 15, label=f"C2b sum red={red}", red=red, reps=500)
                 time_plan(6220800, 1000, -12345, 62208, label=f"C4 sum red={red}", red=red, reps=500)
+    if which == "psweep":
+        for rep in range(2):
+            for pp, p2 in ((2 ** 15, 256), (2 ** 15, 512), (2 ** 16, 256), (2 ** 16, 512), (2 ** 14, 256), (2 ** 14, 128)):
+                time_plan(2 ** 24, 2 ** 10, 2 ** 22, pp, p2=p2, label=f"C2b p={pp} P2={p2}", reps=500)
+            for pp, p2 in ((62208, 256), (62208, 243), (27648, 256), (62208, 324)):
+                time_plan(6220800, 1000, -12345, pp, p2=p2, label=f"C4 p={pp} P2={p2}", reps=500)
+    if which == "psweep2":
+        for rep in range(2):
+            for pp, p2 in ((2 ** 14, 128), (2 ** 15, 128), (2 ** 16, 128), (2 ** 13, 128), (2 ** 14, 64), (2 ** 15, 64)):
+                time_plan(2 ** 24, 2 ** 10, 2 ** 22, pp, p2=p2, label=f"C2b p={pp} P2={p2}", reps=500)
+            for pp, p2 in ((27648, 128), (27648, 144), (27648, 216), (62208, 128), (62208, 144), (62208, 162)):
+                time_plan(6220800, 1000, -12345, pp, p2=p2, label=f"C4 p={pp} P2={p2}", reps=500)
+            for pp, p2 in ((16384, 128), (16384, 64), (8192, 128), (4096, 64)):
+                time_plan(2 ** 20, 64, 0, pp, p2=p2, label=f"C1 p={pp} P2={p2}", reps=500)
+    if which == "dev":
+        for rep in range(2):
+            for pp in (2 ** 14, 2 ** 15):
+                time_plan(2 ** 24, 2 ** 10, 2 ** 22, pp, label=f"C2b p={pp}", reps=500)
+            for pp in (2048, 4096, 16384, 65536):
+                time_plan(2 ** 24, 2 ** 6, 2 ** 22, pp, label=f"C2a p={pp}", reps=500)
+            for pp in (32768, 65536, 262144):
+                time_plan(2 ** 24, 2 ** 14, 2 ** 22, pp, label=f"C2c p={pp}", reps=300)
+            for pp in (16200, 27648, 62208, 10368):
+                time_plan(6220800, 1000, -12345, pp, label=f"C4 p={pp}", reps=500)
+            for pp in (1024, 2048, 4096):
+                time_plan(2 ** 20, 64, 0, pp, label=f"C1 p={pp}", reps=500)
     if which == "fuse":
         for rep in range(2):
             for fz in (True, False):
