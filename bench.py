@@ -34,9 +34,11 @@ CONFIGS = {
     "c2a": (2 ** 24, 2 ** 6, 2 ** 22, None, "sparse", "BASELINE configs[1]: N=2^24, M=2^6, mu=N/4, 32 tones + CN noise"),
     "c2b": (2 ** 24, 2 ** 10, 2 ** 22, None, "sparse", "BASELINE configs[1]: N=2^24, M=2^10, mu=N/4, 32 tones + CN noise"),
     "c2c": (2 ** 24, 2 ** 14, 2 ** 22, None, "sparse", "BASELINE configs[1]: N=2^24, M=2^14, mu=N/4, 32 tones + CN noise"),
+    "c3": (2 ** 16, 256, 0, None, "uniform", "BASELINE configs[2]: 4096 signals x N=2^16, M=256, mu=0, U[-1,1] re/im"),
     "c4": (6220800, 1000, -12345, None, "normal", "BASELINE configs[3]: N=2^10 3^5 5^2, M=1000, mu=-12345, CN(0,1)"),
 }
-SEEDS = {"c1": 1, "c2a": 2, "c2b": 2, "c2c": 2, "c4": 4}
+BATCH = {"c3": 4096}
+SEEDS = {"c1": 1, "c2a": 2, "c2b": 2, "c2c": 2, "c3": 3, "c4": 4}
 EPS = 1e-12
 L2_BYTES = 126 * 1024 * 1024
 
@@ -119,14 +121,16 @@ def make_input_host(pft, cfg, N, mu, M, seed, kind):
     return pft.generate_signal(pft.KIND_NORMAL if kind == "normal" else pft.KIND_UNIFORM, seed, N)
 
 
-def make_input_device(pft, buf, N, mu, M, seed, kind, offset=0):
+def make_input_device(pft, buf, count, mu, M, seed, kind, offset=0, N=None):
+    """`count` elements at global element index `offset` (signal length N for the tones)."""
+    N = N or count
     if kind == "sparse":
         freqs, amps = pft.sparse_tones(seed, 32, mu - M, mu + M)
-        pft.generate_signal_device(buf.data_ptr(), pft.KIND_SPARSE, seed, N, N=N, offset=offset, freqs=freqs,
+        pft.generate_signal_device(buf.data_ptr(), pft.KIND_SPARSE, seed, count, N=N, offset=offset, freqs=freqs,
                                    amps=amps, sigma=1e-3)
     else:
         pft.generate_signal_device(buf.data_ptr(), pft.KIND_NORMAL if kind == "normal" else pft.KIND_UNIFORM, seed,
-                                   N, offset=offset)
+                                   count, offset=offset)
 
 
 def cpu_oracle_rate(pft_mod, plan, a, budget_s: float):
@@ -169,9 +173,12 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "PFT transforms/sec", "value": value, "unit": "transforms/s",
         "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": el / steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)",
-        "data": "synthetic",
-        "config": {"workload": desc, "p": plan.p, "q": plan.q, "r": plan.r, "epsilon": EPS},
+        "higher_is_better": True, "scaling": "strong" if BATCH.get(args.config, 1) > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
+        "config": {"workload": desc, "p": plan.p, "q": plan.q, "r": plan.r, "epsilon": EPS,
+                   "p_choice": "SPEC select_divisor (the reference's CPU cost model)",
+                   "sample": "each step = one signal" + (f" of the {BATCH[args.config]}-signal batch"
+                                                         if args.config in BATCH else "")},
         "input_gbs": value * 16 * N / 1e9,
         "cpu_baseline": {"value": value, "unit": "transforms/s", "cores": cores, "kind": "port",
                          "sample": f"{steps} full transforms (oracle/oracle.cpp, OpenMP {cores} threads)"},
@@ -195,45 +202,56 @@ def run_ours(args):
 
     N, M, mu, p, kind, desc = CONFIGS[args.config]
     W = 2 * M + 1
+    # batched config (C3): the fixed global batch is sharded by signal over the ranks, no
+    # communication (strong scaling); single-signal configs run one replica per GPU (weak)
+    B_total = BATCH.get(args.config, 1)
+    if B_total > 1 and B_total % world:
+        raise SystemExit(f"{args.config}: global batch {B_total} not divisible by {world} GPUs")
+    B = B_total // world if B_total > 1 else 1
+    scaling = "strong" if B_total > 1 else "weak"
 
-    # inputs: >= 2 buffers, together > 2x L2, rotated so no step re-reads a cached input
-    nbuf = max(2, -(-2 * L2_BYTES // (16 * N)))
-    bufs = [torch.empty(N, dtype=torch.complex128, device=dev) for _ in range(nbuf)]
+    # inputs: >= 2 buffers, together > 2x L2, rotated so no step re-reads a cached input (a
+    # batched input is one buffer far larger than L2)
+    nbuf = 1 if B > 1 else max(2, -(-2 * L2_BYTES // (16 * N)))
+    bufs = [torch.empty(N * B, dtype=torch.complex128, device=dev) for _ in range(nbuf)]
     for i, b in enumerate(bufs):
-        make_input_device(pft, b, N, mu, M, SEEDS[args.config] + 100 * rank, kind, offset=i * N)
+        make_input_device(pft, b, N * B, mu, M, SEEDS[args.config] + (0 if B > 1 else 100 * rank), kind,
+                          offset=(rank * B * N if B > 1 else i * N), N=N)
     p_src = "--p"
     if args.p:
         p = args.p
     elif p is None:  # device-aware planner: model-ranked candidates, timed on this GPU
-        p, tuned_us = pft.autotune_divisor(N, M, mu, bufs[0].data_ptr(), epsilon=EPS, device=local)
-        p_src = f"pft_autotune_divisor ({tuned_us:.1f} us/transform in the tuning run)"
+        p, tuned_us = pft.autotune_divisor(N, M, mu, bufs[0].data_ptr(), epsilon=EPS, device=local, batch=B)
+        p_src = f"pft_autotune_divisor ({tuned_us:.1f} us per execute in the tuning run)"
     else:
         p_src = "config"
     plan = pft.build_plan(N, M, mu, p, EPS)
-    d = pft.DevicePlan(plan, device=local, p2=args.p2, pdl=not args.no_pdl, fuse=args.fuse)
+    d = pft.DevicePlan(plan, device=local, p2=args.p2, pdl=not args.no_pdl, fuse=args.fuse, batch_hint=B)
     launches = d.launches_per_execute()
-    out = torch.empty(W, dtype=torch.complex128, device=dev)
+
     stream = torch.cuda.Stream(device=dev)
     sp = stream.cuda_stream
     # Independent transforms alternate between two streams, each with its own workspace and
     # output (pft_execute is re-entrant on distinct (stream, workspace) pairs), so one
     # transform's K2 and K1 FFT tail overlap the next transform's streaming K1.
     side = torch.cuda.Stream(device=dev)
-    ws_elems = -(-d.workspace_bytes(1) // 16)
-    ws = [torch.zeros(ws_elems, dtype=torch.complex128, device=dev) for _ in range(2)]  # zeroed once
-    outs = [out, torch.empty(W, dtype=torch.complex128, device=dev)]
+    ws_elems = -(-d.workspace_bytes(B) // 16)
+    ws = [torch.zeros(ws_elems, dtype=torch.complex128, device=dev) for _ in range(args.streams)]  # zeroed once
+    outs = [torch.empty(W * B, dtype=torch.complex128, device=dev) for _ in range(2)]
+    out = outs[0]
     fork, join = torch.cuda.Event(), torch.cuda.Event()
 
     def step(i):
         if args.streams == 1:
-            d.execute_ptr(bufs[i % nbuf].data_ptr(), out.data_ptr(), stream=sp)
+            d.execute_ptr(bufs[i % nbuf].data_ptr(), out.data_ptr(), batch=B, in_stride=N,
+                          d_ws=ws[0].data_ptr(), stream=sp)
             return
         if i % 2 == 0:
             fork.record(stream)
             side.wait_event(fork)
         st = stream if i % 2 == 0 else side
-        d.execute_ptr(bufs[i % nbuf].data_ptr(), outs[i % 2].data_ptr(), d_ws=ws[i % 2].data_ptr(),
-                      stream=st.cuda_stream)
+        d.execute_ptr(bufs[i % nbuf].data_ptr(), outs[i % 2].data_ptr(), batch=B, in_stride=N,
+                      d_ws=ws[i % 2].data_ptr(), stream=st.cuda_stream)
         if i % 2 == 1 or i == args.steps - 1:
             join.record(st)
             stream.wait_event(join)
@@ -273,27 +291,35 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
-    # single-transform latency (one stream, transforms back to back)
-    lat_graph = capture(lambda i: d.execute_ptr(bufs[i % nbuf].data_ptr(), out.data_ptr(), stream=sp),
-                        min(args.steps, 200))
-    latency_us = timed(lat_graph) / min(args.steps, 200) * 1e3
+    # single-execute latency (one stream, executes back to back)
+    n_lat = min(args.steps, 200)
+    lat_graph = capture(lambda i: d.execute_ptr(bufs[i % nbuf].data_ptr(), out.data_ptr(), batch=B, in_stride=N,
+                                                d_ws=ws[0].data_ptr(), stream=sp), n_lat)
+    latency_us = timed(lat_graph) / n_lat * 1e3
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * args.steps / (ms / 1e3)
+    value = world * B * args.steps / (ms / 1e3)
 
     # ---- roofline of the dominant kernel (K1).  With the sum tail (launches == 1) K1 is the
     # whole transform, so its average launch duration in the timed region is ms_step itself.
     # Otherwise K1 alone (execute_partial: K1 writing the slab), same stream, same inputs.
     peak, peak_src = measured_hbm_peak()
-    Yb = torch.empty(plan.p * plan.r, dtype=torch.complex128, device=dev)
-    n_k1 = min(args.steps, 200)
-    g1 = capture(lambda i: d.execute_partial_ptr(bufs[i % nbuf].data_ptr(), Yb.data_ptr(), stream=sp), n_k1)
-    k1_partial_ms = timed(g1) / n_k1
-    k1_ms = ms_step if launches == 1 else k1_partial_ms
-    k1_gbs = 16 * N / (k1_ms * 1e-3) / 1e9
+    k1_partial_ms = None
+    if B == 1:
+        Yb = torch.empty(plan.p * plan.r, dtype=torch.complex128, device=dev)
+        g1 = capture(lambda i: d.execute_partial_ptr(bufs[i % nbuf].data_ptr(), Yb.data_ptr(), stream=sp), n_lat)
+        k1_partial_ms = timed(g1) / n_lat
+    k1_ms = ms_step if (launches == 1 or k1_partial_ms is None) else k1_partial_ms
+    k1_gbs = 16 * N * B / (k1_ms * 1e-3) / 1e9
+    if launches == 1:
+        k1_note = "K1 is the only kernel of an execute (sum tail): achieved = 16 N B / ms_per_step"
+    elif k1_partial_ms is None:
+        k1_note = "batched K1+K2 step: achieved over the whole step (a lower bound for K1)"
+    else:
+        k1_note = "K1 timed alone (slab output) in a chain of launches"
 
     # parity spot-check of this run's output against the oracle is in tests/; here only
     # the non-finite status word is checked
@@ -304,14 +330,16 @@ def run_ours(args):
         # ---- e2e through the public host API (H2D of the input + D2H of the spectrum)
         e2e = None
         if not args.no_e2e:
-            h_in = torch.empty(N, dtype=torch.complex128, pin_memory=True)
-            h_in.copy_(bufs[0].cpu())
-            h_out = torch.empty(W, dtype=torch.complex128, pin_memory=True)
+            Be = min(B, 64)  # batched: a 64-signal slice per call keeps the pinned buffer small
+            h_in = torch.empty(N * Be, dtype=torch.complex128, pin_memory=True)
+            h_in.copy_(bufs[0][:N * Be].cpu())
+            h_out = torch.empty(W * Be, dtype=torch.complex128, pin_memory=True)
+            d_in2 = torch.empty(N * Be, dtype=torch.complex128, device=dev)
             import ctypes as C
             L = pft.lib()
             def e2e_call():
-                st = L.pft_execute_host(d.handle, C.c_void_p(h_in.data_ptr()), 1, C.c_void_p(h_out.data_ptr()),
-                                        C.c_void_p(bufs[1].data_ptr()), C.c_void_p(out.data_ptr()), C.c_void_p(sp))
+                st = L.pft_execute_host(d.handle, C.c_void_p(h_in.data_ptr()), Be, C.c_void_p(h_out.data_ptr()),
+                                        C.c_void_p(d_in2.data_ptr()), C.c_void_p(out.data_ptr()), C.c_void_p(sp))
                 if st != 0:
                     raise RuntimeError(f"pft_execute_host failed: {st}")
             for _ in range(2):
@@ -321,35 +349,38 @@ def run_ours(args):
             for _ in range(n_e2e):
                 e2e_call()
             el = time.perf_counter() - t0
-            e2e = {"value": n_e2e / el, "unit": "transforms/s", "h2d_bytes_per_step": 16 * N,
-                   "d2h_bytes_per_step": 16 * W, "steps": n_e2e, "timer": "host wall clock around synchronous "
-                   "pft_execute_host (pinned host buffers)"}
+            e2e = {"value": n_e2e * Be / el, "unit": "transforms/s", "h2d_bytes_per_step": 16 * N * Be,
+                   "d2h_bytes_per_step": 16 * W * Be, "steps": n_e2e, "signals_per_call": Be,
+                   "timer": "host wall clock around synchronous pft_execute_host (pinned host buffers)"}
         # ---- CPU baseline: the oracle on this host, bounded sample
         cpu = None
         if not args.no_cpu and world == 1:
             try:
-                a_host = bufs[0].cpu().numpy()
+                a_host = bufs[0][:N].cpu().numpy()
                 rate, n, el = cpu_oracle_rate(pft, plan, a_host, args.cpu_seconds)
                 cpu = {"value": rate, "unit": "transforms/s", "cores": os.cpu_count(), "kind": "port",
-                       "sample": f"{n} full {args.config} transforms in {el:.1f} s (oracle/oracle.cpp, "
-                                 f"OpenMP {os.cpu_count()} threads)"}
+                       "sample": f"{n} full {args.config} transforms (one signal each) in {el:.1f} s "
+                                 f"(oracle/oracle.cpp, OpenMP {os.cpu_count()} threads)"}
             except Exception as e:  # the baseline is reported, never required
                 cpu = {"value": None, "error": str(e)}
         line = {
             "metric": "PFT transforms/sec", "value": value, "unit": "transforms/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
             "config": {"workload": f"{args.config}: {desc}", "N": N, "M": M, "mu": mu, "epsilon": EPS,
+                       "global_batch": B_total, "batch_per_gpu": B,
                        "p": plan.p, "q": plan.q, "r": plan.r, "P1": d.P1, "P2": d.P2, "p_choice": p_src,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "l2": f"{nbuf} rotating inputs of {16 * N / 2**20:.0f} MiB (> L2 126 MiB)",
+                       "parallelism": (f"signals sharded over {world} GPUs" if B_total > 1 else
+                                       f"replicas x{world}") if world > 1 else "single GPU",
+                       "l2": (f"one batched input of {16 * N * B / 2**30:.2f} GiB (> L2 126 MiB)" if B > 1 else
+                              f"{nbuf} rotating inputs of {16 * N / 2**20:.0f} MiB (> L2 126 MiB)"),
                        "timing": "CUDA graph of K steps, CUDA events on the launch stream",
                        "streams": args.streams, "pdl": not args.no_pdl, "fused_k2": args.fuse,
-                       "tail": "sum tail in K1 (one kernel per transform)" if launches == 1 else
-                               f"K2 ({launches} kernels per transform)",
+                       "tail": "sum tail in K1 (one kernel per execute)" if launches == 1 else
+                               f"K2 ({launches} kernels per execute)",
                        "pipelining": "independent transforms alternate over 2 streams with separate "
                                      "workspaces" if args.streams == 2 else
-                                     "single stream; transform i+1's K1 starts streaming while transform "
+                                     "single stream; execute i+1's K1 starts streaming while execute "
                                      "i finishes, via programmatic dependent launch"},
             "latency_us_single_stream": latency_us,
             "input_gbs": value * 16 * N / 1e9,
@@ -357,11 +388,9 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": "k1_contract_fft", "achieved": k1_gbs, "peak": peak,
                          "unit": "GB/s", "frac": k1_gbs / peak, "peak_source": peak_src,
                          "traffic": committed_traffic(args.config),
-                         "algorithmic_bytes_per_launch": 16 * N, "k1_ms": k1_ms,
-                         "k1_share_of_step": k1_ms / ms_step,
-                         "k1_slab_only_ms": k1_partial_ms,
-                         "note": "K1 is the only kernel of a transform (sum tail): achieved = 16 N / ms_per_step"
-                                 if launches == 1 else "K1 timed alone (slab output) in a chain of launches"},
+                         "algorithmic_bytes_per_launch": 16 * N * B, "k1_ms": k1_ms,
+                         "k1_share_of_step": k1_ms / ms_step, "k1_slab_only_ms": k1_partial_ms,
+                         "note": k1_note},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches * args.steps,

@@ -105,9 +105,10 @@ pft_status pft_select_divisor(pft_table_t t, uint64_t N, uint64_t M, double epsi
 pft_status pft_select_divisor_device(pft_table_t t, uint64_t N, uint64_t M, double epsilon, int n_sms,
                                      uint64_t* p, int* r, double* est_us);
 /* Measured choice: times the n_candidates best modelled p on `device` with the caller's input
- * d_in (N complex128 on that device); returns the fastest p and its microseconds/transform. */
+ * d_in (batch x N complex128 on that device, signals contiguous); returns the fastest p and its
+ * microseconds per execute of the batch.                                                  */
 pft_status pft_autotune_divisor(pft_table_t t, uint64_t N, uint64_t M, int64_t mu, double epsilon, int device,
-                                const pft_c128* d_in, int n_candidates, uint64_t* p, double* us);
+                                const pft_c128* d_in, size_t batch, int n_candidates, uint64_t* p, double* us);
 
 typedef struct pft_hplan_s* pft_hplan_t;
 
@@ -154,7 +155,8 @@ typedef struct pft_dplan_opts {
     int device;        /* CUDA ordinal                                              */
     uint64_t p2;       /* residue classes for K1 (0 = auto); must divide p          */
     int k1_stages;     /* K1 TMA ring depth, 4..8 (0 = deepest that keeps 2 CTAs/SM) */
-    int reserved[6];
+    int reserved[6];   /* development A/B knobs, 0 = default (see DevicePlan in __init__.py) */
+    uint64_t batch_hint; /* typical batch per execute (0/1 = single signal): sizes the K1 grid */
 } pft_dplan_opts;
 
 /* Upload a host plan to the device.  opts may be NULL (defaults). */

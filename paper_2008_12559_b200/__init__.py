@@ -321,13 +321,15 @@ def select_divisor_device(N: int, M: int, table: Optional[ScopeTable] = None,
 
 
 def autotune_divisor(N: int, M: int, mu: int, d_in: int, table: Optional[ScopeTable] = None,
-                     epsilon: float = DEFAULT_EPSILON, device: int = 0, candidates: int = 4) -> tuple[int, float]:
+                     epsilon: float = DEFAULT_EPSILON, device: int = 0, candidates: int = 4,
+                     batch: int = 1) -> tuple[int, float]:
     """Measured choice of p: times the `candidates` best modelled divisors on the device with the
-    caller's input (device pointer to N complex128); returns (p, microseconds per transform)."""
+    caller's input (device pointer to batch x N complex128); returns (p, microseconds per execute
+    of the batch)."""
     p = C.c_uint64()
     us = C.c_double()
     _check(lib().pft_autotune_divisor(_table(table).handle, int(N), int(M), int(mu), float(epsilon), int(device),
-                                      C.c_void_p(int(d_in)), int(candidates), C.byref(p), C.byref(us)))
+                                      C.c_void_p(int(d_in)), int(batch), int(candidates), C.byref(p), C.byref(us)))
     return p.value, us.value
 
 
@@ -435,7 +437,7 @@ class DevicePlan:
     pointers (e.g. torch.Tensor.data_ptr() of complex128 CUDA tensors)."""
 
     def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0, k1_stages: int = 0, k2_mode: int = 0,
-                 k2_ctas: int = 0, pdl: bool = True, fuse: bool = False, reducers: int = 0):
+                 k2_ctas: int = 0, pdl: bool = True, fuse: bool = False, reducers: int = 0, batch_hint: int = 1):
         self.plan = plan
         opts = _capi.DPlanOpts()
         opts.device = device
@@ -446,6 +448,7 @@ class DevicePlan:
         opts.reserved[2] = 0 if pdl else 1  # PDL chaining of consecutive transforms
         opts.reserved[3] = 2 if fuse else 0  # K2 fused into K1's tail (grid barrier, opt-in)
         opts.reserved[4] = reducers  # sum tail: reducing CTAs per signal (0 = one per 64 outputs)
+        opts.batch_hint = batch_hint
         h = C.c_void_p()
         _check(lib().pft_dplan_create(plan.handle, C.byref(opts), C.byref(h)))
         self._h = h

@@ -25,7 +25,8 @@ class PlanInfo(C.Structure):
 
 
 class DPlanOpts(C.Structure):
-    _fields_ = [("device", C.c_int), ("p2", C.c_uint64), ("k1_stages", C.c_int), ("reserved", C.c_int * 6)]
+    _fields_ = [("device", C.c_int), ("p2", C.c_uint64), ("k1_stages", C.c_int), ("reserved", C.c_int * 6),
+                ("batch_hint", C.c_uint64)]
 
 
 class ShardInfo(C.Structure):
@@ -71,7 +72,7 @@ SIGNATURES: dict[str, tuple] = {
     "pft_min_terms": (ST, [P, D, U64, U64, C.POINTER(I)]),
     "pft_select_divisor": (ST, [P, U64, U64, D, C.POINTER(U64), C.POINTER(I), PD]),
     "pft_select_divisor_device": (ST, [P, U64, U64, D, I, C.POINTER(U64), C.POINTER(I), PD]),
-    "pft_autotune_divisor": (ST, [P, U64, U64, I64, D, I, P, I, C.POINTER(U64), PD]),
+    "pft_autotune_divisor": (ST, [P, U64, U64, I64, D, I, P, SZ, I, C.POINTER(U64), PD]),
     "pft_plan_build": (ST, [P, U64, U64, I64, U64, D, C.POINTER(P)]),
     "pft_plan_destroy": (None, [P]),
     "pft_plan_info_get": (ST, [P, C.POINTER(PlanInfo)]),

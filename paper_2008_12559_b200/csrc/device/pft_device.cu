@@ -95,7 +95,22 @@ bool sum_p1_ok(uint64_t P1, int r, uint64_t P2) {
            (size_t)pftdev::K1_MIN_STAGES * pftdev::K1_STAGE_BYTES;
 }
 
-uint64_t choose_p2_sum(uint64_t p, int r, int n_sms) {
+// The sum tail pays, per CTA, W outputs of r-term sums plus a W-long row written and reduced
+// through L2.  It is used when that stays small against the CTA's streaming work: the rows'
+// traffic 2 P2 W complex <= 1/8 of the input and the tail's ~(r + 20) W ops <= 10% of the
+// contraction's (3r + 10)/2 per element (C2b: 3% / 3%; C3 at p = 512: 3% / 2%).
+bool sum_tail_pays(uint64_t N, uint64_t W, uint64_t P2, int r) {
+    const double n = static_cast<double>(N), w = static_cast<double>(W), p2 = static_cast<double>(P2);
+    return 16.0 * p2 * w <= n && 10.0 * w * (r + 20) <= n / p2 * (3.0 * r + 10.0) / 2.0;
+}
+
+uint64_t choose_p2_sum(uint64_t p, int r, int n_sms, size_t batch) {
+    if (batch > 1) {
+        // batched signals supply the CTAs: give each CTA as many rows as fit (the smallest P2),
+        // keeping >= 2 CTAs per SM over the batch
+        for (uint64_t d : divisors(p))
+            if (d * batch >= 2ull * (uint64_t)n_sms && sum_p1_ok(p / d, r, d)) return d;
+    }
     for (int pass = 0; pass < 2; ++pass) {  // pass 0: P1 >= K1_BR only
         uint64_t any = 0, pow2 = 0;
         for (uint64_t d : divisors(p)) {
@@ -140,11 +155,14 @@ uint64_t choose_p2(uint64_t p, int r, size_t batch) {
 //                                                           used share of a box's 32 rows
 //   t_tail = 32 W P2 / BW                if W <= p/4 (sum tail: rows written + reduced in L2)
 //          = 8 us + 32 p r / BW          otherwise (slab + K2)
-//   t      = 2 us + max(t_mem, t_fp) + t_tail
+//   t      = 2 us + max(t_mem, t_fp) + t_tail          (per batch of signals: t_mem, t_fp, t_tail
+//                                                     scale with the batch, CTAs come from it)
 // BW = F = 6.6e12 (bytes/s, element-ops/s), calibrated on one B200 at N = 2^24, M = 2^10 where
 // p = 2^13 (r = 10) is FP64-bound and p = 2^14..2^16 follow the row term (measured 51.8, 42.5,
 // 45.1, 48.4 us; model 51.6, 44.6, 46.3, 51.0).
-std::vector<DivisorChoice> rank_divisors_device(const Table& t, uint64_t N, uint64_t M, double eps, int n_sms) {
+std::vector<DivisorChoice> rank_divisors_device(const Table& t, uint64_t N, uint64_t M, double eps, int n_sms,
+                                                size_t batch = 1) {
+    batch = std::max<size_t>(batch, 1);
     if (N <= 1) fail(PFT_ERR_INVALID_ARGUMENT, "select_divisor_device: N = 1 has no non-trivial split");
     if (M > N) fail(PFT_ERR_INVALID_ARGUMENT, "select_divisor_device: M > N");
     if (!t.has_eps(eps)) fail(PFT_ERR_EPSILON_NOT_IN_TABLE, "select_divisor_device: table has no entries for epsilon");
@@ -163,9 +181,9 @@ std::vector<DivisorChoice> rank_divisors_device(const Table& t, uint64_t N, uint
         }
         const uint64_t q = N / p;
         if (q < 2) continue;
-        const bool sum = 4 * W <= p;
-        uint64_t P2 = sum ? choose_p2_sum(p, r, n_sms) : 0;
-        if (!P2) P2 = choose_p2(p, r, 1);
+        uint64_t P2 = choose_p2_sum(p, r, n_sms, batch);
+        const bool sum = P2 && sum_tail_pays(N, W, P2, r);
+        if (!sum) P2 = choose_p2(p, r, batch);
         const uint64_t P1 = p / P2;
         if (!k1_feasible(P1, r)) continue;
         const double rows = static_cast<double>(P1) / (32.0 * static_cast<double>((P1 + 31) / 32));
@@ -173,13 +191,14 @@ std::vector<DivisorChoice> rank_divisors_device(const Table& t, uint64_t N, uint
         const double pad = pairs ? 16.0 * static_cast<double>(chunks) / static_cast<double>(pairs) : 1.0;
         // a K1 CTA streams at most ~55 GB/s (ring depth / latency); with the sum tail two
         // transforms' grids are in flight under PDL
-        const double ctas = static_cast<double>(sum ? 2 * P2 : std::min<uint64_t>(P2, 2ull * n_sms));
+        const double ctas = static_cast<double>(sum ? 2 * P2 * batch : std::min<uint64_t>(P2 * batch, 2ull * n_sms));
         const double bw = std::min(BW, 55e9 * ctas);
         const double t_mem = 16.0 * n / bw * pad * (1.0 + 48.0 / static_cast<double>(q)) / rows;
         const double t_fp = n * (3.0 * r + 10.0) / 2.0 / F / rows;
-        const double t_tail = (sum && choose_p2_sum(p, r, n_sms)) ? 32.0 * static_cast<double>(W * P2) / BW
-                                                                 : 8e-6 + 32.0 * static_cast<double>(p) * r / BW;
-        const double cost = 2e-6 + std::max(t_mem, t_fp) + t_tail;
+        const double nb = static_cast<double>(batch);
+        const double t_tail = sum ? 32.0 * static_cast<double>(W * P2) * nb / BW
+                                  : (batch > 1 ? 0.0 : 8e-6) + 32.0 * static_cast<double>(p) * r * nb / BW;
+        const double cost = 2e-6 + nb * std::max(t_mem, t_fp) + t_tail;
         DivisorChoice c;
         c.p = p;
         c.r = r;
@@ -404,7 +423,7 @@ pft_status pft_select_divisor_device(pft_table_t t, uint64_t N, uint64_t M, doub
 // than modelled"): each candidate p is planned, uploaded and timed over `reps` back-to-back
 // executes of the caller's device input on a private stream (after 3 warm-up executes).
 pft_status pft_autotune_divisor(pft_table_t t, uint64_t N, uint64_t M, int64_t mu, double eps, int device,
-                                const pft_c128* d_in, int n_candidates, uint64_t* p, double* us) {
+                                const pft_c128* d_in, size_t batch, int n_candidates, uint64_t* p, double* us) {
     PFT_API_BEGIN
     PFT_REQUIRE(t != nullptr && d_in != nullptr && p != nullptr, "autotune_divisor: bad arguments");
     PFT_REQUIRE(n_candidates >= 1, "autotune_divisor: n_candidates < 1");
@@ -414,12 +433,16 @@ pft_status pft_autotune_divisor(pft_table_t t, uint64_t N, uint64_t M, int64_t m
     DeviceGuard guard(device);
     cudaDeviceProp prop{};
     cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
-    const auto ranked = rank_divisors_device(t->table, N, M, eps, prop.multiProcessorCount);
+    batch = std::max<size_t>(batch, 1);
+    PFT_REQUIRE(batch <= 65535, "autotune_divisor: batch > 65535");
+    const auto ranked = rank_divisors_device(t->table, N, M, eps, prop.multiProcessorCount, batch);
     struct Res {
         cudaStream_t st = nullptr;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         double2* out = nullptr;
+        void* ws = nullptr;
         ~Res() {
+            if (ws) cudaFree(ws);
             if (out) cudaFree(out);
             if (e0) cudaEventDestroy(e0);
             if (e1) cudaEventDestroy(e1);
@@ -429,8 +452,8 @@ pft_status pft_autotune_divisor(pft_table_t t, uint64_t N, uint64_t M, int64_t m
     cuda_check(cudaStreamCreateWithFlags(&res.st, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaEventCreate(&res.e0), "cudaEventCreate");
     cuda_check(cudaEventCreate(&res.e1), "cudaEventCreate");
-    cuda_check(cudaMalloc(&res.out, (2 * M + 1) * sizeof(double2)), "cudaMalloc(out)");
-    constexpr int reps = 20;
+    cuda_check(cudaMalloc(&res.out, (2 * M + 1) * batch * sizeof(double2)), "cudaMalloc(out)");
+    const int reps = batch > 1 ? 3 : 20;
     double best_us = 0.0;
     uint64_t best_p = 0;
     const size_t n = std::min<size_t>((size_t)n_candidates, ranked.size());
@@ -438,13 +461,23 @@ pft_status pft_autotune_divisor(pft_table_t t, uint64_t N, uint64_t M, int64_t m
         pft_hplan_s hp{build_plan(t->table, N, M, mu, ranked[i].p, eps)};
         pft_dplan_opts o{};
         o.device = device;
+        o.batch_hint = batch;
         pft_dplan_t dpl = nullptr;
         if (pft_dplan_create(&hp, &o, &dpl) != PFT_OK) continue;  // infeasible decomposition
         std::unique_ptr<pft_dplan_s> guard_plan(dpl);
         const auto* in = reinterpret_cast<const double2*>(d_in);
-        for (int w = 0; w < 3; ++w) run_execute(dpl, in, 1, N, res.out, dpl->d_ws, res.st);
+        double2* ws = dpl->d_ws;
+        if (batch > 1) {
+            if (res.ws) cudaFree(res.ws);
+            res.ws = nullptr;
+            const size_t wb = dpl->workspace_bytes(batch);
+            cuda_check(cudaMalloc(&res.ws, wb), "cudaMalloc(workspace)");
+            cuda_check(cudaMemset(res.ws, 0, wb), "cudaMemset(workspace)");
+            ws = static_cast<double2*>(res.ws);
+        }
+        for (int w = 0; w < 3; ++w) run_execute(dpl, in, batch, N, res.out, ws, res.st);
         cuda_check(cudaEventRecord(res.e0, res.st), "cudaEventRecord");
-        for (int k = 0; k < reps; ++k) run_execute(dpl, in, 1, N, res.out, dpl->d_ws, res.st);
+        for (int k = 0; k < reps; ++k) run_execute(dpl, in, batch, N, res.out, ws, res.st);
         cuda_check(cudaEventRecord(res.e1, res.st), "cudaEventRecord");
         cuda_check(cudaEventSynchronize(res.e1), "cudaEventSynchronize");
         float ms = 0.f;
@@ -499,9 +532,12 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     d->W = 2 * H.M + 1;
     const int forced_mode = opts ? opts->reserved[0] : 0;
     uint64_t p2 = opts && opts->p2 ? opts->p2 : 0;
-    if (!p2 && (forced_mode == 0 || forced_mode == 5) && 4 * d->W <= H.p)
-        p2 = choose_p2_sum(H.p, H.r, prop.multiProcessorCount);  // sum tail
-    if (!p2) p2 = choose_p2(H.p, H.r, 1);
+    const size_t batch_hint = opts && opts->batch_hint > 1 ? (size_t)opts->batch_hint : 1;
+    if (!p2 && (forced_mode == 0 || forced_mode == 5)) {  // sum tail, when it pays (or forced)
+        p2 = choose_p2_sum(H.p, H.r, prop.multiProcessorCount, batch_hint);
+        if (p2 && forced_mode == 0 && !sum_tail_pays(H.N, d->W, p2, H.r)) p2 = 0;
+    }
+    if (!p2) p2 = choose_p2(H.p, H.r, batch_hint);
     if (p2 == 0 || H.p % p2 != 0) fail(PFT_ERR_INVALID_ARGUMENT, "dplan_create: p2 must divide p");
     d->P2 = p2;
     d->P1 = H.p / p2;
@@ -540,13 +576,13 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         d->k2_ctas = opts && opts->reserved[1] > 0 ? (uint32_t)opts->reserved[1] : 0;
         d->pdl_chain = !(opts && opts->reserved[2] == 1);  // reserved[2] == 1: plain stream order
         d->allow_fuse = opts && opts->reserved[3] == 2;
-        // Sum tail when the outputs are few relative to p (W <= p/4): K1 finishes the
-        // transform itself (see k1_sum_tail).  Needs the ring to hold the FFT scratch and the
-        // reduction scratch.  Forced off by modes 1-4, forced on (if feasible) by 5.
-        const bool sum_ok = 4 * d->W <= H.p &&
-                            sizeof(double2) * H.r * d->P1 + pftdev::k1_sum_scratch_bytes((uint32_t)d->P1, (uint32_t)d->P2) <=
-                                (size_t)pftdev::K1_MIN_STAGES * pftdev::K1_STAGE_BYTES;
-        d->sum_tail = sum_ok && (forced == 5 || forced == 0);
+        // Sum tail when it pays (sum_tail_pays): K1 finishes the transform itself (see
+        // k1_sum_tail).  Needs the ring to hold the FFT scratch and the tail scratch.  Forced
+        // off by modes 1-4, forced on (if feasible) by 5.
+        const bool fits = sizeof(double2) * H.r * d->P1 +
+                              pftdev::k1_sum_scratch_bytes((uint32_t)d->P1, (uint32_t)d->P2) <=
+                          (size_t)pftdev::K1_MIN_STAGES * pftdev::K1_STAGE_BYTES;
+        d->sum_tail = fits && (forced == 5 || (forced == 0 && sum_tail_pays(H.N, d->W, d->P2, H.r)));
         // reducing CTAs per signal: one per 64 outputs (measured best at C2b/C4: 32; more
         // reducers hold more SM slots from the next transform), opts override
         d->reducers = (uint32_t)std::min<uint64_t>(d->P2, std::max<uint64_t>(1, (d->W + 63) / 64));
