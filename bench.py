@@ -36,9 +36,12 @@ CONFIGS = {
     "c2c": (2 ** 24, 2 ** 14, 2 ** 22, None, "sparse", "BASELINE configs[1]: N=2^24, M=2^14, mu=N/4, 32 tones + CN noise"),
     "c3": (2 ** 16, 256, 0, None, "uniform", "BASELINE configs[2]: 4096 signals x N=2^16, M=256, mu=0, U[-1,1] re/im"),
     "c4": (6220800, 1000, -12345, None, "normal", "BASELINE configs[3]: N=2^10 3^5 5^2, M=1000, mu=-12345, CN(0,1)"),
+    "c5": (2 ** 30, 2 ** 12, 0, None, "uniform", "BASELINE configs[4]: N=2^30, M=2^12, mu=0, U[-1,1] re/im; "
+                                                 "contraction-axis sharded over the GPUs"),
 }
+SHARDED = {"c5"}  # one transform split along the contraction axis when run on > 1 GPU
 BATCH = {"c3": 4096}
-SEEDS = {"c1": 1, "c2a": 2, "c2b": 2, "c2c": 2, "c3": 3, "c4": 4}
+SEEDS = {"c1": 1, "c2a": 2, "c2b": 2, "c2c": 2, "c3": 3, "c4": 4, "c5": 5}
 EPS = 1e-12
 L2_BYTES = 126 * 1024 * 1024
 
@@ -155,6 +158,10 @@ def run_reference(args):
     import oracle
     import paper_2008_12559_b200 as pft
     N, M, mu, p, kind, desc = CONFIGS[args.config]
+    if 16 * N > 4 * 2 ** 30:
+        print(json.dumps({"impl": "reference", "unavailable": f"{args.config}: one CPU transform of a "
+                          f"{16 * N / 2**30:.0f} GiB signal exceeds the bounded per-step sample"}), flush=True)
+        return
     plan = pft.build_plan(N, M, mu, p, EPS)
     a = make_input_host(pft, args.config, N, mu, M, SEEDS[args.config], kind)
     cores = os.cpu_count()
@@ -199,6 +206,8 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if args.config in SHARDED and world > 1:
+        return run_sharded(args, world, rank, local, dev)
 
     N, M, mu, p, kind, desc = CONFIGS[args.config]
     W = 2 * M + 1
@@ -212,7 +221,7 @@ def run_ours(args):
 
     # inputs: >= 2 buffers, together > 2x L2, rotated so no step re-reads a cached input (a
     # batched input is one buffer far larger than L2)
-    nbuf = 1 if B > 1 else max(2, -(-2 * L2_BYTES // (16 * N)))
+    nbuf = 1 if (B > 1 or 16 * N >= 16 * L2_BYTES) else max(2, -(-2 * L2_BYTES // (16 * N)))
     bufs = [torch.empty(N * B, dtype=torch.complex128, device=dev) for _ in range(nbuf)]
     for i, b in enumerate(bufs):
         make_input_device(pft, b, N * B, mu, M, SEEDS[args.config] + (0 if B > 1 else 100 * rank), kind,
@@ -329,7 +338,10 @@ def run_ours(args):
     if rank == 0:
         # ---- e2e through the public host API (H2D of the input + D2H of the spectrum)
         e2e = None
-        if not args.no_e2e:
+        huge = 16 * N > 4 * 2 ** 30  # C5: a host copy / pinned buffer of the whole signal is not sampled
+        if huge:
+            e2e = {"value": None, "skipped": "input > 4 GiB: no pinned host copy in the bench"}
+        if not args.no_e2e and not huge:
             Be = min(B, 64)  # batched: a 64-signal slice per call keeps the pinned buffer small
             h_in = torch.empty(N * Be, dtype=torch.complex128, pin_memory=True)
             h_in.copy_(bufs[0][:N * Be].cpu())
@@ -354,7 +366,9 @@ def run_ours(args):
                    "timer": "host wall clock around synchronous pft_execute_host (pinned host buffers)"}
         # ---- CPU baseline: the oracle on this host, bounded sample
         cpu = None
-        if not args.no_cpu and world == 1:
+        if huge:
+            cpu = {"value": None, "skipped": "input > 4 GiB: one oracle transform exceeds the bounded sample"}
+        if not args.no_cpu and world == 1 and not huge:
             try:
                 a_host = bufs[0][:N].cpu().numpy()
                 rate, n, el = cpu_oracle_rate(pft, plan, a_host, args.cpu_seconds)
@@ -372,7 +386,7 @@ def run_ours(args):
                        "p": plan.p, "q": plan.q, "r": plan.r, "P1": d.P1, "P2": d.P2, "p_choice": p_src,
                        "parallelism": (f"signals sharded over {world} GPUs" if B_total > 1 else
                                        f"replicas x{world}") if world > 1 else "single GPU",
-                       "l2": (f"one batched input of {16 * N * B / 2**30:.2f} GiB (> L2 126 MiB)" if B > 1 else
+                       "l2": (f"one input of {16 * N * B / 2**30:.2f} GiB (> L2 126 MiB)" if nbuf == 1 else
                               f"{nbuf} rotating inputs of {16 * N / 2**20:.0f} MiB (> L2 126 MiB)"),
                        "timing": "CUDA graph of K steps, CUDA events on the launch stream",
                        "streams": args.streams, "pdl": not args.no_pdl, "fused_k2": args.fuse,
@@ -401,6 +415,79 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_sharded(args, world, rank, local, dev):
+    """One huge transform split along the contraction axis: every rank
+    runs K1 on its column slice into a partial slab, NCCL reduces the slabs onto rank 0, which
+    runs K2.  Strong scaling: value = whole-job transforms/s, time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import paper_2008_12559_b200 as pft
+    from paper_2008_12559_b200.sharded import ShardedTransform, gather_local_device
+
+    N, M, mu, p, kind, desc = CONFIGS[args.config]
+    W = 2 * M + 1
+    p = args.p or pft.select_divisor_device(N, M, epsilon=EPS)[0]
+    plan = pft.build_plan(N, M, mu, p, EPS)
+    st = ShardedTransform(plan, world, rank, root=0, device=local, p2=args.p2)
+    # this rank's slice of the (device-generated) global signal; setup, not timed
+    full = torch.empty(N, dtype=torch.complex128, device=dev)
+    make_input_device(pft, full, N, mu, M, SEEDS[args.config], kind, N=N)
+    x = gather_local_device(full, plan.p, plan.q, world, rank)
+    del full
+    torch.cuda.empty_cache()
+    slab = torch.empty(plan.p * plan.r, dtype=torch.complex128, device=dev)
+    out = torch.empty(W, dtype=torch.complex128, device=dev)
+    launches = 2 if rank == 0 else 1
+    for _ in range(args.warmup):
+        st.execute(x, slab, out)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        e0.record()
+        for _ in range(args.steps):  # eager: the NCCL reduce sits between K1 and K2
+            st.execute(x, slab, out)
+        e1.record()
+        torch.cuda.synchronize(dev)
+    t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+    value = args.steps / (ms / 1e3)
+    peak, peak_src = measured_hbm_peak()
+    local_bytes = 16 * plan.p * st.layout.row_len
+    status = st.dplan.status() if rank == 0 else 0
+    if rank == 0:
+        line = {
+            "metric": "PFT transforms/sec", "value": value, "unit": "transforms/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {desc}", "N": N, "M": M, "mu": mu, "epsilon": EPS,
+                       "p": plan.p, "q": plan.q, "r": plan.r, "P1": st.dplan.P1, "P2": st.dplan.P2,
+                       "p_choice": "--p" if args.p else "pft_select_divisor_device (model)",
+                       "parallelism": f"contraction axis split over {world} GPUs + NCCL reduce of the "
+                                      f"{16 * plan.p * plan.r / 2**20:.1f} MiB partial slab",
+                       "l2": f"per-rank slice of {local_bytes / 2**30:.2f} GiB (> L2 126 MiB)",
+                       "timing": "eager steps (K1 | NCCL reduce | K2 on rank 0), CUDA events, max over ranks"},
+            "input_gbs": value * 16 * N / 1e9,
+            "input_gbs_frac_of_peak": value * 16 * N / 1e9 / world / peak,
+            "roofline": {"bound": "hbm", "kernel": "k1_contract_fft", "achieved": local_bytes / (ms_step * 1e-3) / 1e9,
+                         "peak": peak, "unit": "GB/s", "frac": local_bytes / (ms_step * 1e-3) / 1e9 / peak,
+                         "peak_source": peak_src, "traffic": None,
+                         "algorithmic_bytes_per_launch": local_bytes,
+                         "note": "per-rank K1 bytes over the whole step (K1 + reduce + K2): a lower bound"},
+            "cpu_baseline": None,
+            "e2e": None,
+            "gpu_launches": launches * args.steps,
+            "clocks": clk.summary(),
+            "status_flags": status,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main():

@@ -71,6 +71,24 @@ class ShardedTransform:
         self.finalize(slab.data_ptr(), out.data_ptr(), stream)
 
 
+def local_columns(q: int, world: int, rank: int) -> np.ndarray:
+    """Global column of each local column of `rank`'s row layout (-1 = padding)."""
+    idx = np.arange(1, q + 1, dtype=np.float64).astype(np.complex128)
+    return shard_gather(idx, 1, q, world, rank).reshape(-1).real.astype(np.int64) - 1
+
+
+def gather_local_device(full, p: int, q: int, world: int, rank: int):
+    """Device-side shard_gather: `rank`'s local slice (p * row_len complex128) of a CUDA
+    tensor holding the whole signal (setup only: it reads all of `full`)."""
+    import torch
+    cols = local_columns(q, world, rank)
+    sel = torch.from_numpy(np.where(cols < 0, 0, cols)).to(full.device)
+    local = full.view(p, q).index_select(1, sel)
+    if (cols < 0).any():
+        local[:, torch.from_numpy(np.nonzero(cols < 0)[0]).to(full.device)] = 0
+    return local.contiguous().view(-1)
+
+
 def batch_shard(n_signals: int, world: int, rank: int) -> tuple[int, int]:
     """Signals [start, start + count) of rank `rank` when a batch is sharded by signal
     (BASELINE configs[2]); contiguous near-equal split, no communication."""

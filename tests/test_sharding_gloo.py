@@ -64,3 +64,21 @@ def test_contraction_sharding_over_gloo(world, N, M, mu, p):
         results = mgr.dict()
         mp.spawn(_worker, args=(world, port, N, M, mu, p, results), nprocs=world, join=True)
         assert results[0] <= 1e-13, dict(results)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_gather_local_device_matches_shard_gather(pft, world):
+    """bench.py's C5 setup slices a device-resident signal with torch (sharded.gather_local_device);
+    it must equal the library's shard_gather layout for every rank (run here on CPU tensors)."""
+    import torch
+    from paper_2008_12559_b200.sharded import gather_local_device, local_columns
+    p, q = 16, 50
+    a = pft.generate_signal(pft.KIND_UNIFORM, 5, p * q)
+    seen = []
+    for rank in range(world):
+        ref = pft.shard_gather(a, p, q, world, rank)
+        got = gather_local_device(torch.from_numpy(a), p, q, world, rank).numpy().reshape(p, -1)
+        assert np.array_equal(ref, got)
+        cols = local_columns(q, world, rank)
+        seen += [int(c) for c in cols if c >= 0]
+    assert sorted(seen) == list(range(q))  # every column on exactly one rank
