@@ -47,6 +47,10 @@ CASES = [
     (2 ** 18, 0, 5, None, 1e-12, "uniform"),      # M = 0
     (3 * 5 * 7 * 64, 20, 11, 3 * 5 * 64, 1e-12, "normal"),  # odd q = 7
     (2 ** 20, 2 ** 12, 2 ** 18, 2 ** 14, 1e-12, "uniform"),  # M/p = 1/4
+    (2 ** 20, 300, 12345, 512, 1e-12, "uniform"),  # sum tail with W = 601 > p: bins wrap mod p
+    (6220800, 1000, -12345, 15360, 1e-12, "normal"),  # C4 at the autotuned p
+    (6220800, 1000, -12345, 16200, 1e-12, "normal"),  # C4, non-power-of-two P2 = 135, P1 = 120
+    (2 ** 24, 2 ** 6, 2 ** 22, 2048, 1e-12, "uniform"),  # C2a at the autotuned p (P1 = 32)
 ]
 
 
@@ -204,3 +208,45 @@ def test_autotuned_divisor_plan_parity(pft, oracle):
     plan = pft.build_plan(N, M, mu, p, 1e-12)
     got = pft.execute(plan, a).values
     assert rel_l2(got, oracle.execute(plan, a)) <= GATE
+
+
+@pytest.mark.parametrize("N,M,mu,p", [(2 ** 16, 256, 0, 256), (2 ** 16, 256, 0, 512), (2 ** 14, 100, -7, 128)])
+def test_batched_small_signals_sum_tail(pft, oracle, N, M, mu, p):
+    """C3-style batches (BASELINE configs[2]): a large batch hint gives P2 = 2-4 CTAs per
+    signal and the sum tail with W > p (the bins wrap mod p); every signal matches the oracle."""
+    import torch
+    batch = 5
+    plan = pft.build_plan(N, M, mu, p, 1e-12)
+    d = pft.DevicePlan(plan, batch_hint=4096)
+    assert d.launches_per_execute() == 1 and d.P2 <= 8
+    a = pft.generate_signal(pft.KIND_UNIFORM, 33, N * batch)
+    x = torch.from_numpy(a).cuda()
+    ws = torch.zeros(-(-d.workspace_bytes(batch) // 16), dtype=torch.complex128, device="cuda")
+    out = torch.empty(batch * (2 * M + 1), dtype=torch.complex128, device="cuda")
+    for _ in range(2):
+        d.execute_ptr(x.data_ptr(), out.data_ptr(), batch=batch, in_stride=N, d_ws=ws.data_ptr())
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().reshape(batch, 2 * M + 1)
+    for b in range(batch):
+        assert rel_l2(got[b], oracle.execute(plan, a[b * N:(b + 1) * N])) <= GATE, b
+
+
+@pytest.mark.parametrize("N,M,mu,p", [(2 ** 20, 64, 0, 2048), (2 ** 22, 1000, -3, 2 ** 13)])
+def test_sum_tail_and_k2_forms_agree(pft, oracle, N, M, mu, p):
+    """The same plan through the sum tail (k2_mode 5) and through K2 (k2_mode 1): both at the
+    oracle, and the two device forms agree far below the gate."""
+    import torch
+    plan = pft.build_plan(N, M, mu, p, 1e-12)
+    a = pft.generate_signal(pft.KIND_UNIFORM, 8, N)
+    x = torch.from_numpy(a).cuda()
+    ref = oracle.execute(plan, a)
+    res = []
+    for mode, launches in ((5, 1), (1, 2)):
+        d = pft.DevicePlan(plan, k2_mode=mode)
+        assert d.launches_per_execute() == launches
+        out = torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda")
+        d.execute_ptr(x.data_ptr(), out.data_ptr())
+        torch.cuda.synchronize()
+        res.append(out.cpu().numpy())
+        assert rel_l2(res[-1], ref) <= GATE, mode
+    assert rel_l2(res[0], res[1]) <= 1e-13
