@@ -28,6 +28,9 @@ int main() {
     // BASELINE configs[1] (C2b) plan
     const pft::PftPlan plan = pft::build_plan(1u << 24, 1u << 10, 1 << 22, 1u << 15, 1e-12, table);
     std::printf("%s\n", pft::plan_json(plan).c_str());
+    // the device-aware planner's choice for the same transform (model only; no GPU needed)
+    const pft::CostEstimate dev = pft::select_divisor_device(1u << 24, 1u << 10, table, 1e-12);
+    std::printf("device p = %zu, r = %zu, modelled %.1f us/transform\n", dev.p, dev.r, dev.cost);
     // execute an impulse: the DFT of delta is all ones
     const pft::PftPlan p2 = pft::build_plan(1u << 16, 64, 0, std::nullopt, 1e-12, table);
     pft::ComplexVec a(p2.N, pft::cplx(0.0, 0.0));

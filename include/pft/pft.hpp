@@ -154,6 +154,29 @@ inline std::pair<std::size_t, CostEstimate> select_divisor(std::size_t N, std::s
     return {static_cast<std::size_t>(p), CostEstimate{static_cast<std::size_t>(p), static_cast<std::size_t>(r), cost}};
 }
 
+// Device-aware choice of p for the B200 path (not in the reference):
+// the calibrated time model (cost = modelled microseconds per transform) ...
+inline CostEstimate select_divisor_device(std::size_t N, std::size_t M, const ScopeTable& t, double epsilon,
+                                          int n_sms = 148) {
+    uint64_t p = 0;
+    int r = 0;
+    double us = 0.0;
+    detail_api::check(pft_select_divisor_device(t.handle(), N, M, epsilon, n_sms, &p, &r, &us));
+    return CostEstimate{static_cast<std::size_t>(p), static_cast<std::size_t>(r), us};
+}
+
+// ... or measured: the model's best `candidates` timed on `device` with the caller's device
+// input (batch x N complex128).  Returns {p, microseconds per execute}.
+inline std::pair<std::size_t, double> autotune_divisor(std::size_t N, std::size_t M, std::int64_t mu,
+                                                       const ScopeTable& t, double epsilon, const cplx* d_in,
+                                                       std::size_t batch = 1, int candidates = 4, int device = 0) {
+    uint64_t p = 0;
+    double us = 0.0;
+    detail_api::check(pft_autotune_divisor(t.handle(), N, M, mu, epsilon, device, detail_api::c(d_in), batch,
+                                           candidates, &p, &us));
+    return {static_cast<std::size_t>(p), us};
+}
+
 // Frozen configuration.  Tables are host copies; the device upload is
 // made lazily by execute() and cached in the plan.
 struct PftPlan {

@@ -116,3 +116,4 @@ def test_cpp_api_demo_builds_and_runs(tmp_path, pft):
     res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
     assert '"p": 32768' in res.stdout
+    assert "device p = 16384, r = 8" in res.stdout  # pft_select_divisor_device at C2b
