@@ -214,6 +214,17 @@ pft_status pft_status_query(pft_dplan_t d, void* stream, int* flags, int reset);
 pft_status pft_execute_host(pft_dplan_t d, const pft_c128* h_in, size_t batch, pft_c128* h_out,
                             pft_c128* d_in, pft_c128* d_out, void* stream);
 
+/* ---- 2-D PFT (Algorithms 3-4).  `rows`: device plan of axis 2 (length N2,
+ * applied to each of the N1 rows of the row-major N1 x N2 input); `cols`: device plan of axis 1
+ * (length N1).  Output: (2M1+1) x (2M2+1) row-major, out[m1 - mu1 + M1][m2 - mu2 + M2].
+ * Executed as the two batched 1-D passes the block contraction B1^T A B2 factors into.  The
+ * workspace (pft_workspace_bytes_2d) is required; zero it once.                             */
+pft_status pft_workspace_bytes_2d(pft_dplan_t rows, pft_dplan_t cols, size_t* bytes);
+pft_status pft_execute_2d(pft_dplan_t rows, pft_dplan_t cols, const pft_c128* d_in, pft_c128* d_out,
+                          void* d_ws, void* stream);
+/* host convenience: H2D, execute_2d, D2H, synchronous; PFT_ERR_NON_FINITE on non-finite input */
+pft_status pft_execute_2d_host(pft_dplan_t rows, pft_dplan_t cols, const pft_c128* h_in, pft_c128* h_out);
+
 /* ------------------------------------------------------------------ synthetic inputs
  * Seeded counter-based generators (BASELINE.json configs), identical bit-for-bit on
  * host and device for the uniform kind.  kind: 0 = uniform[-1,1] re/im,

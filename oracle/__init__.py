@@ -181,3 +181,39 @@ def compare(actual, estimate, l1_input: float, epsilon: float, two_d: bool = Fal
 def certify(coeffs, xi: float, u: float = np.pi) -> float:
     c = _c(coeffs)
     return float(lib().oracle_certify(_p(c), len(c), float(xi), float(u)))
+
+
+def execute_2d(plan1, plan2, a, parenthesization: str = "LeftFirst") -> np.ndarray:
+    """execute_2d (Algorithm 4) on the CPU: per (k1, k2) block
+    C = B1^T A B2 in the given parenthesization (oracle matmul, ascending l), the r1 r2 2-D
+    FFTs of size p1 x p2 as row-column passes of the 1-D provider, then the
+    Eq. (14) weighted sum with the per-dimension post factors of the two 1-D plans."""
+    p1, q1, r1, p2, q2, r2 = plan1.p, plan1.q, plan1.r, plan2.p, plan2.q, plan2.r
+    A4 = _c(a).reshape(p1, q1, p2, q2)  # A^{(k1,k2)}[l1][l2] = a[q1 k1 + l1][q2 k2 + l2]
+    B1, B2 = _c(plan1.B), _c(plan2.B)
+    if parenthesization == "LeftFirst":  # (B1^T A) B2
+        T = matmul(A4.transpose(0, 2, 3, 1).reshape(-1, q1), B1).reshape(p1, p2, q2, r1)
+        Cb = matmul(T.transpose(0, 1, 3, 2).reshape(-1, q2), B2).reshape(p1, p2, r1, r2)
+    else:  # B1^T (A B2)
+        T = matmul(A4.reshape(-1, q2), B2).reshape(p1, q1, p2, r2)
+        Cb = matmul(T.transpose(0, 2, 3, 1).reshape(-1, q1), B1).reshape(p1, p2, r2, r1).transpose(0, 1, 3, 2)
+    # 2-D FFT over (k1, k2) for every (j1, j2): columns along k1, then along k2
+    F = batch_fft_columns(Cb.reshape(p1, -1)).reshape(p1, p2, r1, r2)
+    F = batch_fft_columns(F.transpose(1, 0, 2, 3).reshape(p2, -1)).reshape(p2, p1, r1, r2).transpose(1, 0, 2, 3)
+    M1, M2 = plan1.M, plan2.M
+    m1 = np.arange(plan1.mu - M1, plan1.mu + M1 + 1)
+    m2 = np.arange(plan2.mu - M2, plan2.mu + M2 + 1)
+    G = F[np.mod(m1, p1)][:, np.mod(m2, p2)]  # (W1, W2, r1, r2)
+    pw1 = np.asarray(plan1.post_powers, dtype=np.float64).reshape(2 * M1 + 1, r1)
+    pw2 = np.asarray(plan2.post_powers, dtype=np.float64).reshape(2 * M2 + 1, r2)
+    S = np.einsum("abjk,aj,bk->ab", G, pw1, pw2)
+    tw1 = _c(plan1.post_twiddles).reshape(-1)
+    tw2 = _c(plan2.post_twiddles).reshape(-1)
+    return S * tw1[:, None] * tw2[None, :]
+
+
+def naive_dft_2d(a, mu1: int, M1: int, mu2: int, M2: int) -> np.ndarray:
+    """Exact-angle 2-D DFT on the rectangle (separable: naive_dft along axis 2, then axis 1)."""
+    a = _c(a)
+    rows = np.stack([naive_dft(row, mu2, M2) for row in a])          # (N1, W2)
+    return np.stack([naive_dft(col, mu1, M1) for col in rows.T]).T   # (W1, W2)

@@ -21,6 +21,7 @@ from ._capi import c128
 __all__ = [
     "PftError", "ApproxPoly", "ScopeTable", "CostEstimate", "TargetRange", "PartialSpectrum", "PftPlan",
     "DevicePlan", "best_approx", "scope_xi", "translate_poly", "divisors", "min_terms", "select_divisor", "select_divisor_device", "autotune_divisor",
+    "Pft2dPlan", "PartialSpectrum2d", "build_plan_2d", "execute_2d", "parenthesization",
     "build_plan", "execute", "mod_index", "l1_norm", "generate_signal", "sparse_tones", "shard_layout",
     "shard_gather",
     "device_count", "lib",
@@ -318,6 +319,83 @@ def select_divisor_device(N: int, M: int, table: Optional[ScopeTable] = None,
     _check(lib().pft_select_divisor_device(_table(table).handle, int(N), int(M), float(epsilon), int(n_sms),
                                            C.byref(p), C.byref(r), C.byref(est)))
     return p.value, r.value, est.value
+
+
+class PartialSpectrum2d:
+    """(2M1+1) x (2M2+1) values on the rectangle R_{(mu1,mu2),(M1,M2)}."""
+
+    def __init__(self, values: np.ndarray, mu1: int, mu2: int, M1: int, M2: int):
+        self.values, self.mu1, self.mu2, self.M1, self.M2 = values, mu1, mu2, M1, M2
+
+    def at(self, m1: int, m2: int) -> complex:
+        i, j = m1 - (self.mu1 - self.M1), m2 - (self.mu2 - self.M2)
+        if not (0 <= i < self.values.shape[0] and 0 <= j < self.values.shape[1]):
+            raise IndexError("(m1, m2) outside the target rectangle")
+        return complex(self.values[i, j])
+
+
+def parenthesization(q1: int, r1: int, q2: int, r2: int) -> str:
+    """SPEC.md:285 / Appendix B: LeftFirst ((B1^T A) B2) iff q2 r1 (q1 + r2) <= q1 r2 (q2 + r1)."""
+    return "LeftFirst" if q2 * r1 * (q1 + r2) <= q1 * r2 * (q2 + r1) else "RightFirst"
+
+
+class Pft2dPlan:
+    """2-D PFT configuration (Algorithm 3): one 1-D plan per dimension --
+    plan1 for axis 1 (N1, M1, mu1, p1), plan2 for axis 2 -- and the CPU parenthesization
+    (LeftFirst iff q2 r1 (q1 + r2) <= q1 r2 (q2 + r1)), which only matters for the CPU cost."""
+
+    def __init__(self, plan1: "PftPlan", plan2: "PftPlan"):
+        self.plan1, self.plan2 = plan1, plan2
+        self.parenthesization = parenthesization(plan1.q, plan1.r, plan2.q, plan2.r)
+        self.achieved_epsilon = max(plan1.achieved_epsilon, plan2.achieved_epsilon)
+        self._dplans = None
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return self.plan1.N, self.plan2.N
+
+    def device_plans(self, device: int = 0):
+        """(rows, cols): the axis-2 plan batched over the N1 rows, the axis-1 plan over the
+        2M2+1 columns of the first pass."""
+        if self._dplans is None:
+            rows = DevicePlan(self.plan2, device=device, batch_hint=self.plan1.N)
+            cols = DevicePlan(self.plan1, device=device, batch_hint=2 * self.plan2.M + 1)
+            self._dplans = (rows, cols)
+        return self._dplans
+
+    def workspace_bytes(self, device: int = 0) -> int:
+        rows, cols = self.device_plans(device)
+        n = C.c_size_t()
+        _check(lib().pft_workspace_bytes_2d(rows.handle, cols.handle, C.byref(n)))
+        return n.value
+
+    def execute_ptr(self, d_in: int, d_out: int, d_ws: int, stream: int = 0, device: int = 0) -> None:
+        rows, cols = self.device_plans(device)
+        _check(lib().pft_execute_2d(rows.handle, cols.handle, C.c_void_p(d_in), C.c_void_p(d_out),
+                                    C.c_void_p(d_ws), C.c_void_p(stream or None)))
+
+
+def build_plan_2d(N1: int, N2: int, M1: int, M2: int, mu1: int, mu2: int, p1: Optional[int] = None,
+                  p2: Optional[int] = None, epsilon: float = DEFAULT_EPSILON,
+                  table: Optional[ScopeTable] = None) -> Pft2dPlan:
+    """Algorithm 3: per-dimension plans (p_d auto via select_divisor)."""
+    for N, M in ((N1, M1), (N2, M2)):
+        if 2 * M > N:
+            raise PftValueError(1, "build_plan_2d: M_d > N_d / 2")
+    return Pft2dPlan(build_plan(N1, M1, mu1, p1, epsilon, table), build_plan(N2, M2, mu2, p2, epsilon, table))
+
+
+def execute_2d(plan: Pft2dPlan, a, device: int = 0) -> PartialSpectrum2d:
+    """Algorithm 4 on the GPU: a is N1 x N2 (row-major) complex128."""
+    N1, N2 = plan.shape
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    if a.size != N1 * N2:
+        raise PftValueError(6, "execute_2d: grid shape does not match the plan")
+    W1, W2 = 2 * plan.plan1.M + 1, 2 * plan.plan2.M + 1
+    out = np.zeros((W1, W2), dtype=np.complex128)
+    rows, cols = plan.device_plans(device)
+    _check(lib().pft_execute_2d_host(rows.handle, cols.handle, _ptr(a), _ptr(out)))
+    return PartialSpectrum2d(out, plan.plan1.mu, plan.plan2.mu, plan.plan1.M, plan.plan2.M)
 
 
 def autotune_divisor(N: int, M: int, mu: int, d_in: int, table: Optional[ScopeTable] = None,

@@ -72,6 +72,9 @@ SIGNATURES: dict[str, tuple] = {
     "pft_min_terms": (ST, [P, D, U64, U64, C.POINTER(I)]),
     "pft_select_divisor": (ST, [P, U64, U64, D, C.POINTER(U64), C.POINTER(I), PD]),
     "pft_select_divisor_device": (ST, [P, U64, U64, D, I, C.POINTER(U64), C.POINTER(I), PD]),
+    "pft_workspace_bytes_2d": (ST, [P, P, C.POINTER(SZ)]),
+    "pft_execute_2d": (ST, [P, P, P, P, P, P]),
+    "pft_execute_2d_host": (ST, [P, P, P, P]),
     "pft_autotune_divisor": (ST, [P, U64, U64, I64, D, I, P, SZ, I, C.POINTER(U64), PD]),
     "pft_plan_build": (ST, [P, U64, U64, I64, U64, D, C.POINTER(P)]),
     "pft_plan_destroy": (None, [P]),

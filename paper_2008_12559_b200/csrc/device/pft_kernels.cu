@@ -892,6 +892,30 @@ extern "C" int pft_debug_timeline2(unsigned long long* host) {
 }
 #endif
 
+// 2-D PFT glue: out[c][r] = in[r][c] for an rows x cols complex128 matrix, through a 32 x 33
+// shared tile (coalesced on both sides).
+__global__ void k_transpose(const double2* __restrict__ in, double2* __restrict__ out, uint64_t rows,
+                            uint64_t cols) {
+    __shared__ double2 tile[32][33];
+    const uint64_t c0 = (uint64_t)blockIdx.x * 32, r0 = (uint64_t)blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const uint64_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const uint64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][i];
+    }
+}
+
+cudaError_t launch_transpose(const double2* in, double2* out, uint64_t rows, uint64_t cols, cudaStream_t st) {
+    if (rows == 0 || cols == 0) return cudaSuccess;
+    const dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+    k_transpose<<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_k0(const GenParams& G, cudaStream_t st) {
     const int threads = 256;
     uint64_t blocks = (G.count + threads - 1) / threads;
