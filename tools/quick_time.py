@@ -160,6 +160,13 @@ if __name__ == "__main__":
                 time_plan(6220800, 1000, -12345, pp, label=f"C4 p={pp}", reps=500)
             for pp in (1024, 2048, 4096):
                 time_plan(2 ** 20, 64, 0, pp, label=f"C1 p={pp}", reps=500)
+    if which == "k1ab":
+        for rep in range(2):
+            time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 14, label="C2b p=2^14", reps=500)
+            time_plan(2 ** 24, 2 ** 10, 2 ** 22, 2 ** 13, label="C2b p=2^13 r=10", reps=500)
+            time_plan(6220800, 1000, -12345, 15360, label="C4 p=15360", reps=500)
+            time_plan(2 ** 24, 2 ** 14, 2 ** 22, 2 ** 15, label="C2c p=2^15 r=14", reps=200)
+            time_plan(2 ** 20, 64, 0, 2048, label="C1 p=2048", reps=500)
     if which == "fuse":
         for rep in range(2):
             for fz in (True, False):
