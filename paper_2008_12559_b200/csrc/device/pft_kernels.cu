@@ -299,10 +299,6 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         fence_barrier_init();
     }
     __syncthreads();  // barriers initialised: the producer starts streaming immediately
-#ifdef PFT_K1_TRIGGER_EARLY
-    // (experiment) release the dependent K2 at the start of K1 instead of after its main loop
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
 
     const uint32_t c = blockIdx.x;  // residue class k = c (mod P2)
     const uint32_t b = blockIdx.y;  // signal
@@ -369,9 +365,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     // All of A has been read: let K2 (launched with programmatic stream serialization)
     // get scheduled and run its prologue while this grid finishes its FFT tail.
     PFT_STAMP(2)
-#ifndef PFT_K1_TRIGGER_EARLY
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
     __syncthreads();
     PFT_STAMP(3)
 
@@ -762,13 +756,11 @@ static cudaError_t launch_k1_r(const CUtensorMap& map, const K1Params& P, dim3 g
         attr[n].val.programmaticStreamSerializationAllowed = 1;
         ++n;
     }
-#ifndef PFT_NO_COOP
     if (P.fused) {  // the grid barrier needs every CTA resident
         attr[n].id = cudaLaunchAttributeCooperative;
         attr[n].val.cooperative = 1;
         ++n;
     }
-#endif
     cfg.attrs = attr;
     cfg.numAttrs = n;
     if (mu0) return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, true>, map, P);

@@ -250,3 +250,20 @@ def test_sum_tail_and_k2_forms_agree(pft, oracle, N, M, mu, p):
         res.append(out.cpu().numpy())
         assert rel_l2(res[-1], ref) <= GATE, mode
     assert rel_l2(res[0], res[1]) <= 1e-13
+
+
+@pytest.mark.parametrize("mode", [1, 2, 3, 4, 5])
+def test_every_second_pass_form(pft, oracle, mode):
+    """Each second-pass form forced on the same plan (K2 FFT 1, dot 2, direct 3, L2 4; sum tail
+    5) matches the oracle: the auto selection only picks among them by speed."""
+    import torch
+    N, M, mu, p = 2 ** 20, 100, 777, 4096
+    plan = pft.build_plan(N, M, mu, p, 1e-12)
+    a = pft.generate_signal(pft.KIND_UNIFORM, 12, N)
+    x = torch.from_numpy(a).cuda()
+    d = pft.DevicePlan(plan, k2_mode=mode)
+    out = torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda")
+    for _ in range(2):
+        d.execute_ptr(x.data_ptr(), out.data_ptr())
+    torch.cuda.synchronize()
+    assert rel_l2(out.cpu().numpy(), oracle.execute(plan, a)) <= GATE
