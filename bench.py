@@ -235,7 +235,8 @@ def run_ours(args):
     else:
         p_src = "config"
     plan = pft.build_plan(N, M, mu, p, EPS)
-    d = pft.DevicePlan(plan, device=local, p2=args.p2, pdl=not args.no_pdl, fuse=args.fuse, batch_hint=B)
+    d = pft.DevicePlan(plan, device=local, p2=args.p2, pdl=not args.no_pdl, fuse=args.fuse, batch_hint=B,
+                       k2_mode=args.k2_mode)
     launches = d.launches_per_execute()
 
     stream = torch.cuda.Stream(device=dev)
@@ -502,6 +503,8 @@ def main():
     ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
                     help="1 (default): one stream; consecutive transforms overlap through programmatic "
                          "dependent launch (K2 releases the next K1).  2: alternate two streams")
+    ap.add_argument("--k2-mode", type=int, default=0,
+                    help="second-pass form (0 auto; 1 K2 fft, 2 dot, 3 direct, 4 L2, 5 sum tail)")
     ap.add_argument("--no-pdl", action="store_true", help="plain stream order between kernels")
     ap.add_argument("--fuse", action="store_true", help="fuse K2 into K1's tail (grid barrier)")
     ap.add_argument("--no-e2e", action="store_true")
