@@ -136,6 +136,15 @@ def make_input_device(pft, buf, count, mu, M, seed, kind, offset=0, N=None):
                                    count, offset=offset)
 
 
+def omp_threads(n: int) -> None:
+    """Set the OpenMP team size of the oracle library (libgomp is shared by the process)."""
+    import ctypes
+    try:
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+    except OSError:
+        pass
+
+
 def cpu_oracle_rate(pft_mod, plan, a, budget_s: float):
     """Transforms/s of the CPU oracle (all host threads) on the same plan and input."""
     import oracle
@@ -376,6 +385,10 @@ def run_ours(args):
                 cpu = {"value": rate, "unit": "transforms/s", "cores": os.cpu_count(), "kind": "port",
                        "sample": f"{n} full {args.config} transforms (one signal each) in {el:.1f} s "
                                  f"(oracle/oracle.cpp, OpenMP {os.cpu_count()} threads)"}
+                omp_threads(1)  # report the 1-thread rate as well
+                r1, n1, el1 = cpu_oracle_rate(pft, plan, a_host, min(args.cpu_seconds, 5.0))
+                omp_threads(os.cpu_count())
+                cpu["one_thread"] = {"value": r1, "sample": f"{n1} transforms in {el1:.1f} s, 1 thread"}
             except Exception as e:  # the baseline is reported, never required
                 cpu = {"value": None, "error": str(e)}
         line = {
