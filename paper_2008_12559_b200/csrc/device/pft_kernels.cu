@@ -88,7 +88,7 @@ __device__ __forceinline__ void k2_fft_block(const K2Params& P, uint32_t m1, uin
 
 // One TMA stage (a box of K1_BR rows x K1_CP mirror column pairs + the pair table slice)
 // into the row accumulators of this lane: lanes li, li + LANES_PER_ROW, ... of row `rin`.
-template <int R, bool MU0>
+template <int R, bool MU0, bool FULL>
 __device__ __forceinline__ void k1_accumulate_stage(const unsigned char* st, int rin, int li, uint32_t valid,
                                                     double (&are)[R], double (&aim)[R]) {
     const double2* front = reinterpret_cast<const double2*>(st) + rin * K1_CP;
@@ -99,7 +99,7 @@ __device__ __forceinline__ void k1_accumulate_stage(const unsigned char* st, int
         const int i = li + u * K1_LANES_PER_ROW;
         // branch-free masking of pairs past the end of the view (keeps the
         // independent pairs in one basic block so their chains interleave)
-        const bool ok = (uint32_t)i < valid;
+        const bool ok = FULL || (uint32_t)i < valid;  // FULL: every pair of the chunk is in the view
         const double2 z = make_double2(0.0, 0.0);
         const double2 x1 = ok ? front[i] : z;               // column l
         const double2 x2 = ok ? mirror[K1_CP - 1 - i] : z;  // column q - l
@@ -354,8 +354,14 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                 // the warp diverged, and reading a stage from a diverged warp was observed to
                 // return corrupt rows on B200 when two K1 CTAs share an SM.
                 __syncwarp();
-                k1_accumulate_stage<R, MU0>(ring + (size_t)s * K1_STAGE_BYTES, rin, li,
-                                            min((uint32_t)K1_CP, npairs - ch * K1_CP), are, aim);
+                // full chunks skip the per-pair masking (selects and zero moves were about as
+                // many instructions as the FP64 work); only a row's last chunk can be partial
+                const uint32_t valid = min((uint32_t)K1_CP, npairs - ch * K1_CP);
+                const unsigned char* stage = ring + (size_t)s * K1_STAGE_BYTES;
+                if (valid == (uint32_t)K1_CP)
+                    k1_accumulate_stage<R, MU0, true>(stage, rin, li, valid, are, aim);
+                else
+                    k1_accumulate_stage<R, MU0, false>(stage, rin, li, valid, are, aim);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);  // stage s may be refilled
             }
