@@ -267,3 +267,25 @@ def test_every_second_pass_form(pft, oracle, mode):
         d.execute_ptr(x.data_ptr(), out.data_ptr())
     torch.cuda.synchronize()
     assert rel_l2(out.cpu().numpy(), oracle.execute(plan, a)) <= GATE
+
+
+EDGE = [
+    # (N, M, mu, p): degenerate shapes the planner can produce
+    (4096, 2047, 0, None),     # M = N/2 - 1: r = 25, q = 4
+    (4096, 1000, 5, 4096),     # p = N: q = 1, no column pairs (only l = 0)
+    (8191, 100, 3, None),      # prime N: p = N, q = 1
+    (8, 3, 1, None),           # tiny N
+    (4096, 100, 0, 2048),      # q = 2: one unpaired pair of singles (l = 0, q/2)
+    (4095, 10, 0, 1365),       # q = 3: one pair + l = 0
+    (2 ** 20, 0, 0, None),     # M = 0: p = 2, q = N/2, r = 1
+    (96, 47, -1000, None),     # mu far below 0
+]
+
+
+@pytest.mark.parametrize("N,M,mu,p", EDGE)
+def test_degenerate_shapes(pft, oracle, N, M, mu, p):
+    plan = pft.build_plan(N, M, mu, p, 1e-12)
+    a = uniform(pft, 17, N)
+    gpu = pft.execute(plan, a).values
+    ref = oracle.execute(plan, a)
+    assert rel_l2(gpu, ref) <= GATE, plan.json()
