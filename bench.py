@@ -215,7 +215,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if args.config in SHARDED and world > 1:
+    if args.config in SHARDED and (world > 1 or args.force_sharded):
         return run_sharded(args, world, rank, local, dev)
 
     N, M, mu, p, kind, desc = CONFIGS[args.config]
@@ -457,7 +457,8 @@ def run_sharded(args, world, rank, local, dev):
     for _ in range(args.warmup):
         st.execute(x, slab, out)
     torch.cuda.synchronize(dev)
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize(dev)
@@ -467,12 +468,19 @@ def run_sharded(args, world, rank, local, dev):
         e1.record()
         torch.cuda.synchronize(dev)
     t = torch.tensor([e0.elapsed_time(e1)], device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     ms_step = ms / args.steps
     value = args.steps / (ms / 1e3)
     peak, peak_src = measured_hbm_peak()
     local_bytes = 16 * plan.p * st.layout.row_len
+    check = None
+    if world == 1:  # --force-sharded on one GPU: the partial/finalize path against plain execute
+        ref = torch.empty_like(out)
+        st.dplan.execute_ptr(x.data_ptr(), ref.data_ptr())
+        torch.cuda.synchronize(dev)
+        check = float(torch.linalg.vector_norm(out - ref) / torch.linalg.vector_norm(ref))
     status = st.dplan.status() if rank == 0 else 0
     if rank == 0:
         line = {
@@ -498,10 +506,12 @@ def run_sharded(args, world, rank, local, dev):
             "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
             "status_flags": status,
+            "sharded_vs_plain_rel_l2": check,
         }
         print(json.dumps(line), flush=True)
-    dist.barrier()
-    dist.destroy_process_group()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def main():
@@ -518,6 +528,8 @@ def main():
                          "dependent launch (K2 releases the next K1).  2: alternate two streams")
     ap.add_argument("--k2-mode", type=int, default=0,
                     help="second-pass form (0 auto; 1 K2 fft, 2 dot, 3 direct, 4 L2, 5 sum tail)")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="c5: run the contraction-axis sharded path even on one GPU (checks it)")
     ap.add_argument("--no-pdl", action="store_true", help="plain stream order between kernels")
     ap.add_argument("--fuse", action="store_true", help="fuse K2 into K1's tail (grid barrier)")
     ap.add_argument("--no-e2e", action="store_true")
