@@ -30,7 +30,25 @@ constexpr uint32_t K1_STAGE_BYTES = 2 * K1_BOX_BYTES + K1_TAB_BYTES;
 #define PFT_K1_MIN_STAGES 4
 #endif
 constexpr int K1_MIN_STAGES = PFT_K1_MIN_STAGES, K1_MAX_STAGES = 8;
-constexpr size_t K1_MIN_RING_BYTES = (size_t)K1_MIN_STAGES * K1_STAGE_BYTES;
+
+// FP64 tensor-core contraction (mma.sync m8n8k4 f64, DMMA) for r in [PFT_K1_TC_MIN_R, 18]: per
+// pair the even moments j = 2, 4, .., 16 and the odd moments j = 1, 3, .., 15 are two 8-column
+// tiles, B fragments t_l^j come with each stage ([pair][g]{even, odd}, host-built), j = 0 and
+// (r = 18) j = 17 stay on the FP64 pipe.  A DMMA does 256 FMAs per issue: the contraction
+// sheds the power chain and most of its instruction overhead.  Stages carry the fragment
+// slice, so the ring may be 3 stages deep to keep two CTAs per SM.
+// Measured (same box): C3 p = 256, r = 18: 1190 vs 1276 us per batch (split vector path);
+// r = 14: no gain (1404 vs 1405 us); r <= 9 slower (C2b r = 8: 56.8 vs 41.5 us; C4 r = 9:
+// 27.6 vs 20.9 us), so from r = 16.
+#ifndef PFT_K1_TC_MIN_R
+#define PFT_K1_TC_MIN_R 16
+#endif
+__host__ __device__ constexpr bool k1_tc(int r) { return r >= PFT_K1_TC_MIN_R && r <= 18; }
+constexpr uint32_t K1_TC_BYTES = K1_CP * 16 * 8;  // 16 pairs x 8 columns x {even, odd} doubles
+__host__ __device__ constexpr uint32_t k1_stage_bytes(int r) { return K1_STAGE_BYTES + (k1_tc(r) ? K1_TC_BYTES : 0); }
+__host__ __device__ constexpr int k1_min_stages(int r) { return k1_tc(r) ? 3 : K1_MIN_STAGES; }
+inline size_t k1_min_ring_bytes(int r) { return (size_t)k1_min_stages(r) * k1_stage_bytes(r); }
+static_assert(K1_TC_BYTES % 128 == 0, "TMA destinations stay 128-byte aligned");
 static_assert(K1_LANES_PER_ROW >= 1 && K1_LANES_PER_ROW <= 32 && K1_CP % K1_LANES_PER_ROW == 0, "row mapping");
 static_assert(K1_STAGE_BYTES % 128 == 0, "TMA destinations stay 128-byte aligned");
 
@@ -59,11 +77,30 @@ struct K2Params {
     int* status;
 };
 
-// Pair-table entry (host-built): phase_l = e^{-2 pi i mu (l - q/2)/N} and t_l = 1 - 2l/q.
+// Pair-table entry (host-built): phase_l = e^{-2 pi i mu (l - q/2)/N}, t_l = 1 - 2l/q and
+// t_l^h, h = ceil(r/2) (start of the upper j half under the two-lane j split, k1_js).
 // The mirror column q-l uses conj(phase_l) and -t_l (exact identities of SPEC.md:126).
 struct PairEntry {
-    double c, s, t, pad;
+    double c, s, t, th;
 };
+
+// K1 splits the r moments of a row over JS lanes (JS = 2 from r >= PFT_K1_JS_MIN_R without
+// phase factors (mu = 0), from r >= PFT_K1_JS_MIN_R_PHASE with them; vector path only): each
+// lane keeps ceil(r/2) accumulator pairs instead of r (no spills with two CTAs per SM), takes
+// twice the pairs of a chunk (more independent power chains) and the row reduction shuffles
+// half the values over one level fewer.  With phases both lanes repeat the phase multiply, so
+// the split pays later (measured C3 p = 256, r = 18, mu = 0: 1535 -> 1267 us per batch;
+// C2c r = 14 with phases: 79.8 unsplit vs 84.2 us split; C4 r = 9: 21.0 vs 25.1 us).
+#ifndef PFT_K1_JS_MIN_R
+#define PFT_K1_JS_MIN_R 12
+#endif
+#ifndef PFT_K1_JS_MIN_R_PHASE
+#define PFT_K1_JS_MIN_R_PHASE 19
+#endif
+__host__ __device__ constexpr int k1_js(int r, bool mu0) {
+    return !k1_tc(r) && r >= (mu0 ? PFT_K1_JS_MIN_R : PFT_K1_JS_MIN_R_PHASE) ? 2 : 1;
+}
+
 
 struct K1Params {
     // local view of A (rows k = c + P2 k1 at a + k * row_stride, signal b at + b * batch_stride)
@@ -77,6 +114,7 @@ struct K1Params {
     int32_t single0_col, singleh_col;
     double2 phase0, phaseh;     // phase_0, phase_{q/2}
     const PairEntry* pairtab;   // [>= gp_end + K1_CP]
+    const double2* tcfrag;      // [>= gp_end + K1_CP][8] {t^(2+2g), t^(1+2g)} (k1_tc(r) plans)
     const double2* w;           // [r]  w_{eps, r-1, j}
     const double2* omega;       // [p]  e^{-2 pi i t / p}
     uint32_t P1, P2;            // p = P1 * P2
@@ -108,13 +146,13 @@ struct GenParams {
 // (needs r*P1*16 <= the smallest ring)
 inline size_t k1_smem_bytes(int r, uint32_t P1, uint32_t stages) {
     const size_t p1 = P1 ? P1 : 1;
-    return (size_t)stages * K1_STAGE_BYTES + sizeof(double2) * ((size_t)r * p1 + p1) + 2 * stages * sizeof(uint64_t);
+    return (size_t)stages * k1_stage_bytes(r) + sizeof(double2) * ((size_t)r * p1 + p1) + 2 * stages * sizeof(uint64_t);
 }
 // K1 ring depth: as deep as possible while two CTAs still share an SM.
 inline uint32_t k1_pick_stages(int r, uint32_t P1) {
     const size_t per_cta = (228 * 1024) / 2 - 1024;
     uint32_t s = K1_MAX_STAGES;
-    while (s > K1_MIN_STAGES && k1_smem_bytes(r, P1, s) > per_cta) --s;
+    while (s > (uint32_t)k1_min_stages(r) && k1_smem_bytes(r, P1, s) > per_cta) --s;
     return s;
 }
 // Z + scratch (r x P2 each) + omega_P2 + four-step twiddles (P2 each)

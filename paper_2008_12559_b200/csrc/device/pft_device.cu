@@ -73,7 +73,7 @@ constexpr size_t kK2SmemLimit = 220 * 1024;
 bool k1_feasible(uint64_t P1, int r) {
     pftdev::FftRadices fr;
     if (P1 > 1 && !factor_radices((uint32_t)P1, fr)) return false;
-    return sizeof(double2) * (size_t)r * P1 <= pftdev::K1_MIN_RING_BYTES;  // FFT scratch = the ring
+    return sizeof(double2) * (size_t)r * P1 <= pftdev::k1_min_ring_bytes(r);  // FFT scratch = the ring
 }
 
 bool k2_fft_feasible(uint64_t P2, int r) {
@@ -90,9 +90,9 @@ bool k2_fft_feasible(uint64_t P2, int r) {
 // largest P2, taking a power of two if within 15% of it.  0 = none.
 bool sum_p1_ok(uint64_t P1, int r, uint64_t P2) {
     if (!k1_feasible(P1, r)) return false;
-    if (pftdev::k1_smem_bytes(r, (uint32_t)P1, pftdev::K1_MIN_STAGES) > (228 * 1024) / 2 - 1024) return false;
+    if (pftdev::k1_smem_bytes(r, (uint32_t)P1, pftdev::k1_min_stages(r)) > (228 * 1024) / 2 - 1024) return false;
     return sizeof(double2) * r * P1 + pftdev::k1_sum_scratch_bytes((uint32_t)P1, (uint32_t)P2) <=
-           (size_t)pftdev::K1_MIN_STAGES * pftdev::K1_STAGE_BYTES;
+           pftdev::k1_min_ring_bytes(r);
 }
 
 // The sum tail pays, per CTA, W outputs of r-term sums plus a W-long row written and reduced
@@ -236,6 +236,7 @@ struct pft_dplan_s {
     // device allocations
     void* tables = nullptr;
     pftdev::PairEntry* d_pairtab = nullptr;
+    double2* d_tcfrag = nullptr;  // k1_tc plans: [pairs][8] B fragments
     double2* d_w = nullptr;
     double2 phase0{1.0, 0.0}, phaseh{1.0, 0.0};
     double2* d_omega = nullptr;
@@ -264,7 +265,7 @@ struct pft_dplan_s {
     }
     bool fused(size_t batch) const {
         return allow_fuse && !sum_tail && k2_mode == pftdev::K2_FFT &&
-               pftdev::k2_smem_bytes(host.r, (uint32_t)P2) <= (size_t)k1_stages * pftdev::K1_STAGE_BYTES &&
+               pftdev::k2_smem_bytes(host.r, (uint32_t)P2) <= (size_t)k1_stages * pftdev::k1_stage_bytes(host.r) &&
                P2 * batch <= k1_capacity;
     }
 
@@ -283,6 +284,7 @@ struct pft_dplan_s {
         P.phase0 = phase0;
         P.phaseh = phaseh;
         P.pairtab = d_pairtab;
+        P.tcfrag = d_tcfrag;
         P.w = d_w;
         P.omega = d_omega;
         P.P1 = (uint32_t)P1;
@@ -547,7 +549,8 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     if (!k1_feasible(d->P1, H.r))
         fail(PFT_ERR_UNSUPPORTED, "dplan_create: P1 * r too large for K1 shared memory; choose a larger p2");
     d->k1_stages = (opts && opts->k1_stages) ? (uint32_t)opts->k1_stages : pftdev::k1_pick_stages(H.r, (uint32_t)d->P1);
-    PFT_REQUIRE(d->k1_stages >= (uint32_t)pftdev::K1_MIN_STAGES && d->k1_stages <= (uint32_t)pftdev::K1_MAX_STAGES, "dplan_create: k1_stages out of [4, 8]");
+    PFT_REQUIRE(d->k1_stages >= (uint32_t)pftdev::k1_min_stages(H.r) && d->k1_stages <= (uint32_t)pftdev::K1_MAX_STAGES,
+                "dplan_create: k1_stages out of [min stages (3 or 4), 8]");
     // K2 form: length-P2 FFT when it fits shared memory (fastest measured), else the dot form,
     // else the direct global form.
     {
@@ -581,7 +584,7 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         // off by modes 1-4, forced on (if feasible) by 5.
         const bool fits = sizeof(double2) * H.r * d->P1 +
                               pftdev::k1_sum_scratch_bytes((uint32_t)d->P1, (uint32_t)d->P2) <=
-                          (size_t)pftdev::K1_MIN_STAGES * pftdev::K1_STAGE_BYTES;
+                          pftdev::k1_min_ring_bytes(H.r);
         d->sum_tail = fits && (forced == 5 || (forced == 0 && sum_tail_pays(H.N, d->W, d->P2, H.r)));
         // reducing CTAs per signal: one per 64 outputs (measured best at C2b/C4: 32; more
         // reducers hold more SM slots from the next transform), opts override
@@ -595,12 +598,33 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
 #pragma omp parallel for schedule(static)
     for (long long t = 0; t < (long long)H.p; ++t) omega[t] = cispi_frac(-2 * (__int128)t, H.p);
 
-    // pair table {Re phase_l, Im phase_l, t_l, 0} for l in [0, L), zero-padded so a chunk
-    // read past the last pair stays in bounds
+    // pair table {Re phase_l, Im phase_l, t_l, t_l^h} for l in [0, L), h = ceil(r/2) (the first
+    // power of the upper j half when K1 splits j over two lanes; formed by the same ascending
+    // repeated multiplication as the kernel's power chain, so both splits see identical powers),
+    // zero-padded so a chunk read past the last pair stays in bounds
     const uint64_t L = (H.q + 1) / 2;
     const uint64_t n_pt = L + 2 * pftdev::K1_CP;
+    // (tensor-core plans, k1_tc: t_l^17 for r = 18, the moment outside the two DMMA tiles).
+    // Tensor-core plans also get the B-fragment table {t_l^(2+2g), t_l^(1+2g)}, g in [8]
+    // (zero where j >= r), same ascending powers.
+    const bool tc = pftdev::k1_tc(H.r);
+    const int h_split = tc ? H.r - 1 : (H.r + 1) / 2;  // t^h serves the two-lane j split
     std::vector<pftdev::PairEntry> pairtab(n_pt, pftdev::PairEntry{0.0, 0.0, 0.0, 0.0});
-    for (uint64_t l = 0; l < L; ++l) pairtab[l] = {H.phase[l].real(), H.phase[l].imag(), H.tvals[l], 0.0};
+    std::vector<double> tcfrag(tc ? n_pt * 16 : 0, 0.0);
+    for (uint64_t l = 0; l < L; ++l) {
+        const double t = H.tvals[l];
+        double pw[32];  // r <= 25
+        pw[0] = 1.0;
+        for (int j = 1; j < 32; ++j) pw[j] = pw[j - 1] * t;  // pw[1] = 1 * t = t exactly
+        pairtab[l] = {H.phase[l].real(), H.phase[l].imag(), t, pw[h_split]};
+        if (tc) {
+            for (int g = 0; g < 8; ++g) {
+                const int je = 2 + 2 * g, jo = 1 + 2 * g;
+                tcfrag[l * 16 + 2 * g] = je < H.r ? pw[je] : 0.0;
+                tcfrag[l * 16 + 2 * g + 1] = jo < H.r ? pw[jo] : 0.0;
+            }
+        }
+    }
     d->phase0 = make_double2(H.phase[0].real(), H.phase[0].imag());
     if (H.q % 2 == 0) d->phaseh = make_double2(H.phase[H.q / 2].real(), H.phase[H.q / 2].imag());
 
@@ -608,8 +632,8 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t b_pt0 = al(n_pt * sizeof(pftdev::PairEntry)), b_w = al(H.r * sizeof(double2)),
                  b_om = al(H.p * sizeof(double2)), b_pp = al(d->W * H.r * sizeof(double)),
-                 b_pt = al(d->W * sizeof(double2));
-    const size_t total = b_pt0 + b_w + b_om + b_pp + b_pt;
+                 b_pt = al(d->W * sizeof(double2)), b_tc = al(tcfrag.size() * sizeof(double));
+    const size_t total = b_pt0 + b_w + b_om + b_pp + b_pt + b_tc;
     cuda_check(cudaMalloc(&d->tables, total), "cudaMalloc(tables)");
     char* base = static_cast<char*>(d->tables);
     d->d_pairtab = reinterpret_cast<pftdev::PairEntry*>(base);
@@ -617,6 +641,11 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     d->d_omega = reinterpret_cast<double2*>(base + b_pt0 + b_w);
     d->d_post_powers = reinterpret_cast<double*>(base + b_pt0 + b_w + b_om);
     d->d_post_twiddles = reinterpret_cast<double2*>(base + b_pt0 + b_w + b_om + b_pp);
+    if (tc) {
+        d->d_tcfrag = reinterpret_cast<double2*>(base + b_pt0 + b_w + b_om + b_pp + b_pt);
+        cuda_check(cudaMemcpy(d->d_tcfrag, tcfrag.data(), tcfrag.size() * sizeof(double), cudaMemcpyHostToDevice),
+                   "upload tensor-core fragment table");
+    }
     cuda_check(cudaMemcpy(d->d_pairtab, pairtab.data(), n_pt * sizeof(pftdev::PairEntry), cudaMemcpyHostToDevice),
                "upload pair table");
     cuda_check(cudaMemcpy(d->d_w, H.w.data(), H.r * sizeof(double2), cudaMemcpyHostToDevice), "upload w");

@@ -87,16 +87,25 @@ template <int R>
 __device__ __forceinline__ void k2_fft_block(const K2Params& P, uint32_t m1, uint32_t b, double2* zs);
 
 // One TMA stage (a box of K1_BR rows x K1_CP mirror column pairs + the pair table slice)
-// into the row accumulators of this lane: lanes li, li + LANES_PER_ROW, ... of row `rin`.
-template <int R, bool MU0, bool FULL>
+// into the row accumulators of this lane.  The K1_LANES_PER_ROW lanes of row `rin` are
+// li = pl * JS + jh: pair lane pl takes pairs pl, pl + LANES_PER_ROW / JS, ... and j half jh
+// accumulates j = jh * H + jj (H = ceil(R / JS), jj < H) with powers t^j formed by
+// ascending repeated multiplication from t^{jh H} (the pair table's t^h for jh = 1).
+template <int R, int JS, bool MU0, bool FULL>
 __device__ __forceinline__ void k1_accumulate_stage(const unsigned char* st, int rin, int li, uint32_t valid,
-                                                    double (&are)[R], double (&aim)[R]) {
+                                                    double (&are)[(R + JS - 1) / JS],
+                                                    double (&aim)[(R + JS - 1) / JS]) {
+    constexpr int H = (R + JS - 1) / JS;
+    constexpr int PL = K1_LANES_PER_ROW / JS;  // pair lanes per row
     const double2* front = reinterpret_cast<const double2*>(st) + rin * K1_CP;
     const double2* mirror = reinterpret_cast<const double2*>(st + K1_BOX_BYTES) + rin * K1_CP;
     const PairEntry* tab = reinterpret_cast<const PairEntry*>(st + 2 * K1_BOX_BYTES);
+    const int pl = li / JS, jh = li % JS;
+    // the j parity of jj = 0 is that of jh * H: swap the (sum, difference) roles when odd
+    const bool swap = ((jh * H) & 1) != 0;
 #pragma unroll
-    for (int u = 0; u < K1_CP / K1_LANES_PER_ROW; ++u) {
-        const int i = li + u * K1_LANES_PER_ROW;
+    for (int u = 0; u < K1_CP / PL; ++u) {
+        const int i = pl + u * PL;
         // branch-free masking of pairs past the end of the view (keeps the
         // independent pairs in one basic block so their chains interleave)
         const bool ok = FULL || (uint32_t)i < valid;  // FULL: every pair of the chunk is in the view
@@ -115,51 +124,155 @@ __device__ __forceinline__ void k1_accumulate_stage(const unsigned char* st, int
             Sv = make_double2(fma(cs.x, su.x, -cs.y * di.y), fma(cs.x, su.y, cs.y * di.x));
             Dv = make_double2(fma(cs.x, di.x, -cs.y * su.y), fma(cs.x, di.y, cs.y * su.x));
         }
-        are[0] += Sv.x;
-        aim[0] += Sv.y;
-        double tp = t;
+        if constexpr (JS == 1) {
+            are[0] += Sv.x;
+            aim[0] += Sv.y;
+            double tp = t;
 #pragma unroll
-        for (int j = 1; j < R; ++j) {
-            const double2 v = (j & 1) ? Dv : Sv;  // t^j (b + (-1)^j b')
-            are[j] = fma(v.x, tp, are[j]);
-            aim[j] = fma(v.y, tp, aim[j]);
-            if (j + 1 < R) tp *= t;
+            for (int j = 1; j < R; ++j) {
+                const double2 v = (j & 1) ? Dv : Sv;  // t^j (b + (-1)^j b')
+                are[j] = fma(v.x, tp, are[j]);
+                aim[j] = fma(v.y, tp, aim[j]);
+                if (j + 1 < R) tp *= t;
+            }
+        } else {
+            const double2 E = swap ? Dv : Sv, O = swap ? Sv : Dv;  // jj even / odd
+            double tp = jh ? tab[i].th : 1.0;
+#pragma unroll
+            for (int jj = 0; jj < H; ++jj) {
+                const double2 v = (jj & 1) ? O : E;
+                are[jj] = fma(v.x, tp, are[jj]);
+                aim[jj] = fma(v.y, tp, aim[jj]);
+                if (jj + 1 < H) tp *= t;
+            }
         }
     }
 }
 
-// End of a row batch: add this lane's unpaired column (l = 0 with t = 1 feeds every j;
-// l = q/2 with t = 0 only j = 0), reduce over the LANES_PER_ROW lanes of the row (fixed
-// xor-butterfly order) and store C[k1][j] = w_j acc_j into Cs[j][k1].
-template <int R, bool MU0>
+// End of a row batch: add the row's unpaired columns (l = 0 with t = 1 feeds every j: pair
+// lane 0, both j halves; l = q/2 with t = 0 only j = 0: lane li = JS), reduce over the pair
+// lanes of the row (fixed xor-butterfly order) and store C[k1][j] = w_j acc_j into Cs[j][k1].
+template <int R, int JS, bool MU0>
 __device__ __forceinline__ void k1_finish_row(const K1Params& P, double2 xs, int scol, int li, uint32_t k1,
-                                              double (&are)[R], double (&aim)[R], double2* Cs) {
+                                              double (&are)[(R + JS - 1) / JS],
+                                              double (&aim)[(R + JS - 1) / JS], double2* Cs) {
+    constexpr int H = (R + JS - 1) / JS;
+    constexpr int PL = K1_LANES_PER_ROW / JS;
     if (scol >= 0) {
         double2 x = xs;
-        if constexpr (!MU0) x = cmul(x, li == 0 ? P.phase0 : P.phaseh);
+        const bool zero_col = li < JS;  // l = 0; else l = q/2
+        if constexpr (!MU0) x = cmul(x, zero_col ? P.phase0 : P.phaseh);
         are[0] += x.x;
         aim[0] += x.y;
-        if (li == 0) {
+        if (zero_col) {
 #pragma unroll
-            for (int j = 1; j < R; ++j) {
+            for (int j = 1; j < H; ++j) {
                 are[j] += x.x;
                 aim[j] += x.y;
             }
         }
     }
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
+    for (int j = 0; j < H; ++j) {
 #pragma unroll
-        for (int off = K1_LANES_PER_ROW / 2; off >= 1; off >>= 1) {
+        for (int off = K1_LANES_PER_ROW / 2; off >= JS; off >>= 1) {
             are[j] += __shfl_xor_sync(0xffffffffu, are[j], off);
             aim[j] += __shfl_xor_sync(0xffffffffu, aim[j], off);
         }
     }
+    const int pl = li / JS, jh = li % JS;
 #pragma unroll
-    for (int j = 0; j < R; ++j) {
-        if (k1 < P.P1 && (j % K1_LANES_PER_ROW) == li)
-            Cs[(size_t)j * P.P1 + k1] = cmul(make_double2(are[j], aim[j]), __ldg(P.w + j));  // C = w_j acc_j
+    for (int jj = 0; jj < H; ++jj) {
+        const int j = jh * H + jj;
+        if (k1 < P.P1 && j < R && (jj % PL) == pl)
+            Cs[(size_t)j * P.P1 + k1] = cmul(make_double2(are[jj], aim[jj]), __ldg(P.w + j));  // C = w_j acc_j
     }
+}
+
+// ---- tensor-core contraction (k1_tc(R)): one warp = 4 rows of the box as the 8 m-rows of a
+// DMMA tile (m = 2 * row + part, part 0/1 = re/im); per k-step the 4 k-columns are pairs
+// ks * 4 + t4.  A = (b_l + b_{q-l}) parts against the even-moment tile, (b_l - b_{q-l}) parts
+// against the odd-moment tile; the MMA sums over the pairs, so only the FP64-pipe moments
+// (j = 0, and j = 17 for R = 18) need a cross-lane reduction at the end of the row batch.
+__device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+template <int R, bool MU0, bool FULL>
+__device__ __forceinline__ void k1_tc_stage(const unsigned char* st, int rin, int part, int t4, int g, uint32_t valid,
+                                            double (&de)[2], double (&dd)[2], double& v0, double& vl) {
+    const double2* front = reinterpret_cast<const double2*>(st) + rin * K1_CP;
+    const double2* mirror = reinterpret_cast<const double2*>(st + K1_BOX_BYTES) + rin * K1_CP;
+    const PairEntry* tab = reinterpret_cast<const PairEntry*>(st + 2 * K1_BOX_BYTES);
+    const double2* frag = reinterpret_cast<const double2*>(st + 2 * K1_BOX_BYTES + K1_TAB_BYTES);  // [pair][g]
+#pragma unroll
+    for (int ks = 0; ks < K1_CP / 4; ++ks) {
+        const int i = ks * 4 + t4;
+        const bool ok = FULL || (uint32_t)i < valid;
+        double ae, ao;  // this lane's part of phase_l x1 + conj(phase_l) x2 and of the difference
+        if constexpr (MU0) {
+            const double x1 = ok ? reinterpret_cast<const double*>(front + i)[part] : 0.0;
+            const double x2 = ok ? reinterpret_cast<const double*>(mirror + (K1_CP - 1 - i))[part] : 0.0;
+            ae = x1 + x2;
+            ao = x1 - x2;
+        } else {
+            const double2 z = make_double2(0.0, 0.0);
+            const double2 x1 = ok ? front[i] : z;
+            const double2 x2 = ok ? mirror[K1_CP - 1 - i] : z;
+            const double2 cs = *reinterpret_cast<const double2*>(&tab[i].c);
+            const double2 su = make_double2(x1.x + x2.x, x1.y + x2.y);
+            const double2 di = make_double2(x1.x - x2.x, x1.y - x2.y);
+            ae = part ? fma(cs.x, su.y, cs.y * di.x) : fma(cs.x, su.x, -cs.y * di.y);
+            ao = part ? fma(cs.x, di.y, cs.y * su.x) : fma(cs.x, di.x, -cs.y * su.y);
+        }
+        const double2 b = frag[i * 8 + g];  // {t^(2+2g), t^(1+2g)}
+        dmma_m8n8k4(de, ae, b.x);
+        dmma_m8n8k4(dd, ao, b.y);
+        v0 += ae;
+        if constexpr (R == 18) vl = fma(ao, tab[i].th, vl);  // t^17
+    }
+}
+
+// End of a tensor-core row batch: the unpaired columns (l = 0, t = 1: every j, so every tile
+// column of every lane plus the FP64 moments once on t4 = 0; l = q/2, t = 0: j = 0 only, on
+// t4 = 1), the 4-lane reduction of the FP64 moments, and the raw moment parts into Cs (the w_j
+// factor is applied in one pass after the loop).  Tile column n = 2 t4 + e holds j = 2 + 2n
+// (even tile) and j = 1 + 2n (odd tile).
+template <int R, bool MU0>
+__device__ __forceinline__ void k1_tc_finish_row(const K1Params& P, double2 x0, double2 xh, int part, int t4,
+                                                 uint32_t k1, double (&de)[2], double (&dd)[2], double v0,
+                                                 double vl, double2* Cs) {
+    if constexpr (!MU0) {
+        x0 = cmul(x0, P.phase0);
+        xh = cmul(xh, P.phaseh);
+    }
+    const double x0p = part ? x0.y : x0.x, xhp = part ? xh.y : xh.x;  // zero when not in the view
+    de[0] += x0p;
+    de[1] += x0p;
+    dd[0] += x0p;
+    dd[1] += x0p;
+    if (t4 == 0) {
+        v0 += x0p;
+        vl += x0p;
+    }
+    if (t4 == 1) v0 += xhp;
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, off);
+        vl += __shfl_xor_sync(0xffffffffu, vl, off);
+    }
+    if (k1 >= P.P1) return;
+    double* cs = reinterpret_cast<double*>(Cs);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int n = 2 * t4 + e, je = 2 + 2 * n, jo = 1 + 2 * n;
+        if (je < R) cs[2 * ((size_t)je * P.P1 + k1) + part] = de[e];
+        if (jo < R) cs[2 * ((size_t)jo * P.P1 + k1) + part] = dd[e];
+    }
+    if (t4 == 0) cs[2 * (size_t)k1 + part] = v0;
+    if (R == 18 && t4 == 1) cs[2 * ((size_t)17 * P.P1 + k1) + part] = vl;
 }
 
 // Sum tail (few output bins, W <= p/4), which replaces K2.  CTA (c, b) writes its residue row
@@ -212,6 +325,7 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     unsigned* s_ticket = reinterpret_cast<unsigned*>(part + (size_t)nw * 64);
     __threadfence();
     __syncthreads();
+    PFT_STAMP(5)
     if (tid == 0) {
         st_release_u32(ready + c, 1u);
         *s_ticket = atomicAdd(ctl, 1u);
@@ -284,7 +398,8 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const uint32_t S = P.stages;
     unsigned char* ring = smem_raw;                                                     // [S] stages
-    double2* Cs = reinterpret_cast<double2*>(smem_raw + (size_t)S * K1_STAGE_BYTES);  // [R][P1]
+    constexpr uint32_t STAGE = k1_stage_bytes(R);
+    double2* Cs = reinterpret_cast<double2*>(smem_raw + (size_t)S * STAGE);  // [R][P1]
     double2* tw1 = Cs + (size_t)R * P.P1;                                              // omega_P1^t
     uint64_t* full = reinterpret_cast<uint64_t*>(tw1 + P.P1);
     uint64_t* empty = full + S;
@@ -311,18 +426,28 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         // ---- producer: one elected lane streams front/mirror boxes + table slices
         if (lane == 0 && total > 0) {
             prefetch_tensormap(&tmap);
+            uint32_t s = 0, ph = 0, rb = 0, ch = 0;  // slot, its phase; row batch, chunk
             for (uint32_t it = 0; it < total; ++it) {
-                const uint32_t s = it % S, n = it / S;
-                if (n > 0) mbar_wait(&empty[s], (n - 1) & 1);
-                const uint32_t rb = it / nch, ch = it - rb * nch;
-                unsigned char* st = ring + (size_t)s * K1_STAGE_BYTES;
-                mbar_arrive_expect_tx(&full[s], K1_STAGE_BYTES);
+                if (it >= S) mbar_wait(&empty[s], ph ^ 1u);
+                unsigned char* st = ring + (size_t)s * STAGE;
+                mbar_arrive_expect_tx(&full[s], STAGE);
                 const int row0 = (int)(rb * K1_BR);
                 const int f0 = P.fcol0 + (int)(ch * K1_CP);
                 const int m0 = P.mcol0 - (int)(ch * K1_CP) - (K1_CP - 1);  // may be < 0: zero fill
                 tma_load_4d(st, &tmap, 2 * f0, (int)c, row0, (int)b, &full[s]);
                 tma_load_4d(st + K1_BOX_BYTES, &tmap, 2 * m0, (int)c, row0, (int)b, &full[s]);
                 bulk_load(st + 2 * K1_BOX_BYTES, P.pairtab + P.gp0 + ch * K1_CP, K1_TAB_BYTES, &full[s]);
+                if constexpr (k1_tc(R))
+                    bulk_load(st + 2 * K1_BOX_BYTES + K1_TAB_BYTES, P.tcfrag + (size_t)(P.gp0 + ch * K1_CP) * 8,
+                              K1_TC_BYTES, &full[s]);
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+                if (++ch == nch) {
+                    ch = 0;
+                    ++rb;
+                }
             }
         }
     } else {
@@ -330,25 +455,62 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         // FFT twiddles omega_P1^t = omega_p^{t P2} for the tail, staged while the first
         // TMA boxes are in flight (read after the __syncthreads that ends the main loop)
         for (uint32_t t = tid; t < P.P1; t += K1_CONSUMER_WARPS * 32) tw1[t] = __ldg(P.omega + (size_t)t * P.P2);
+        if constexpr (k1_tc(R)) {
+            const int g = lane >> 2, t4 = lane & 3, part = g & 1;
+            const int rin = warp * 4 + (g >> 1);  // row within the box
+            uint32_t s = 0, ph = 0;
+            for (uint32_t rb = 0; rb < nrb; ++rb) {
+                double de[2] = {0.0, 0.0}, dd[2] = {0.0, 0.0}, v0 = 0.0, vl = 0.0;
+                const uint32_t k1 = rb * K1_BR + rin;
+                // unpaired columns l = 0 (all lanes) and l = q/2 (t4 = 1): loads issued now,
+                // consumed after the chunk loop
+                double2 x0 = make_double2(0.0, 0.0), xh = make_double2(0.0, 0.0);
+                if (k1 < P.P1) {
+                    const double2* row = P.a + (size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride;
+                    if (P.single0_col >= 0) x0 = __ldg(row + P.single0_col);
+                    if (t4 == 1 && P.singleh_col >= 0) xh = __ldg(row + P.singleh_col);
+                }
+                for (uint32_t ch = 0; ch < nch; ++ch) {
+                    mbar_wait(&full[s], ph);
+#ifdef PFT_TIMELINE
+                    if (rb == 0 && ch == 0) PFT_STAMP(1)
+#endif
+                    __syncwarp();
+                    const uint32_t valid = min((uint32_t)K1_CP, npairs - ch * K1_CP);
+                    const unsigned char* stage = ring + (size_t)s * STAGE;
+                    if (valid == (uint32_t)K1_CP)
+                        k1_tc_stage<R, MU0, true>(stage, rin, part, t4, g, valid, de, dd, v0, vl);
+                    else
+                        k1_tc_stage<R, MU0, false>(stage, rin, part, t4, g, valid, de, dd, v0, vl);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[s]);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                k1_tc_finish_row<R, MU0>(P, x0, xh, part, t4, k1, de, dd, v0, vl, Cs);
+            }
+        } else {
+        constexpr int JS = k1_js(R, MU0), H = (R + JS - 1) / JS;
         const int li = lane & (K1_LANES_PER_ROW - 1);
         const int rin = (warp * 32 + lane) / K1_LANES_PER_ROW;  // row within the box
+        uint32_t s = 0, ph = 0;                                  // ring slot and its phase
         for (uint32_t rb = 0; rb < nrb; ++rb) {
-            double are[R], aim[R];
+            double are[H], aim[H];
 #pragma unroll
-            for (int j = 0; j < R; ++j) are[j] = aim[j] = 0.0;
+            for (int j = 0; j < H; ++j) are[j] = aim[j] = 0.0;
             const uint32_t k1 = rb * K1_BR + rin;
-            // unpaired column of this lane (l = 0 on li 0, l = q/2 on li 1): issue the load now,
-            // consume it after the chunk loop so its DRAM latency is hidden
-            const int scol = li == 0 ? P.single0_col : (li == 1 ? P.singleh_col : -1);
+            // unpaired columns (l = 0 on the lanes li < JS, l = q/2 on li = JS): issue the load
+            // now, consume it after the chunk loop so its DRAM latency is hidden
+            const int scol = li < JS ? P.single0_col : (li == JS ? P.singleh_col : -1);
             double2 xs = make_double2(0.0, 0.0);
             if (k1 < P.P1 && scol >= 0)
                 xs = __ldg(P.a + (size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride + scol);
             for (uint32_t ch = 0; ch < nch; ++ch) {
-                const uint32_t it = rb * nch + ch;
-                const uint32_t s = it % S, n = it / S;
-                mbar_wait(&full[s], n & 1);
+                mbar_wait(&full[s], ph);
 #ifdef PFT_TIMELINE
-                if (it == 0) PFT_STAMP(1)
+                if (rb == 0 && ch == 0) PFT_STAMP(1)
 #endif
                 // Reconverge before touching the stage: lane 0's `empty` arrive below leaves
                 // the warp diverged, and reading a stage from a diverged warp was observed to
@@ -357,22 +519,32 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                 // full chunks skip the per-pair masking (selects and zero moves were about as
                 // many instructions as the FP64 work); only a row's last chunk can be partial
                 const uint32_t valid = min((uint32_t)K1_CP, npairs - ch * K1_CP);
-                const unsigned char* stage = ring + (size_t)s * K1_STAGE_BYTES;
+                const unsigned char* stage = ring + (size_t)s * STAGE;
                 if (valid == (uint32_t)K1_CP)
-                    k1_accumulate_stage<R, MU0, true>(stage, rin, li, valid, are, aim);
+                    k1_accumulate_stage<R, JS, MU0, true>(stage, rin, li, valid, are, aim);
                 else
-                    k1_accumulate_stage<R, MU0, false>(stage, rin, li, valid, are, aim);
+                    k1_accumulate_stage<R, JS, MU0, false>(stage, rin, li, valid, are, aim);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);  // stage s may be refilled
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
-            k1_finish_row<R, MU0>(P, xs, scol, li, k1, are, aim, Cs);
+            k1_finish_row<R, JS, MU0>(P, xs, scol, li, k1, are, aim, Cs);
         }
+        }  // vector path
     }
     // All of A has been read: let K2 (launched with programmatic stream serialization)
     // get scheduled and run its prologue while this grid finishes its FFT tail.
     PFT_STAMP(2)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __syncthreads();
+    if constexpr (k1_tc(R)) {  // C = w_j acc_j (the vector path applies it at the row store)
+        for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x)
+            Cs[idx] = cmul(Cs[idx], __ldg(P.w + idx / P.P1));
+        __syncthreads();
+    }
     PFT_STAMP(3)
 
     // First FFT pass over k1 (length P1) for every column j, in shared memory; the ring is

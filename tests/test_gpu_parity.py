@@ -289,3 +289,37 @@ def test_degenerate_shapes(pft, oracle, N, M, mu, p):
     gpu = pft.execute(plan, a).values
     ref = oracle.execute(plan, a)
     assert rel_l2(gpu, ref) <= GATE, plan.json()
+
+
+def _m_for_terms(pft, r: int, p: int):
+    """Smallest M whose plan at (eps = 1e-12, p) needs exactly r terms, or None."""
+    for M in range(0, 3 * p):
+        try:
+            got = pft.min_terms(1e-12, M, p)
+        except Exception:
+            return None
+        if got == r:
+            return M
+        if got > r:
+            return None
+    return None
+
+
+@pytest.mark.parametrize("mu", [0, 1234])
+@pytest.mark.parametrize("r", list(range(2, 26)))
+def test_every_contraction_path(pft, oracle, r, mu):
+    """Every r instantiation of K1 against the oracle, with and without phase factors: the
+    unsplit vector contraction, the two-lane j split (k1_js) and the FP64 tensor-core
+    (DMMA) contraction (k1_tc, r = 16..18) all meet the gate."""
+    N = 2 ** 15
+    for p in (256, 8192):
+        M = _m_for_terms(pft, r, p)
+        if M is not None:
+            break
+    else:
+        pytest.skip(f"no M gives r = {r}")
+    plan = pft.build_plan(N, M, mu, p, 1e-12)
+    assert plan.r == r
+    a = uniform(pft, 100 + r, N)
+    got = pft.execute(plan, a).values
+    assert rel_l2(got, oracle.execute(plan, a)) <= GATE
