@@ -45,7 +45,16 @@ constexpr int K1_MIN_STAGES = PFT_K1_MIN_STAGES, K1_MAX_STAGES = 8;
 #endif
 __host__ __device__ constexpr bool k1_tc(int r) { return r >= PFT_K1_TC_MIN_R && r <= 18; }
 constexpr uint32_t K1_TC_BYTES = K1_CP * 16 * 8;  // 16 pairs x 8 columns x {even, odd} doubles
-__host__ __device__ constexpr uint32_t k1_stage_bytes(int r) { return K1_STAGE_BYTES + (k1_tc(r) ? K1_TC_BYTES : 0); }
+// Tensor-core stages: each box arrives as two 8-pair halves (128-byte rows) with the TMA
+// 128-byte swizzle (16-byte chunk c of row y at c ^ (y & 7)), so the four rows a warp reads
+// together ({0, 1, 4, 5} + offset) hit eight distinct chunks: 2 wavefronts per operand load
+// instead of 4.  Swizzled destinations need 1024-byte alignment, hence the padded stage.
+constexpr uint32_t K1_TC_DATA_BYTES = K1_STAGE_BYTES + K1_TC_BYTES;                // bytes landed per stage
+constexpr uint32_t K1_TC_STAGE_BYTES = (K1_TC_DATA_BYTES + 1023) / 1024 * 1024;    // stage stride
+static_assert(K1_CP == 16 && K1_BR == 32, "tensor-core stage layout assumes 32 rows x 16 pairs");
+__host__ __device__ constexpr uint32_t k1_stage_bytes(int r) { return k1_tc(r) ? K1_TC_STAGE_BYTES : K1_STAGE_BYTES; }
+__host__ __device__ constexpr uint32_t k1_stage_data_bytes(int r) { return k1_tc(r) ? K1_TC_DATA_BYTES : K1_STAGE_BYTES; }
+__host__ __device__ constexpr uint32_t k1_ring_align_slack(int r) { return k1_tc(r) ? 1024 : 0; }
 __host__ __device__ constexpr int k1_min_stages(int r) { return k1_tc(r) ? 3 : K1_MIN_STAGES; }
 inline size_t k1_min_ring_bytes(int r) { return (size_t)k1_min_stages(r) * k1_stage_bytes(r); }
 static_assert(K1_TC_BYTES % 128 == 0, "TMA destinations stay 128-byte aligned");
@@ -146,7 +155,8 @@ struct GenParams {
 // (needs r*P1*16 <= the smallest ring)
 inline size_t k1_smem_bytes(int r, uint32_t P1, uint32_t stages) {
     const size_t p1 = P1 ? P1 : 1;
-    return (size_t)stages * k1_stage_bytes(r) + sizeof(double2) * ((size_t)r * p1 + p1) + 2 * stages * sizeof(uint64_t);
+    return k1_ring_align_slack(r) + (size_t)stages * k1_stage_bytes(r) + sizeof(double2) * ((size_t)r * p1 + p1) +
+           2 * stages * sizeof(uint64_t);
 }
 // K1 ring depth: as deep as possible while two CTAs still share an SM.
 inline uint32_t k1_pick_stages(int r, uint32_t P1) {

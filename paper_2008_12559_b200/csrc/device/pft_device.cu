@@ -364,11 +364,14 @@ CUtensorMap make_input_map(const pft_dplan_s* d, const void* base, uint64_t row_
     const cuuint64_t row_bytes = row_stride * 16;
     const cuuint64_t strides[3] = {row_bytes, row_bytes * d->P2,
                                    (batch > 1 ? batch_stride : d->P1 * d->P2 * row_stride) * 16};
-    const cuuint32_t box[4] = {2 * pftdev::K1_CP, 1, pftdev::K1_BR, 1};
+    // tensor-core plans: 8-pair half boxes (128-byte rows) with the 128-byte swizzle
+    const bool tc = pftdev::k1_tc(d->host.r);
+    const cuuint32_t box[4] = {(cuuint32_t)(tc ? pftdev::K1_CP : 2 * pftdev::K1_CP), 1, (cuuint32_t)pftdev::K1_BR, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUresult r = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims,
                                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                            tc ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(PFT_ERR_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
     return map;
@@ -618,10 +621,10 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         for (int j = 1; j < 32; ++j) pw[j] = pw[j - 1] * t;  // pw[1] = 1 * t = t exactly
         pairtab[l] = {H.phase[l].real(), H.phase[l].imag(), t, pw[h_split]};
         if (tc) {
-            for (int g = 0; g < 8; ++g) {
-                const int je = 2 + 2 * g, jo = 1 + 2 * g;
-                tcfrag[l * 16 + 2 * g] = je < H.r ? pw[je] : 0.0;
-                tcfrag[l * 16 + 2 * g + 1] = jo < H.r ? pw[jo] : 0.0;
+            for (int g = 0; g < 8; ++g) {  // column g stored at g ^ 2 (l & 3) (bank spread, k1_tc_stage)
+                const int je = 2 + 2 * g, jo = 1 + 2 * g, gs = g ^ (2 * (int)(l & 3));
+                tcfrag[l * 16 + 2 * gs] = je < H.r ? pw[je] : 0.0;
+                tcfrag[l * 16 + 2 * gs + 1] = jo < H.r ? pw[jo] : 0.0;
             }
         }
     }

@@ -189,8 +189,9 @@ __device__ __forceinline__ void k1_finish_row(const K1Params& P, double2 xs, int
     }
 }
 
-// ---- tensor-core contraction (k1_tc(R)): one warp = 4 rows of the box as the 8 m-rows of a
-// DMMA tile (m = 2 * row + part, part 0/1 = re/im); per k-step the 4 k-columns are pairs
+// ---- tensor-core contraction (k1_tc(R)): one warp = 4 rows of the box ({0, 1, 4, 5} + 8 (w / 2)
+// + 2 (w % 2): distinct swizzle chunks) as the 8 m-rows of a DMMA tile (m = 2 * row index +
+// part, part 0/1 = re/im); per k-step the 4 k-columns are pairs
 // ks * 4 + t4.  A = (b_l + b_{q-l}) parts against the even-moment tile, (b_l - b_{q-l}) parts
 // against the odd-moment tile; the MMA sums over the pairs, so only the FP64-pipe moments
 // (j = 0, and j = 17 for R = 18) need a cross-lane reduction at the end of the row batch.
@@ -200,11 +201,17 @@ __device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) 
                  : "d"(a), "d"(b));
 }
 
+// Element (row y, pair column j) of a swizzled tensor-core box (two 8-pair halves of
+// [32 rows][128 B], 16-byte chunk c of row y stored at chunk c ^ (y & 7)).
+__device__ __forceinline__ const double2* tc_box_elt(const unsigned char* box, int y, int j) {
+    return reinterpret_cast<const double2*>(box + (j >> 3) * (K1_BR * 128) + y * 128 + (((j & 7) ^ (y & 7)) << 4));
+}
+
+// gs: this lane's fragment column g stored at g ^ 2 (pair & 3) (global pair index): the eight
+// lanes of a 128-bit load phase (g = 2h, 2h + 1; t4 = 0..3) then read eight distinct chunks.
 template <int R, bool MU0, bool FULL>
-__device__ __forceinline__ void k1_tc_stage(const unsigned char* st, int rin, int part, int t4, int g, uint32_t valid,
+__device__ __forceinline__ void k1_tc_stage(const unsigned char* st, int rin, int part, int t4, int gs, uint32_t valid,
                                             double (&de)[2], double (&dd)[2], double& v0, double& vl) {
-    const double2* front = reinterpret_cast<const double2*>(st) + rin * K1_CP;
-    const double2* mirror = reinterpret_cast<const double2*>(st + K1_BOX_BYTES) + rin * K1_CP;
     const PairEntry* tab = reinterpret_cast<const PairEntry*>(st + 2 * K1_BOX_BYTES);
     const double2* frag = reinterpret_cast<const double2*>(st + 2 * K1_BOX_BYTES + K1_TAB_BYTES);  // [pair][g]
 #pragma unroll
@@ -212,22 +219,24 @@ __device__ __forceinline__ void k1_tc_stage(const unsigned char* st, int rin, in
         const int i = ks * 4 + t4;
         const bool ok = FULL || (uint32_t)i < valid;
         double ae, ao;  // this lane's part of phase_l x1 + conj(phase_l) x2 and of the difference
+        const double2* p1 = tc_box_elt(st, rin, i);                                // column l
+        const double2* p2 = tc_box_elt(st + K1_BOX_BYTES, rin, K1_CP - 1 - i);     // column q - l
         if constexpr (MU0) {
-            const double x1 = ok ? reinterpret_cast<const double*>(front + i)[part] : 0.0;
-            const double x2 = ok ? reinterpret_cast<const double*>(mirror + (K1_CP - 1 - i))[part] : 0.0;
+            const double x1 = ok ? reinterpret_cast<const double*>(p1)[part] : 0.0;
+            const double x2 = ok ? reinterpret_cast<const double*>(p2)[part] : 0.0;
             ae = x1 + x2;
             ao = x1 - x2;
         } else {
             const double2 z = make_double2(0.0, 0.0);
-            const double2 x1 = ok ? front[i] : z;
-            const double2 x2 = ok ? mirror[K1_CP - 1 - i] : z;
+            const double2 x1 = ok ? *p1 : z;
+            const double2 x2 = ok ? *p2 : z;
             const double2 cs = *reinterpret_cast<const double2*>(&tab[i].c);
             const double2 su = make_double2(x1.x + x2.x, x1.y + x2.y);
             const double2 di = make_double2(x1.x - x2.x, x1.y - x2.y);
             ae = part ? fma(cs.x, su.y, cs.y * di.x) : fma(cs.x, su.x, -cs.y * di.y);
             ao = part ? fma(cs.x, di.y, cs.y * su.x) : fma(cs.x, di.x, -cs.y * su.y);
         }
-        const double2 b = frag[i * 8 + g];  // {t^(2+2g), t^(1+2g)}
+        const double2 b = frag[i * 8 + gs];  // {t^(2+2g), t^(1+2g)}
         dmma_m8n8k4(de, ae, b.x);
         dmma_m8n8k4(dd, ao, b.y);
         v0 += ae;
@@ -399,7 +408,9 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     const uint32_t S = P.stages;
     unsigned char* ring = smem_raw;                                                     // [S] stages
     constexpr uint32_t STAGE = k1_stage_bytes(R);
-    double2* Cs = reinterpret_cast<double2*>(smem_raw + (size_t)S * STAGE);  // [R][P1]
+    if constexpr (k1_ring_align_slack(R) > 0)  // swizzled TMA destinations: 1024-byte aligned ring
+        ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
+    double2* Cs = reinterpret_cast<double2*>(smem_raw + k1_ring_align_slack(R) + (size_t)S * STAGE);  // [R][P1]
     double2* tw1 = Cs + (size_t)R * P.P1;                                              // omega_P1^t
     uint64_t* full = reinterpret_cast<uint64_t*>(tw1 + P.P1);
     uint64_t* empty = full + S;
@@ -430,12 +441,20 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
             for (uint32_t it = 0; it < total; ++it) {
                 if (it >= S) mbar_wait(&empty[s], ph ^ 1u);
                 unsigned char* st = ring + (size_t)s * STAGE;
-                mbar_arrive_expect_tx(&full[s], STAGE);
+                mbar_arrive_expect_tx(&full[s], k1_stage_data_bytes(R));
                 const int row0 = (int)(rb * K1_BR);
                 const int f0 = P.fcol0 + (int)(ch * K1_CP);
                 const int m0 = P.mcol0 - (int)(ch * K1_CP) - (K1_CP - 1);  // may be < 0: zero fill
-                tma_load_4d(st, &tmap, 2 * f0, (int)c, row0, (int)b, &full[s]);
-                tma_load_4d(st + K1_BOX_BYTES, &tmap, 2 * m0, (int)c, row0, (int)b, &full[s]);
+                if constexpr (k1_tc(R)) {  // 8-pair swizzled halves
+                    constexpr int HB = K1_BR * 128;
+                    tma_load_4d(st, &tmap, 2 * f0, (int)c, row0, (int)b, &full[s]);
+                    tma_load_4d(st + HB, &tmap, 2 * (f0 + 8), (int)c, row0, (int)b, &full[s]);
+                    tma_load_4d(st + K1_BOX_BYTES, &tmap, 2 * m0, (int)c, row0, (int)b, &full[s]);
+                    tma_load_4d(st + K1_BOX_BYTES + HB, &tmap, 2 * (m0 + 8), (int)c, row0, (int)b, &full[s]);
+                } else {
+                    tma_load_4d(st, &tmap, 2 * f0, (int)c, row0, (int)b, &full[s]);
+                    tma_load_4d(st + K1_BOX_BYTES, &tmap, 2 * m0, (int)c, row0, (int)b, &full[s]);
+                }
                 bulk_load(st + 2 * K1_BOX_BYTES, P.pairtab + P.gp0 + ch * K1_CP, K1_TAB_BYTES, &full[s]);
                 if constexpr (k1_tc(R))
                     bulk_load(st + 2 * K1_BOX_BYTES + K1_TAB_BYTES, P.tcfrag + (size_t)(P.gp0 + ch * K1_CP) * 8,
@@ -456,8 +475,11 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         // TMA boxes are in flight (read after the __syncthreads that ends the main loop)
         for (uint32_t t = tid; t < P.P1; t += K1_CONSUMER_WARPS * 32) tw1[t] = __ldg(P.omega + (size_t)t * P.P2);
         if constexpr (k1_tc(R)) {
-            const int g = lane >> 2, t4 = lane & 3, part = g & 1;
-            const int rin = warp * 4 + (g >> 1);  // row within the box
+            const int g = lane >> 2, t4 = lane & 3, part = g & 1, rr = g >> 1;
+            // row within the box: the 16 lanes of a 64-bit load phase (rr = 0, 1) take rows y and
+            // y + 4, whose swizzled chunks differ in bit 2 (conflict-free operand loads)
+            const int rin = 8 * (warp >> 1) + 2 * (warp & 1) + 4 * (rr & 1) + (rr >> 1);
+            const int fsw = 2 * (int)((P.gp0 + (uint32_t)t4) & 3u);  // fragment-table swizzle of this lane's pairs
             uint32_t s = 0, ph = 0;
             for (uint32_t rb = 0; rb < nrb; ++rb) {
                 double de[2] = {0.0, 0.0}, dd[2] = {0.0, 0.0}, v0 = 0.0, vl = 0.0;
@@ -479,9 +501,9 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                     const uint32_t valid = min((uint32_t)K1_CP, npairs - ch * K1_CP);
                     const unsigned char* stage = ring + (size_t)s * STAGE;
                     if (valid == (uint32_t)K1_CP)
-                        k1_tc_stage<R, MU0, true>(stage, rin, part, t4, g, valid, de, dd, v0, vl);
+                        k1_tc_stage<R, MU0, true>(stage, rin, part, t4, g ^ fsw, valid, de, dd, v0, vl);
                     else
-                        k1_tc_stage<R, MU0, false>(stage, rin, part, t4, g, valid, de, dd, v0, vl);
+                        k1_tc_stage<R, MU0, false>(stage, rin, part, t4, g ^ fsw, valid, de, dd, v0, vl);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
                     if (++s == S) {

@@ -3,7 +3,7 @@
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p ${VARIANT_DIR:-variants}
-python -m paper_2008_12559_b200.build >/dev/null
+[ -n "$SKIP_MAIN" ] || python -m paper_2008_12559_b200.build >/dev/null
 FLAGS="-std=c++20 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC,-fopenmp -I include -I paper_2008_12559_b200/csrc -I paper_2008_12559_b200/build/gen"
 for spec in "$@"; do
   name=${spec%%:*}; defs=${spec#*:}
