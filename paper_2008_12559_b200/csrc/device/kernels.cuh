@@ -37,19 +37,20 @@ constexpr int K1_MIN_STAGES = PFT_K1_MIN_STAGES, K1_MAX_STAGES = 8;
 // (r = 18) j = 17 stay on the FP64 pipe.  A DMMA does 256 FMAs per issue: the contraction
 // sheds the power chain and most of its instruction overhead.  Stages carry the fragment
 // slice, so the ring may be 3 stages deep to keep two CTAs per SM.
-// Measured (same box): C3 p = 256, r = 18: 1190 vs 1276 us per batch (split vector path);
-// r = 14: no gain (1404 vs 1405 us); r <= 9 slower (C2b r = 8: 56.8 vs 41.5 us; C4 r = 9:
-// 27.6 vs 20.9 us), so from r = 16.
+// Measured (same box, swizzled 4-stage layout): C3 p = 256, r = 18: 1017 vs 1276 us per batch
+// (split vector path); C3 p = 512, r = 14: 1180 vs 1400 us; C2c p = 2^15, r = 14 with phases:
+// 71.6 vs 79.6 us; C2c p = 2^16, r = 12: 83.8 vs 110.5 us.  An earlier unswizzled layout was
+// slower than the vector path at r <= 9 (C2b r = 8: 56.8 vs 41.5 us), so from r = 12.
 #ifndef PFT_K1_TC_MIN_R
-#define PFT_K1_TC_MIN_R 16
+#define PFT_K1_TC_MIN_R 12
 #endif
 __host__ __device__ constexpr bool k1_tc(int r) { return r >= PFT_K1_TC_MIN_R && r <= 18; }
 constexpr uint32_t K1_TC_BYTES = K1_CP * 16 * 8;  // 16 pairs x 8 columns x {even, odd} doubles
 // Tensor-core stages: each box arrives as two 8-pair halves (128-byte rows) with the TMA
 // 128-byte swizzle (16-byte chunk c of row y at c ^ (y & 7)), so the four rows a warp reads
 // together ({0, 1, 4, 5} + offset) hit eight distinct chunks: 2 wavefronts per operand load
-// instead of 4.  Swizzled destinations need 1024-byte alignment, hence the padded stage.
-constexpr uint32_t K1_TC_DATA_BYTES = K1_STAGE_BYTES + K1_TC_BYTES;                // bytes landed per stage
+// instead of 4.  Swizzled destinations need 1024-byte alignment (the 18 KB stage is a multiple).
+constexpr uint32_t K1_TC_DATA_BYTES = 2 * K1_BOX_BYTES + K1_TC_BYTES;             // bytes landed per stage
 constexpr uint32_t K1_TC_STAGE_BYTES = (K1_TC_DATA_BYTES + 1023) / 1024 * 1024;    // stage stride
 static_assert(K1_CP == 16 && K1_BR == 32, "tensor-core stage layout assumes 32 rows x 16 pairs");
 __host__ __device__ constexpr uint32_t k1_stage_bytes(int r) { return k1_tc(r) ? K1_TC_STAGE_BYTES : K1_STAGE_BYTES; }

@@ -209,11 +209,14 @@ __device__ __forceinline__ const double2* tc_box_elt(const unsigned char* box, i
 
 // gs: this lane's fragment column g stored at g ^ 2 (pair & 3) (global pair index): the eight
 // lanes of a 128-bit load phase (g = 2h, 2h + 1; t4 = 0..3) then read eight distinct chunks.
+// The stage holds the two boxes and the fragment slice only (18 KB: four stages fit beside the
+// C slab at two CTAs per SM); phases (mu != 0) come from the L1-resident pair table `ptab`
+// (this chunk's entries), and t^17 (R = 18) = t^16 t from the pair's own fragment record.
 template <int R, bool MU0, bool FULL>
-__device__ __forceinline__ void k1_tc_stage(const unsigned char* st, int rin, int part, int t4, int gs, uint32_t valid,
-                                            double (&de)[2], double (&dd)[2], double& v0, double& vl) {
-    const PairEntry* tab = reinterpret_cast<const PairEntry*>(st + 2 * K1_BOX_BYTES);
-    const double2* frag = reinterpret_cast<const double2*>(st + 2 * K1_BOX_BYTES + K1_TAB_BYTES);  // [pair][g]
+__device__ __forceinline__ void k1_tc_stage(const unsigned char* st, const PairEntry* __restrict__ ptab, int rin,
+                                            int part, int t4, int gs, int fsw, uint32_t valid, double (&de)[2],
+                                            double (&dd)[2], double& v0, double& vl) {
+    const double2* frag = reinterpret_cast<const double2*>(st + 2 * K1_BOX_BYTES);  // [pair][g ^ fsw]
 #pragma unroll
     for (int ks = 0; ks < K1_CP / 4; ++ks) {
         const int i = ks * 4 + t4;
@@ -230,7 +233,7 @@ __device__ __forceinline__ void k1_tc_stage(const unsigned char* st, int rin, in
             const double2 z = make_double2(0.0, 0.0);
             const double2 x1 = ok ? *p1 : z;
             const double2 x2 = ok ? *p2 : z;
-            const double2 cs = *reinterpret_cast<const double2*>(&tab[i].c);
+            const double2 cs = __ldg(reinterpret_cast<const double2*>(&ptab[i].c));
             const double2 su = make_double2(x1.x + x2.x, x1.y + x2.y);
             const double2 di = make_double2(x1.x - x2.x, x1.y - x2.y);
             ae = part ? fma(cs.x, su.y, cs.y * di.x) : fma(cs.x, su.x, -cs.y * di.y);
@@ -240,7 +243,10 @@ __device__ __forceinline__ void k1_tc_stage(const unsigned char* st, int rin, in
         dmma_m8n8k4(de, ae, b.x);
         dmma_m8n8k4(dd, ao, b.y);
         v0 += ae;
-        if constexpr (R == 18) vl = fma(ao, tab[i].th, vl);  // t^17
+        if constexpr (R == 18) {  // t^17 = t^16 (g = 7, even) * t (g = 0, odd)
+            const double t16 = frag[i * 8 + (7 ^ fsw)].x, t1 = frag[i * 8 + fsw].y;
+            vl = fma(ao, t16 * t1, vl);
+        }
     }
 }
 
@@ -455,10 +461,10 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                     tma_load_4d(st, &tmap, 2 * f0, (int)c, row0, (int)b, &full[s]);
                     tma_load_4d(st + K1_BOX_BYTES, &tmap, 2 * m0, (int)c, row0, (int)b, &full[s]);
                 }
-                bulk_load(st + 2 * K1_BOX_BYTES, P.pairtab + P.gp0 + ch * K1_CP, K1_TAB_BYTES, &full[s]);
                 if constexpr (k1_tc(R))
-                    bulk_load(st + 2 * K1_BOX_BYTES + K1_TAB_BYTES, P.tcfrag + (size_t)(P.gp0 + ch * K1_CP) * 8,
-                              K1_TC_BYTES, &full[s]);
+                    bulk_load(st + 2 * K1_BOX_BYTES, P.tcfrag + (size_t)(P.gp0 + ch * K1_CP) * 8, K1_TC_BYTES, &full[s]);
+                else
+                    bulk_load(st + 2 * K1_BOX_BYTES, P.pairtab + P.gp0 + ch * K1_CP, K1_TAB_BYTES, &full[s]);
                 if (++s == S) {
                     s = 0;
                     ph ^= 1u;
@@ -500,10 +506,11 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                     __syncwarp();
                     const uint32_t valid = min((uint32_t)K1_CP, npairs - ch * K1_CP);
                     const unsigned char* stage = ring + (size_t)s * STAGE;
+                    const PairEntry* ptab = P.pairtab + P.gp0 + ch * K1_CP;
                     if (valid == (uint32_t)K1_CP)
-                        k1_tc_stage<R, MU0, true>(stage, rin, part, t4, g ^ fsw, valid, de, dd, v0, vl);
+                        k1_tc_stage<R, MU0, true>(stage, ptab, rin, part, t4, g ^ fsw, fsw, valid, de, dd, v0, vl);
                     else
-                        k1_tc_stage<R, MU0, false>(stage, rin, part, t4, g ^ fsw, valid, de, dd, v0, vl);
+                        k1_tc_stage<R, MU0, false>(stage, ptab, rin, part, t4, g ^ fsw, fsw, valid, de, dd, v0, vl);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
                     if (++s == S) {
