@@ -102,13 +102,20 @@ struct WarpsTeam {
     __device__ __forceinline__ void sync() const { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
 };
 
+// Bank swizzle of the buffer between the first two stages of a power-of-two transform: the
+// first stage (Ns = 1) writes y[R j + r], 8 lanes of a 128-bit store phase R * 16 bytes apart
+// (8-way conflicts); XOR-ing the 16-byte slot within each 128-byte block with the block index
+// spreads them, and the second stage's contiguous reads stay conflict-free.
+__device__ __forceinline__ int fft_swz(int i) { return i ^ ((i >> 3) & 7); }
+
 // One Stockham stage with a radix known at compile time (2, 3, 4, 8).  When n is a power
 // of two (POW2) the index arithmetic uses shifts/masks (lg_nb = log2(n/R), lg_ns =
-// log2(Ns)); otherwise integer division.
+// log2(Ns)); otherwise integer division.  sw: 1 = swizzled destination, 2 = swizzled source
+// (POW2 only).  colw: per-column factor applied to the inputs (first stage), or null.
 template <int R, bool POW2, class TW>
 __device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__ src, double2* __restrict__ dst,
                                                      int ncols, int n, int Ns, int lg_nb, int lg_ns, const TW& tw,
-                                                     int t0, int nt) {
+                                                     int t0, int nt, int sw = 0, const double2* colw = nullptr) {
     const int nb = n / R;
     const uint32_t tstride = (uint32_t)(n / (Ns * R));
     for (int idx = t0; idx < ncols * nb; idx += nt) {
@@ -124,11 +131,20 @@ __device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__
             k = j % Ns;
             base = (j / Ns) * Ns * R + k;
         }
-        const double2* s = src + (size_t)col * n;
-        double2* d = dst + (size_t)col * n;
         double2 v[R];
+        if (POW2 && (sw & 2)) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = s[j + r * nb];
+            for (int r = 0; r < R; ++r) v[r] = src[fft_swz(col * n + j + r * nb)];
+        } else {
+            const double2* s = src + (size_t)col * n;
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[r] = s[j + r * nb];
+        }
+        if (colw) {
+            const double2 wc = colw[col];
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[r] = cmul(v[r], wc);
+        }
         if (k != 0) {
 #pragma unroll
             for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw((uint32_t)(k * r) * tstride));
@@ -137,8 +153,14 @@ __device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__
         if constexpr (R == 3) dft3(v[0], v[1], v[2]);
         if constexpr (R == 4) dft4(v[0], v[1], v[2], v[3]);
         if constexpr (R == 8) dft8(v);
+        if (POW2 && (sw & 1)) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) d[base + r * Ns] = v[r];
+            for (int r = 0; r < R; ++r) dst[fft_swz(col * n + base + r * Ns)] = v[r];
+        } else {
+            double2* d = dst + (size_t)col * n;
+#pragma unroll
+            for (int r = 0; r < R; ++r) d[base + r * Ns] = v[r];
+        }
     }
 }
 
@@ -168,9 +190,11 @@ __device__ __forceinline__ void stockham_stage_generic(const double2* __restrict
 
 // Full transform of ncols columns; returns the buffer holding the result (x or y).
 // Caller must team.sync() before (inputs written); the last stage ends with a team.sync().
+// colw: optional per-column factor folded into the first stage's loads (null = none).
 template <class TW, class Team = BlockTeam>
 __device__ __forceinline__ double2* fft_columns(double2* x, double2* y, int ncols, const FftRadices& plan,
-                                                const TW& tw, const Team team = Team{}) {
+                                                const TW& tw, const Team team = Team{},
+                                                const double2* colw = nullptr) {
     const int t0 = team.tid(), nt = team.size();
     double2* src = x;
     double2* dst = y;
@@ -182,20 +206,29 @@ __device__ __forceinline__ double2* fft_columns(double2* x, double2* y, int ncol
         const int R = plan.radix[st];
         const int lg_r = R == 2 ? 1 : R == 4 ? 2 : 3;
         const int lg_nb = lg_n - lg_r;
+        const double2* cw = st == 0 ? colw : nullptr;
         if (pow2) {
+            // swizzle the buffer between stages 0 and 1 (n >= 64 keeps every 8-block in a column)
+            const int sw = (n >= 64 && plan.count >= 2) ? (st == 0 ? 1 : st == 1 ? 2 : 0) : 0;
             switch (R) {
-                case 2: stockham_stage_fixed<2, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt); break;
-                case 4: stockham_stage_fixed<4, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt); break;
-                default: stockham_stage_fixed<8, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt); break;
+                case 2: stockham_stage_fixed<2, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw); break;
+                case 4: stockham_stage_fixed<4, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw); break;
+                default: stockham_stage_fixed<8, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw); break;
             }
             lg_ns += lg_r;
         } else {
             switch (R) {
-                case 2: stockham_stage_fixed<2, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt); break;
-                case 3: stockham_stage_fixed<3, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt); break;
-                case 4: stockham_stage_fixed<4, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt); break;
-                case 8: stockham_stage_fixed<8, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt); break;
-                default: stockham_stage_generic(src, dst, ncols, n, Ns, R, tw, t0, nt); break;
+                case 2: stockham_stage_fixed<2, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
+                case 3: stockham_stage_fixed<3, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
+                case 4: stockham_stage_fixed<4, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
+                case 8: stockham_stage_fixed<8, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
+                default:
+                    if (cw) {  // generic radix: apply the column factor in place first
+                        for (int i = t0; i < ncols * n; i += nt) src[i] = cmul(src[i], cw[i / n]);
+                        team.sync();
+                    }
+                    stockham_stage_generic(src, dst, ncols, n, Ns, R, tw, t0, nt);
+                    break;
             }
         }
         team.sync();

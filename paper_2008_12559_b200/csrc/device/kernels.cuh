@@ -152,11 +152,11 @@ struct GenParams {
     double2* out;
 };
 
-// ring + C slab + P1 twiddles + 2*S mbarriers; the ring doubles as the FFT scratch
+// ring + C slab + P1 twiddles + w (r) + 2*S mbarriers; the ring doubles as the FFT scratch
 // (needs r*P1*16 <= the smallest ring)
 inline size_t k1_smem_bytes(int r, uint32_t P1, uint32_t stages) {
     const size_t p1 = P1 ? P1 : 1;
-    return k1_ring_align_slack(r) + (size_t)stages * k1_stage_bytes(r) + sizeof(double2) * ((size_t)r * p1 + p1) +
+    return k1_ring_align_slack(r) + (size_t)stages * k1_stage_bytes(r) + sizeof(double2) * ((size_t)r * p1 + p1 + r) +
            2 * stages * sizeof(uint64_t);
 }
 // K1 ring depth: as deep as possible while two CTAs still share an SM.

@@ -300,7 +300,7 @@ __device__ __forceinline__ void k1_tc_finish_row(const K1Params& P, double2 x0, 
 // K1) could not allow.
 template <int R>
 __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* res, uint32_t c, uint32_t b,
-                                         unsigned char* scratch) {
+                                         unsigned char* scratch, double2 tail_tw) {
     const K2Params& Q = P.k2;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
     const int64_t Mh = (int64_t)((Q.W - 1) / 2);
@@ -309,8 +309,12 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     // omega_p^{(m mod p) c} = omega_p^{m1 c} omega_P2^{m2 c}: both factors from tables in the idle ring
     double2* twc = reinterpret_cast<double2*>(scratch);  // [P1] omega_p^{m1 c}
     double2* tw2 = twc + P.P1;                            // [P2] omega_P2^t
-    for (uint32_t t = tid; t < P.P1; t += nt) twc[t] = __ldg(P.omega + (size_t)t * c);  // m1 c < p
-    for (uint32_t t = tid; t < P.P2; t += nt) tw2[t] = __ldg(P.omega + (size_t)t * P.P1);
+    // entries t < blockDim.x were prefetched during the stream (tail_tw); the rest load now
+    for (uint32_t t = tid; t < P.P1 + P.P2; t += nt) {
+        double2 v = tail_tw;
+        if (t >= (uint32_t)nt) v = __ldg(P.omega + (t < P.P1 ? (size_t)t * c : (size_t)(t - P.P1) * P.P1));  // m1 c < p
+        twc[t] = v;  // twc[P1 + t'] is tw2[t']
+    }
     __syncthreads();
     double2* __restrict__ rowc = P.Y + ((size_t)b * P.P2 + c) * Q.W;
     for (uint64_t so = tid; so < Q.W; so += nt) {
@@ -418,7 +422,8 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     double2* Cs = reinterpret_cast<double2*>(smem_raw + k1_ring_align_slack(R) + (size_t)S * STAGE);  // [R][P1]
     double2* tw1 = Cs + (size_t)R * P.P1;                                              // omega_P1^t
-    uint64_t* full = reinterpret_cast<uint64_t*>(tw1 + P.P1);
+    double2* wsm = tw1 + P.P1;                                                         // w_j (tensor-core path)
+    uint64_t* full = reinterpret_cast<uint64_t*>(wsm + R);
     uint64_t* empty = full + S;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -431,6 +436,13 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         fence_barrier_init();
     }
     __syncthreads();  // barriers initialised: the producer starts streaming immediately
+    // sum tail: this thread's entry of the tail's twiddle tables, fetched now so its latency
+    // hides behind the stream (entry t < P1: omega_p^{t c}; P1 <= t < P1 + P2: omega_P2^{t - P1})
+    double2 tail_tw = make_double2(0.0, 0.0);
+    if (P.sum_tail && (uint32_t)tid < P.P1 + P.P2) {
+        const uint32_t t = tid;
+        tail_tw = __ldg(P.omega + (t < P.P1 ? (size_t)t * blockIdx.x : (size_t)(t - P.P1) * P.P1));
+    }
 
     const uint32_t c = blockIdx.x;  // residue class k = c (mod P2)
     const uint32_t b = blockIdx.y;  // signal
@@ -480,6 +492,8 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         // FFT twiddles omega_P1^t = omega_p^{t P2} for the tail, staged while the first
         // TMA boxes are in flight (read after the __syncthreads that ends the main loop)
         for (uint32_t t = tid; t < P.P1; t += K1_CONSUMER_WARPS * 32) tw1[t] = __ldg(P.omega + (size_t)t * P.P2);
+        if constexpr (k1_tc(R))
+            for (uint32_t t = tid; t < (uint32_t)R; t += K1_CONSUMER_WARPS * 32) wsm[t] = __ldg(P.w + t);
         if constexpr (k1_tc(R)) {
             const int g = lane >> 2, t4 = lane & 3, part = g & 1, rr = g >> 1;
             // row within the box: the 16 lanes of a 64-bit load phase (rr = 0, 1) take rows y and
@@ -569,9 +583,10 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     PFT_STAMP(2)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __syncthreads();
-    if constexpr (k1_tc(R)) {  // C = w_j acc_j (the vector path applies it at the row store)
-        for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x)
-            Cs[idx] = cmul(Cs[idx], __ldg(P.w + idx / P.P1));
+    // C = w_j acc_j: the vector path applies w_j at the row store; the tensor-core path folds
+    // it into the first FFT stage's loads (or one pass when there is no FFT)
+    if (k1_tc(R) && P.P1 <= 1) {
+        for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) Cs[idx] = cmul(Cs[idx], wsm[idx / P.P1]);
         __syncthreads();
     }
     PFT_STAMP(3)
@@ -579,14 +594,16 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     // First FFT pass over k1 (length P1) for every column j, in shared memory; the ring is
     // idle now and serves as the Stockham scratch buffer.
     const double2* res = Cs;
-    if (P.P1 > 1) res = fft_columns(Cs, reinterpret_cast<double2*>(ring), R, P.fft, SmemTwiddles{tw1});
+    if (P.P1 > 1)
+        res = fft_columns(Cs, reinterpret_cast<double2*>(ring), R, P.fft, SmemTwiddles{tw1}, BlockTeam{},
+                          k1_tc(R) ? static_cast<const double2*>(wsm) : nullptr);
     PFT_STAMP(4)
     // K1 is launched with programmatic stream serialization, so it may run while the previous
     // kernel of the stream (K2 of the previous transform, which may still read this
     // workspace) drains: wait for it only here, right before overwriting the slab.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (P.sum_tail) {
-        k1_sum_tail<R>(P, res, c, b, ring + (size_t)R * P.P1 * sizeof(double2));
+        k1_sum_tail<R>(P, res, c, b, ring + (size_t)R * P.P1 * sizeof(double2), tail_tw);
         return;
     }
     // Y[b][m1][c][j]: the slab for one m1 is contiguous over (c, j) for K2.
