@@ -75,6 +75,35 @@ __device__ __forceinline__ void dft8(double2 (&v)[8]) {
     v[7] = csub(e3, t3);
 }
 
+// 16-point DFT as 4 x 4: DFT-4 over n1 (stride 4) for each n2, twiddles W16^{n2 k1}, DFT-4
+// over n2; X[k1 + 4 k2] lands at v[4 k1 + k2] and is transposed back to v[k].
+__device__ __forceinline__ void dft16(double2 (&v)[16]) {
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4(v[n2], v[n2 + 4], v[n2 + 8], v[n2 + 12]);
+    const double c = 0.92387953251128675613, s = 0.38268343236508977173, h = 0.70710678118654752440;
+    // v[n2 + 4 k1] *= W16^{n2 k1}, W16^m = cos(2 pi m/16) - i sin(2 pi m/16)
+    v[5] = cmul(v[5], make_double2(c, -s));     // m = 1
+    v[9] = cmul(v[9], make_double2(h, -h));     // m = 2
+    v[13] = cmul(v[13], make_double2(s, -c));   // m = 3
+    v[6] = cmul(v[6], make_double2(h, -h));     // m = 2
+    v[10] = cmul_mi(v[10]);                     // m = 4
+    v[14] = cmul(v[14], make_double2(-h, -h));  // m = 6
+    v[7] = cmul(v[7], make_double2(s, -c));     // m = 3
+    v[11] = cmul(v[11], make_double2(-h, -h));  // m = 6
+    v[15] = cmul(v[15], make_double2(-c, s));   // m = 9
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+    // transpose the 4 x 4 block: X[k1 + 4 k2] = v[4 k1 + k2]
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = a + 1; b < 4; ++b) {
+            const double2 t = v[4 * a + b];
+            v[4 * a + b] = v[4 * b + a];
+            v[4 * b + a] = t;
+        }
+}
+
 __device__ __forceinline__ void dft3(double2& v0, double2& v1, double2& v2) {
     const double h = 0.86602540378443864676;  // sqrt(3)/2
     const double2 t = cadd(v1, v2);
@@ -108,7 +137,7 @@ struct WarpsTeam {
 // spreads them, and the second stage's contiguous reads stay conflict-free.
 __device__ __forceinline__ int fft_swz(int i) { return i ^ ((i >> 3) & 7); }
 
-// One Stockham stage with a radix known at compile time (2, 3, 4, 8).  When n is a power
+// One Stockham stage with a radix known at compile time (2, 3, 4, 8, 16).  When n is a power
 // of two (POW2) the index arithmetic uses shifts/masks (lg_nb = log2(n/R), lg_ns =
 // log2(Ns)); otherwise integer division.  sw: 1 = swizzled destination, 2 = swizzled source
 // (POW2 only).  colw: per-column factor applied to the inputs (first stage), or null.
@@ -153,6 +182,7 @@ __device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__
         if constexpr (R == 3) dft3(v[0], v[1], v[2]);
         if constexpr (R == 4) dft4(v[0], v[1], v[2], v[3]);
         if constexpr (R == 8) dft8(v);
+        if constexpr (R == 16) dft16(v);
         if (POW2 && (sw & 1)) {
 #pragma unroll
             for (int r = 0; r < R; ++r) dst[fft_swz(col * n + base + r * Ns)] = v[r];
@@ -204,7 +234,7 @@ __device__ __forceinline__ double2* fft_columns(double2* x, double2* y, int ncol
     const int lg_n = 31 - __clz(n);
     for (int st = 0; st < plan.count; ++st) {
         const int R = plan.radix[st];
-        const int lg_r = R == 2 ? 1 : R == 4 ? 2 : 3;
+        const int lg_r = R == 2 ? 1 : R == 4 ? 2 : R == 8 ? 3 : 4;
         const int lg_nb = lg_n - lg_r;
         const double2* cw = st == 0 ? colw : nullptr;
         if (pow2) {
@@ -213,7 +243,8 @@ __device__ __forceinline__ double2* fft_columns(double2* x, double2* y, int ncol
             switch (R) {
                 case 2: stockham_stage_fixed<2, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw); break;
                 case 4: stockham_stage_fixed<4, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw); break;
-                default: stockham_stage_fixed<8, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw); break;
+                case 8: stockham_stage_fixed<8, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw); break;
+                default: stockham_stage_fixed<16, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw); break;
             }
             lg_ns += lg_r;
         } else {
@@ -222,6 +253,7 @@ __device__ __forceinline__ double2* fft_columns(double2* x, double2* y, int ncol
                 case 3: stockham_stage_fixed<3, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
                 case 4: stockham_stage_fixed<4, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
                 case 8: stockham_stage_fixed<8, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
+                case 16: stockham_stage_fixed<16, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
                 default:
                     if (cw) {  // generic radix: apply the column factor in place first
                         for (int i = t0; i < ncols * n; i += nt) src[i] = cmul(src[i], cw[i / n]);

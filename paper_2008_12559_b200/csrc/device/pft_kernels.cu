@@ -318,7 +318,8 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     __syncthreads();
     double2* __restrict__ rowc = P.Y + ((size_t)b * P.P2 + c) * Q.W;
     for (uint64_t so = tid; so < Q.W; so += nt) {
-        uint32_t mp = (uint32_t)(Q.first_mod_p + (so < Q.p ? so : so % Q.p));
+        const uint64_t sr = so < Q.p ? so : (Q.W >> 32) ? so % Q.p : (uint64_t)((uint32_t)so % (uint32_t)Q.p);
+        uint32_t mp = (uint32_t)(Q.first_mod_p + sr);
         if (mp >= Q.p) mp -= (uint32_t)Q.p;
         const uint32_t m1 = p1_pow2 ? mp & (P.P1 - 1) : mp % P.P1;
         const uint32_t m2 = p1_pow2 ? mp >> lg_p1 : mp / P.P1;
@@ -342,10 +343,12 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     unsigned* ready = ctl + 2;
     double2* part = tw2 + P.P2;                           // [nw][64] reducer partials
     unsigned* s_ticket = reinterpret_cast<unsigned*>(part + (size_t)nw * 64);
-    __threadfence();
+    // the block barrier orders every thread's row stores before thread 0's gpu-scope fence and
+    // release (the cooperative-groups grid-sync pattern); one fence instead of one per thread
     __syncthreads();
     PFT_STAMP(5)
     if (tid == 0) {
+        __threadfence();
         st_release_u32(ready + c, 1u);
         *s_ticket = atomicAdd(ctl, 1u);
     }
