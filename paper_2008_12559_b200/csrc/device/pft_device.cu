@@ -88,9 +88,10 @@ bool k2_fft_feasible(uint64_t P2, int r) {
 // P2 for the sum tail: at most one K1 CTA per SM per transform, so under PDL two transforms
 // stream side by side (measured C2b p = 2^14: P2 = 128 42.5 us vs P2 = 256 46.5 us; C4
 // p = 27648: 128 21.7 us, 144 22.9 us, 256 27.7 us).  Among divisors P2 <= n_sms whose
-// P1 = p / P2 keeps two K1 CTAs per SM and fits the tail scratch: prefer P1 >= K1_BR (a
-// box's 32 rows all belong to the CTA; P1 = 16 measured 62 vs 38 us at C2a), then the
-// largest P2, taking a power of two if within 15% of it.  0 = none.
+// P1 = p / P2 keeps two K1 CTAs per SM and fits the tail scratch: prefer a power-of-two
+// P1 >= K1_BR, then P1 >= K1_BR (a box's 32 rows all belong to the CTA; P1 = 16 measured
+// 62 vs 38 us at C2a), then the largest P2, taking a power of two if within 15% of it.
+// 0 = none.
 bool sum_p1_ok(uint64_t P1, int r, uint64_t P2) {
     if (!k1_feasible(P1, r)) return false;
     if (pftdev::k1_smem_bytes(r, (uint32_t)P1, pftdev::k1_min_stages(r)) > (228 * 1024) / 2 - 1024) return false;
@@ -114,12 +115,17 @@ uint64_t choose_p2_sum(uint64_t p, int r, int n_sms, size_t batch) {
         for (uint64_t d : divisors(p))
             if (d * batch >= 2ull * (uint64_t)n_sms && sum_p1_ok(p / d, r, d)) return d;
     }
-    for (int pass = 0; pass < 2; ++pass) {  // pass 0: P1 >= K1_BR only
+    // pass 0: P1 a power of two >= K1_BR (full 32-row boxes, radix-16/8 FFT: C4 p = 11520
+    // measured 17.6 us with P1 = 128, P2 = 90 vs 20.2 us with P1 = 90, P2 = 128);
+    // pass 1: P1 >= K1_BR; pass 2: any.  Within a pass the largest P2, taking a power of two
+    // if within 15% of it.
+    for (int pass = 0; pass < 3; ++pass) {
         uint64_t any = 0, pow2 = 0;
         for (uint64_t d : divisors(p)) {
             if (d > (uint64_t)n_sms) break;
             const uint64_t P1 = p / d;
-            if (pass == 0 && P1 < (uint64_t)pftdev::K1_BR) continue;
+            if (pass < 2 && P1 < (uint64_t)pftdev::K1_BR) continue;
+            if (pass == 0 && (P1 & (P1 - 1)) != 0) continue;
             if (!sum_p1_ok(P1, r, d)) continue;
             any = d;
             if ((d & (d - 1)) == 0) pow2 = d;
