@@ -252,6 +252,31 @@ pft_status pft_sparse_tones(uint64_t seed, int n, int64_t lo, int64_t hi, int64_
 /* ------------------------------------------------------------------ device introspection */
 /* Number of kernel launches one pft_execute issues (for launch accounting). */
 pft_status pft_launches_per_execute(pft_dplan_t d, int* launches);
+
+/* ------------------------------------------------------------------ data formats and callers
+ * The formats either side of execute and the pipeline that calls it (
+ * SPEC.md cli module: SignalFile, cmd_transform output, cmd_anomaly, §4.4).      */
+#define PFT_SIGNAL_CSV 0   /* rows "re" or "re,im"                                             */
+#define PFT_SIGNAL_F64LE 1 /* header {"PFTS", u32 complex flag, u32 length} + LE doubles        */
+/* SignalFile read: *n = length (always set); values copied to out when out != NULL (cap >= n,
+ * else PFT_ERR_BUFFER_TOO_SMALL); *is_complex = channel flag.  Parse errors: PFT_ERR_IO.    */
+pft_status pft_signal_read(const char* path, int fmt, pft_c128* out, uint64_t cap, uint64_t* n, int* is_complex);
+pft_status pft_signal_write(const char* path, int fmt, const pft_c128* v, uint64_t n, int is_complex);
+/* cmd_transform output: CSV "m,re,im", m = mu - M .. mu + M, 17 significant digits (re-parsing
+ * is bit-exact, SPEC.md cli "File round-trip").                                             */
+pft_status pft_spectrum_write_csv(const char* path, int64_t mu, uint64_t M, const pft_c128* values);
+pft_status pft_spectrum_read_csv(const char* path, int64_t* first_m, pft_c128* out, uint64_t cap, uint64_t* n);
+/* cmd_anomaly core: fitted curve from coeffs[s] = a_{s-M} on R_{0,M} (conjugate symmetry of
+ * real x), scores |x_n - fit_n|, top k by descending score, ties by ascending index.  fitted
+ * (N doubles) may be NULL.                                                                  */
+pft_status pft_anomaly_from_coeffs(const double* x, uint64_t N, const pft_c128* coeffs, uint64_t M, uint64_t k,
+                                   uint64_t* idx, double* score, double* fitted);
+/* cmd_anomaly with source = pft: the coefficients from one execute of a device plan built for
+ * (N, M, mu = 0) on the real series x (host memory, N doubles), then the scoring above.      */
+pft_status pft_anomaly(pft_dplan_t d, const double* x, uint64_t k, uint64_t* idx, double* score, double* fitted);
+/* (N, M, mu) of a device plan. */
+pft_status pft_dplan_shape(pft_dplan_t d, uint64_t* N, uint64_t* M, int64_t* mu);
+
 pft_status pft_device_count(int* n);
 
 #ifdef __cplusplus

@@ -670,3 +670,79 @@ def generate_signal_device(d_out: int, kind: int, seed: int, count: int, N: int 
     d, keep = _desc(kind, seed, N, offset, freqs, amps, sigma)
     _check(lib().pft_generate_device(C.byref(d), C.c_void_p(d_out), count, C.c_void_p(stream or None)))
     del keep
+
+
+# ----------------------------------------------------------------------------- data formats
+
+SIGNAL_CSV, SIGNAL_F64LE = 0, 1
+
+
+def _signal_format(path: str, fmt: Optional[int]) -> int:
+    if fmt is not None:
+        return int(fmt)
+    return SIGNAL_CSV if str(path).lower().endswith(".csv") else SIGNAL_F64LE
+
+
+def read_signal(path, fmt: Optional[int] = None) -> tuple[np.ndarray, bool]:
+    """SignalFile read (SPEC.md cli "SignalFile"): csv rows "re" / "re,im", or f64le with the
+    16-byte {"PFTS", u32 complex flag, u32 length} header.  Returns (complex128 values,
+    is_complex).  Format from the extension (.csv) unless given."""
+    f = _signal_format(path, fmt)
+    n, cx = C.c_uint64(), C.c_int()
+    _check(lib().pft_signal_read(str(path).encode(), f, None, 0, C.byref(n), C.byref(cx)))
+    out = np.zeros(n.value, dtype=np.complex128)
+    _check(lib().pft_signal_read(str(path).encode(), f, _ptr(out), out.size, C.byref(n), C.byref(cx)))
+    return out, bool(cx.value)
+
+
+def write_signal(path, values, fmt: Optional[int] = None, is_complex: Optional[bool] = None) -> None:
+    v = np.ascontiguousarray(np.asarray(values, dtype=np.complex128))
+    if is_complex is None:
+        is_complex = bool(np.iscomplexobj(values))
+    _check(lib().pft_signal_write(str(path).encode(), _signal_format(path, fmt), _ptr(v), v.size, int(is_complex)))
+
+
+def write_spectrum_csv(path, spectrum: "PartialSpectrum") -> None:
+    """cmd_transform output: CSV "m,re,im" over [mu - M, mu + M], bit-exact on re-read."""
+    v = np.ascontiguousarray(spectrum.values, dtype=np.complex128)
+    _check(lib().pft_spectrum_write_csv(str(path).encode(), int(spectrum.range.mu), int(spectrum.range.half_width),
+                                        _ptr(v)))
+
+
+def read_spectrum_csv(path) -> tuple[int, np.ndarray]:
+    """(first m, values) of a "m,re,im" file."""
+    n, m0 = C.c_uint64(), C.c_int64()
+    _check(lib().pft_spectrum_read_csv(str(path).encode(), C.byref(m0), None, 0, C.byref(n)))
+    out = np.zeros(n.value, dtype=np.complex128)
+    _check(lib().pft_spectrum_read_csv(str(path).encode(), C.byref(m0), _ptr(out), out.size, C.byref(n)))
+    return m0.value, out
+
+
+# ----------------------------------------------------------------------------- anomaly pipeline
+
+def anomaly_from_coeffs(x, coeffs, M: int, k: int) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """cmd_anomaly scoring (SPEC.md cli; PAPER.md §4.4) from coefficients on R_{0,M}
+    (coeffs[s] = a_{s-M}): (top-k indices, their scores, fitted curve)."""
+    xv = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    cv = np.ascontiguousarray(np.asarray(coeffs, dtype=np.complex128))
+    if cv.size != 2 * M + 1:
+        raise PftValueError(6, f"coeffs length {cv.size} != 2M+1 = {2 * M + 1}")
+    idx = np.zeros(k, dtype=np.uint64)
+    sc = np.zeros(k, dtype=np.float64)
+    fit = np.zeros(xv.size, dtype=np.float64)
+    _check(lib().pft_anomaly_from_coeffs(_ptr(xv), xv.size, _ptr(cv), M, k, _ptr(idx), _ptr(sc), _ptr(fit)))
+    return idx.astype(np.int64), sc, fit
+
+
+def anomaly(x, M: int, k: int, p: Optional[int] = None, epsilon: float = DEFAULT_EPSILON,
+            device: int = 0) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """cmd_anomaly with source = pft: coefficients on R_{0,M} from one GPU execute, then the
+    scoring of anomaly_from_coeffs (inside the library: pft_anomaly)."""
+    xv = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    plan = build_plan(xv.size, M, 0, p, epsilon)
+    d = DevicePlan(plan, device=device)
+    idx = np.zeros(k, dtype=np.uint64)
+    sc = np.zeros(k, dtype=np.float64)
+    fit = np.zeros(xv.size, dtype=np.float64)
+    _check(lib().pft_anomaly(d._h, _ptr(xv), k, _ptr(idx), _ptr(sc), _ptr(fit)))
+    return idx.astype(np.int64), sc, fit

@@ -103,6 +103,13 @@ SIGNATURES: dict[str, tuple] = {
     "pft_sparse_tones": (ST, [U64, I, I64, I64, P, P]),
     "pft_launches_per_execute": (ST, [P, C.POINTER(I)]),
     "pft_device_count": (ST, [C.POINTER(I)]),
+    "pft_signal_read": (ST, [C.c_char_p, I, P, U64, C.POINTER(U64), C.POINTER(I)]),
+    "pft_signal_write": (ST, [C.c_char_p, I, P, U64, I]),
+    "pft_spectrum_write_csv": (ST, [C.c_char_p, I64, U64, P]),
+    "pft_spectrum_read_csv": (ST, [C.c_char_p, C.POINTER(I64), P, U64, C.POINTER(U64)]),
+    "pft_anomaly_from_coeffs": (ST, [P, U64, P, U64, U64, P, P, P]),
+    "pft_anomaly": (ST, [P, P, U64, P, P, P]),
+    "pft_dplan_shape": (ST, [P, C.POINTER(U64), C.POINTER(U64), C.POINTER(I64)]),
 }
 
 STATUS_NAMES = {

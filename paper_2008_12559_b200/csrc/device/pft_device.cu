@@ -686,6 +686,15 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
 
 void pft_dplan_destroy(pft_dplan_t d) { delete d; }
 
+pft_status pft_dplan_shape(pft_dplan_t d, uint64_t* N, uint64_t* M, int64_t* mu) {
+    PFT_API_BEGIN
+    const pft_dplan_s* x = dp(d);
+    if (N) *N = x->host.N;
+    if (M) *M = x->host.M;
+    if (mu) *mu = x->host.mu;
+    PFT_API_END
+}
+
 pft_status pft_dplan_layout(pft_dplan_t d, uint64_t* p1, uint64_t* p2) {
     PFT_API_BEGIN
     if (p1) *p1 = dp(d)->P1;
