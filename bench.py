@@ -245,7 +245,8 @@ def run_ours(args):
         p_src = "config"
     plan = pft.build_plan(N, M, mu, p, EPS)
     d = pft.DevicePlan(plan, device=local, p2=args.p2, pdl=not args.no_pdl, fuse=args.fuse, batch_hint=B,
-                       k2_mode=args.k2_mode)
+                       k2_mode=args.k2_mode, k2_tail={"auto": 0, "on": 1, "off": -1}[args.k2_tail],
+                       reducers=args.reducers, k2_ctas=args.k2_ctas)
     launches = d.launches_per_execute()
 
     stream = torch.cuda.Stream(device=dev)
@@ -404,8 +405,10 @@ def run_ours(args):
                               f"{nbuf} rotating inputs of {16 * N / 2**20:.0f} MiB (> L2 126 MiB)"),
                        "timing": "CUDA graph of K steps, CUDA events on the launch stream",
                        "streams": args.streams, "pdl": not args.no_pdl, "fused_k2": args.fuse,
-                       "tail": "sum tail in K1 (one kernel per execute)" if launches == 1 else
-                               f"K2 ({launches} kernels per execute)",
+                       "tail": {"sum tail": "sum tail in K1 (one kernel per execute)",
+                                "K2 tail": "K2 work by K1's last-arriving CTAs (one kernel per execute)",
+                                "fused K2": "K2 in K1 behind a grid barrier (one kernel per execute)"}.get(
+                                    d.tail_kind(), f"K2 ({launches} kernels per execute)"),
                        "pipelining": "independent transforms alternate over 2 streams with separate "
                                      "workspaces" if args.streams == 2 else
                                      "single stream; execute i+1's K1 starts streaming while execute "
@@ -532,6 +535,10 @@ def main():
                     help="c5: run the contraction-axis sharded path even on one GPU (checks it)")
     ap.add_argument("--no-pdl", action="store_true", help="plain stream order between kernels")
     ap.add_argument("--fuse", action="store_true", help="fuse K2 into K1's tail (grid barrier)")
+    ap.add_argument("--k2-tail", default="auto", choices=["auto", "on", "off"],
+                    help="K2's work by K1's last-arriving CTAs instead of a K2 grid (many output bins)")
+    ap.add_argument("--k2-ctas", type=int, default=0, help="K2 grid width (L2 form)")
+    ap.add_argument("--reducers", type=int, default=0, help="sum tail / K2 tail working CTAs per signal (0 = plan)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

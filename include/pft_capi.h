@@ -252,6 +252,10 @@ pft_status pft_sparse_tones(uint64_t seed, int n, int64_t lo, int64_t hi, int64_
 /* ------------------------------------------------------------------ device introspection */
 /* Number of kernel launches one pft_execute issues (for launch accounting). */
 pft_status pft_launches_per_execute(pft_dplan_t d, int* launches);
+/* How an unsharded execute finishes after the contraction + first FFT pass (K1):
+ * 0 separate K2 grid, 1 sum tail in K1 (few bins), 2 K2 work by K1's last arrivals (many
+ * bins), 3 K2 in K1 behind a grid barrier (opt-in). */
+pft_status pft_dplan_tail_kind(pft_dplan_t d, int* kind);
 
 /* ------------------------------------------------------------------ data formats and callers
  * The formats either side of execute and the pipeline that calls it (

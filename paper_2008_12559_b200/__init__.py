@@ -515,7 +515,8 @@ class DevicePlan:
     pointers (e.g. torch.Tensor.data_ptr() of complex128 CUDA tensors)."""
 
     def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0, k1_stages: int = 0, k2_mode: int = 0,
-                 k2_ctas: int = 0, pdl: bool = True, fuse: bool = False, reducers: int = 0, batch_hint: int = 1):
+                 k2_ctas: int = 0, pdl: bool = True, fuse: bool = False, reducers: int = 0, batch_hint: int = 1,
+                 k2_tail: int = 0):
         self.plan = plan
         opts = _capi.DPlanOpts()
         opts.device = device
@@ -524,8 +525,10 @@ class DevicePlan:
         opts.reserved[0] = k2_mode  # 0 auto, 1 fft, 2 dot, 3 direct, 4 l2, 5 sum tail (A/B testing)
         opts.reserved[1] = k2_ctas  # K2 grid width for the L2 form (0 = default)
         opts.reserved[2] = 0 if pdl else 1  # PDL chaining of consecutive transforms
-        opts.reserved[3] = 2 if fuse else 0  # K2 fused into K1's tail (grid barrier, opt-in)
-        opts.reserved[4] = reducers  # sum tail: reducing CTAs per signal (0 = one per 64 outputs)
+        # K2 fused into K1's tail (grid barrier, opt-in); else K2 tail by last arrivals: auto (0),
+        # forced on (k2_tail > 0), off (k2_tail < 0)
+        opts.reserved[3] = 2 if fuse else (3 if k2_tail > 0 else 4 if k2_tail < 0 else 0)
+        opts.reserved[4] = reducers  # sum tail / K2 tail: working CTAs per signal (0 = default)
         opts.batch_hint = batch_hint
         h = C.c_void_p()
         _check(lib().pft_dplan_create(plan.handle, C.byref(opts), C.byref(h)))
@@ -559,6 +562,15 @@ class DevicePlan:
         n = C.c_int()
         _check(lib().pft_launches_per_execute(self._h, C.byref(n)))
         return n.value
+
+    TAIL_KINDS = ("K2 grid", "sum tail", "K2 tail", "fused K2")
+
+    def tail_kind(self) -> str:
+        """How execute finishes after K1: "K2 grid", "sum tail", "K2 tail" (K2's work by K1's
+        last arrivals) or "fused K2" (grid barrier, opt-in)."""
+        n = C.c_int()
+        _check(lib().pft_dplan_tail_kind(self._h, C.byref(n)))
+        return self.TAIL_KINDS[n.value]
 
     def execute_ptr(self, d_in: int, d_out: int, batch: int = 1, in_stride: int = 0, d_ws: int = 0,
                     stream: int = 0) -> None:

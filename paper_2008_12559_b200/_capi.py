@@ -102,6 +102,7 @@ SIGNATURES: dict[str, tuple] = {
     "pft_generate_device": (ST, [C.POINTER(SignalDesc), P, U64, P]),
     "pft_sparse_tones": (ST, [U64, I, I64, I64, P, P]),
     "pft_launches_per_execute": (ST, [P, C.POINTER(I)]),
+    "pft_dplan_tail_kind": (ST, [P, C.POINTER(I)]),
     "pft_device_count": (ST, [C.POINTER(I)]),
     "pft_signal_read": (ST, [C.c_char_p, I, P, U64, C.POINTER(U64), C.POINTER(I)]),
     "pft_signal_write": (ST, [C.c_char_p, I, P, U64, I]),

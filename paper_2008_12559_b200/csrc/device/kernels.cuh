@@ -136,6 +136,9 @@ struct K1Params {
     uint32_t reducers;          // sum tail: the last `reducers` CTAs of a signal reduce its rows
     unsigned* arrivals;         // sum tail: per signal {tickets, done, ready[P2]} (zeroed once)
     uint32_t tl_seq;            // launch sequence number (PFT_TIMELINE instrumentation only)
+    int k2_tail;                // K2 work done by the last `reducers` CTAs of a signal to write
+                                // their slab (last-arrival, no grid-wide wait; see k1_k2_tail)
+    uint32_t k2_group;          // k2_tail: columns j per FFT group (the group's Z + scratch fit the ring)
     int fused;                  // run K2 in K1's tail behind a grid barrier (cooperative launch)
     unsigned* bar;              // grid-barrier state {count, generation} (workspace tail, zeroed once)
     K2Params k2;                // K2 parameters for the fused tail
@@ -184,6 +187,11 @@ inline size_t ctrl_bytes(size_t batch, size_t per_signal) {
 // reducer partials, ticket
 inline size_t k1_sum_scratch_bytes(uint32_t P1, uint32_t P2) {
     return 16 * ((size_t)P1 + P2) + (size_t)K1_THREADS / 32 * 64 * 16 + 16;
+}
+// K1's last-arrival K2 tail: Z + scratch for `group` columns, omega_P2 + four-step twiddles,
+// ticket word
+inline size_t k1_k2_tail_bytes(uint32_t group, uint32_t P2) {
+    return sizeof(double2) * (2 * (size_t)group * P2 + 2 * (size_t)P2) + 16;
 }
 cudaError_t configure_k2(int r, uint32_t P2);
 cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t batch, bool mu0, cudaStream_t st);

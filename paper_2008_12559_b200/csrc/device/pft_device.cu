@@ -138,6 +138,9 @@ uint64_t choose_p2_sum(uint64_t p, int r, int n_sms, size_t batch) {
 // Choose P2 | p (K1 grid = P2 x batch CTAs; P1 = p / P2 is K1's in-CTA FFT length, P2 is
 // K2's).  Prefer decompositions where both FFT passes fit shared memory, then the
 // smallest P2 that still gives >= kTargetCtas CTAs (fewer residue classes = less K2 work).
+// development knob reserved[3]: 2 grid-barrier fusion, 3 K2 tail on, 4 K2 tail off
+int opts_k2_tail(const pft_dplan_opts* o) { return o ? o->reserved[3] : 0; }
+
 uint64_t choose_p2(uint64_t p, int r, size_t batch) {
     const auto divs = divisors(p);
     const size_t nb = std::max<size_t>(batch, 1);
@@ -238,6 +241,8 @@ struct pft_dplan_s {
     bool pdl_chain = true;  // K2 releases the next K1 early (programmatic dependent launch)
     bool allow_fuse = false; // K2 fused into K1's tail (opt-in; measured slower at C2b/C4)
     bool sum_tail = false;   // unsharded execute: K1 sum tail, no K2 (few output bins)
+    bool k2_tail = false;    // unsharded execute: K2's work by K1's last arrivals (many bins)
+    uint32_t k2_group = 0;   // k2_tail: columns j per FFT group
     uint32_t reducers = 0;   // sum tail: CTAs per signal that reduce the residue rows
     uint64_t k1_capacity = 0;  // co-resident K1 CTAs on the device
     bool mu0 = false;
@@ -267,7 +272,7 @@ struct pft_dplan_s {
     }
 
     size_t slab_elems() const { return (size_t)host.p * host.r; }
-    size_t counters_per_signal() const { return sum_tail ? P2 + 2 : 0; }
+    size_t counters_per_signal() const { return sum_tail ? P2 + 2 : k2_tail ? 2 : 0; }
     size_t data_elems() const { return sum_tail ? std::max<size_t>(slab_elems(), (size_t)P2 * W) : slab_elems(); }
     size_t workspace_bytes(size_t batch) const {
         return data_elems() * sizeof(double2) * batch + pftdev::ctrl_bytes(batch, counters_per_signal());
@@ -402,6 +407,16 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
                                                   pftdev::kBarrierBytes);
         P1.k2 = P2;
         cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
+        return;
+    }
+    if (d->k2_tail) {
+        P1.k2_tail = 1;
+        P1.k2_group = d->k2_group;
+        P1.reducers = d->reducers;
+        P1.arrivals = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(Y + d->data_elems() * batch) +
+                                                  pftdev::kBarrierBytes);
+        P1.k2 = P2;
+        cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 (K2 tail) launch");
         return;
     }
     if (d->fused(batch)) {
@@ -602,6 +617,32 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         // reducers hold more SM slots from the next transform), opts override
         d->reducers = (uint32_t)std::min<uint64_t>(d->P2, std::max<uint64_t>(1, (d->W + 63) / 64));
         if (opts && opts->reserved[4] > 0) d->reducers = (uint32_t)std::min<uint64_t>(d->P2, opts->reserved[4]);
+        // Last-arrival K2 tail (k1_k2_tail) when K2 takes the FFT form and the tail is short
+        // against the stream: the columns go through the FFT in groups whose Z + scratch fit
+        // the ring.  Workers hold their SM slots, and a K1 CTA of the next transform that starts
+        // late finishes late (each CTA streams a fixed 1/P2 of the input), so the tail's m1
+        // rounds (~15 us each beside a streaming CTA, PFT_TIMELINE at C2c) must stay <= 10% of
+        // the stream: C5 (2^30) gains 6% (3099 -> 2907 us), C2c (2^24, 2 rounds) loses (67 -> 77
+        // us at 1 round).  reserved[3]: 3 forces it on (if feasible), 4 off (separate K2 grid).
+        const int want_tail = opts_k2_tail(opts);
+        if (!d->sum_tail && d->k2_mode == pftdev::K2_FFT && !d->allow_fuse && want_tail != 4) {
+            const size_t ring = (size_t)d->k1_stages * pftdev::k1_stage_bytes(H.r);
+            const size_t fixed = pftdev::k1_k2_tail_bytes(0, (uint32_t)d->P2);
+            const size_t per_col = 2 * sizeof(double2) * d->P2;
+            const uint64_t gmax = ring > fixed ? (ring - fixed) / per_col : 0;
+            if (gmax >= 1) {
+                const uint64_t groups = ((uint64_t)H.r + gmax - 1) / gmax;
+                d->k2_group = (uint32_t)(((uint64_t)H.r + groups - 1) / groups);
+                d->k2_tail = true;
+                // workers per signal: all m1 in one round when P1 is small, else 64 (opts override)
+                d->reducers = (uint32_t)std::min<uint64_t>(d->P1, std::min<uint64_t>(d->P2, 64));
+                if (opts && opts->reserved[4] > 0)
+                    d->reducers = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(d->P1, d->P2), opts->reserved[4]);
+                const double rounds = (double)((d->P1 + d->reducers - 1) / d->reducers);
+                const double stream_us = 16.0 * (double)H.N * (double)batch_hint / 6.5e6;
+                if (want_tail != 3 && rounds * 15.0 > 0.10 * stream_us) d->k2_tail = false;
+            }
+        }
     }
     d->mu0 = std::all_of(H.phase.begin(), H.phase.end(), [](const cplx& z) { return z == cplx(1.0, 0.0); });
 
@@ -720,7 +761,15 @@ pft_status pft_launches_per_execute(pft_dplan_t d, int* launches) {
     PFT_API_BEGIN
     dp(d);
     PFT_REQUIRE(launches != nullptr, "launches is null");
-    *launches = (dp(d)->fused(1) || dp(d)->sum_tail) ? 1 : 2;
+    *launches = (dp(d)->fused(1) || dp(d)->sum_tail || dp(d)->k2_tail) ? 1 : 2;
+    PFT_API_END
+}
+
+pft_status pft_dplan_tail_kind(pft_dplan_t d, int* kind) {
+    PFT_API_BEGIN
+    const pft_dplan_s* x = dp(d);
+    PFT_REQUIRE(kind != nullptr, "kind is null");
+    *kind = x->sum_tail ? 1 : x->k2_tail ? 2 : x->fused(1) ? 3 : 0;
     PFT_API_END
 }
 

@@ -48,9 +48,13 @@ __device__ unsigned long long g_pft_timeline2[4][4096][6];
 #define PFT_STAMP2(slot) \
     if (threadIdx.x == 0 && blockIdx.x + blockIdx.y * gridDim.x < 4096) \
         g_pft_timeline2[P.tl_seq & 3][blockIdx.x + blockIdx.y * gridDim.x][slot] = gtimer();
+// K2-tail worker k of signal 0 (k1_k2_tail)
+#define PFT_STAMPW(k, slot) \
+    if (threadIdx.x == 0 && blockIdx.y == 0 && (k) < 4096) g_pft_timeline2[P.tl_seq & 3][(k)][slot] = gtimer();
 #else
 #define PFT_STAMP(slot)
 #define PFT_STAMP2(slot)
+#define PFT_STAMPW(k, slot)
 #endif
 
 // Grid-wide barrier for K1's fused K2 tail (all CTAs are co-resident: cooperative launch).
@@ -414,6 +418,131 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     }
 }
 
+// Last-arrival K2 tail (many output bins, e.g. C2c): K2's work -- the length-P2 pass for one
+// m1 pruned to the bins Eq. (7) reads, fused with the post-process -- is done inside K1 by the
+// last `reducers` CTAs of signal b to write their slab, not by a separate K2 grid that waits
+// for all of K1 (and whose 123 KB CTAs cannot sit beside the next transform's K1 CTAs).  Each
+// CTA publishes its slab and takes a ticket; the last L arrivals wait for the ticket count to
+// reach P2 (they are the stragglers, so this wait is short), then worker k handles m1 = k,
+// k + L, ...  The columns j go through the FFT in groups of `k2_group` so Z + scratch fit the
+// idle ring beside two K1 CTAs per SM; a bin's partial sum over j is kept in `out` between
+// groups (same thread, same ascending-j fma chain as k2_fft_block: results are bitwise those
+// of the standalone K2).  Under PDL the next transform's K1 streams on the other slots.
+template <int R>
+__device__ __forceinline__ void k1_k2_tail(const K1Params& P, uint32_t c, uint32_t b, double2* zs) {
+    const K2Params& Q = P.k2;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const uint32_t G = P.k2_group;
+    double2* Z = zs;                              // [G][P2]
+    double2* scratch = zs + (size_t)G * P.P2;     // [G][P2]
+    double2* tw2 = scratch + (size_t)G * P.P2;    // omega_P2^t
+    double2* pre = tw2 + P.P2;                    // omega_p^{m1 c}
+    unsigned* s_t = reinterpret_cast<unsigned*>(pre + P.P2);
+    unsigned* ctl = P.arrivals + (size_t)b * 2;   // {tickets, done}
+    __syncthreads();  // the CTA's slab stores precede thread 0's fence and ticket
+    if (tid == 0) {
+        __threadfence();
+        *s_t = atomicAdd(ctl, 1u);
+    }
+    __syncthreads();
+    const uint32_t t = *s_t, L = P.reducers;
+    if (t + L < P.P2) return;
+    const uint32_t k = t + L - P.P2;
+    PFT_STAMPW(k, 0)
+    double2* __restrict__ out = Q.out + (size_t)b * Q.W;
+    // Per m1, a thread's first bin s = s0 + P1 tid takes its r post powers and post twiddle from
+    // registers loaded before the slab (these tables come from DRAM: the next transform's
+    // stream has evicted them; a dependent load per j serialised ~r DRAM latencies).  The
+    // first m1's tables load before the wait for the stragglers.
+    double pw0[R];
+    double2 ptw0 = make_double2(0.0, 0.0);
+    auto prefetch = [&](uint32_t m1) {
+        const uint64_t s0 = (uint64_t)((m1 + P.P1 - Q.first_mod_p1) % P.P1);
+        for (uint32_t c2 = tid; c2 < P.P2; c2 += nt) pre[c2] = __ldg(P.omega + (size_t)m1 * c2);  // m1 c < p
+        const uint64_t sf = s0 + (uint64_t)P.P1 * tid;
+        if (sf < Q.W) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) pw0[j] = __ldg(Q.post_powers + sf * R + j);
+            ptw0 = __ldg(Q.post_twiddles + sf);
+        }
+    };
+    for (uint32_t c2 = tid; c2 < P.P2; c2 += nt) tw2[c2] = __ldg(P.omega + (size_t)c2 * P.P1);  // omega_P2^c
+    if (k < P.P1) prefetch(k);
+    if (tid == 0) {
+        while (ld_acquire_u32(ctl) < P.P2) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
+    PFT_STAMPW(k, 1)
+    for (uint32_t m1 = k; m1 < P.P1; m1 += L) {
+        const uint64_t s0 = (uint64_t)((m1 + P.P1 - Q.first_mod_p1) % P.P1);
+        if (s0 >= Q.W) continue;  // no output slot maps to this m1 (block-uniform)
+        if (m1 != k) {
+            prefetch(m1);
+            __syncthreads();
+        }
+        const double2* __restrict__ Ym = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
+        for (uint32_t j0 = 0; j0 < (uint32_t)R; j0 += G) {
+            const uint32_t g = min(G, (uint32_t)R - j0), n = P.P2 * g;
+            // Z[jj][c] = omega_p^{m1 c} Y[c][j0 + jj]; all of a thread's L2 loads in flight first
+            constexpr int U = 8;
+            for (uint32_t base = tid; base < n; base += U * nt) {
+                double2 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t idx = base + u * nt;
+                    const uint32_t cc = idx / g, jj = idx - cc * g;
+                    v[u] = idx < n ? __ldcg(Ym + (size_t)cc * R + j0 + jj) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t idx = base + u * nt;
+                    if (idx < n) {
+                        const uint32_t cc = idx / g, jj = idx - cc * g;
+                        Z[(size_t)jj * P.P2 + cc] = (m1 == 0 || cc == 0) ? v[u] : cmul(v[u], pre[cc]);
+                    }
+                }
+            }
+            __syncthreads();
+            if (m1 == k && j0 == 0) { PFT_STAMPW(k, 2) }
+            const double2* res = Z;
+            if (P.P2 > 1) res = fft_columns(Z, scratch, (int)g, Q.fft2, SmemTwiddles{tw2});
+            if (m1 == k && j0 == 0) { PFT_STAMPW(k, 3) }
+            const bool last = j0 + g == (uint32_t)R;
+            const uint64_t sf = s0 + (uint64_t)P.P1 * tid;
+            for (uint64_t s = sf; s < Q.W; s += (uint64_t)P.P1 * nt) {
+                uint64_t mp = Q.first_mod_p + s % Q.p;
+                if (mp >= Q.p) mp -= Q.p;
+                const uint32_t m2 = (uint32_t)(mp / P.P1);
+                const bool first = s == sf;
+                double2 acc = j0 == 0 ? make_double2(0.0, 0.0) : out[s];  // this thread's partial
+#pragma unroll
+                for (int j = 0; j < R; ++j) {  // ascending j, this group's columns
+                    if ((uint32_t)j < j0 || (uint32_t)j >= j0 + g) continue;
+                    const double pw = first ? pw0[j] : __ldg(Q.post_powers + s * R + j);
+                    const double2 v = res[(size_t)(j - j0) * P.P2 + m2];
+                    acc.x = fma(v.x, pw, acc.x);
+                    acc.y = fma(v.y, pw, acc.y);
+                }
+                if (last) {
+                    acc = cmul(acc, first ? ptw0 : __ldg(Q.post_twiddles + s));  // e^{-pi i m / p}
+                    if (!isfinite(acc.x) || !isfinite(acc.y)) atomicOr(Q.status, 1);
+                }
+                out[s] = acc;
+            }
+            __syncthreads();  // Z / scratch reuse by the next group or m1
+        }
+        if (m1 == k) { PFT_STAMPW(k, 4) }
+    }
+    PFT_STAMPW(k, 5)
+    // the last worker to finish re-arms the signal's counters
+    if (tid == 0 && atomicAdd(ctl + 1, 1u) == L - 1) {
+        ctl[0] = 0;
+        ctl[1] = 0;
+        __threadfence();
+    }
+}
+
 template <int R, bool MU0>
 __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_constant__ CUtensorMap tmap,
                                                                   const K1Params P) {
@@ -616,6 +745,10 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         Y[((size_t)m1 * P.P2 + c) * R + j] = res[(size_t)j * P.P1 + m1];
     }
     PFT_STAMP(5)
+    if (P.k2_tail) {
+        k1_k2_tail<R>(P, c, b, reinterpret_cast<double2*>(ring));
+        return;
+    }
     if (P.fused) {
         // Fused K2: once every residue's slab is in L2, CTA (c, b) finishes bins m1 = c,
         // c + P2, ... of signal b; the other CTAs exit and free their SM slots for the next
@@ -1092,7 +1225,7 @@ cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t
 
 cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st) {
     const uint32_t gx = P.mode == K2_L2 ? (P.k2_ctas ? P.k2_ctas : 148u)
-                                           : P.P1;
+                                         : P.P1;
     const dim3 grid(gx, batch);
     switch (r) {
 #define X(n) case n: return launch_k2_r<n>(P, grid, st);

@@ -156,7 +156,7 @@ def test_sharded_partials_sum_to_unsharded(pft, oracle, N, M, mu, p, world):
     assert rel_l2(out.cpu().numpy(), ref) <= GATE
 
 
-@pytest.mark.parametrize("form", ["fused", "k2", "sum", "sum-all-reduce"])
+@pytest.mark.parametrize("form", ["fused", "k2", "k2-tail", "k2-tail-1", "sum", "sum-all-reduce"])
 def test_batched_workspace_and_tail_forms(pft, oracle, form):
     """Batched execute through a caller workspace (zeroed once, reused) with each tail form:
     K2 fused into K1's tail (grid barrier), a separate K2, or the K1 sum tail (no K2; the last
@@ -165,8 +165,9 @@ def test_batched_workspace_and_tail_forms(pft, oracle, form):
     import torch
     N, M, mu, batch = 2 ** 16, 128, 77, 3
     plan = pft.build_plan(N, M, mu, None, 1e-12)
-    kw = {"fused": dict(fuse=True, k2_mode=1), "k2": dict(k2_mode=1), "sum": dict(k2_mode=5),
-          "sum-all-reduce": dict(k2_mode=5, reducers=1 << 20)}[form]
+    kw = {"fused": dict(fuse=True, k2_mode=1), "k2": dict(k2_mode=1, k2_tail=-1),
+          "k2-tail": dict(k2_mode=1, k2_tail=1), "k2-tail-1": dict(k2_mode=1, k2_tail=1, reducers=1),
+          "sum": dict(k2_mode=5), "sum-all-reduce": dict(k2_mode=5, reducers=1 << 20)}[form]
     d = pft.DevicePlan(plan, **kw)
     assert d.launches_per_execute() == (2 if form == "k2" else 1)
     fuse = form
@@ -242,7 +243,7 @@ def test_sum_tail_and_k2_forms_agree(pft, oracle, N, M, mu, p):
     ref = oracle.execute(plan, a)
     res = []
     for mode, launches in ((5, 1), (1, 2)):
-        d = pft.DevicePlan(plan, k2_mode=mode)
+        d = pft.DevicePlan(plan, k2_mode=mode, k2_tail=-1)
         assert d.launches_per_execute() == launches
         out = torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda")
         d.execute_ptr(x.data_ptr(), out.data_ptr())
@@ -267,6 +268,33 @@ def test_every_second_pass_form(pft, oracle, mode):
         d.execute_ptr(x.data_ptr(), out.data_ptr())
     torch.cuda.synchronize()
     assert rel_l2(out.cpu().numpy(), oracle.execute(plan, a)) <= GATE
+
+
+@pytest.mark.parametrize("N,M,mu,p,reducers", [
+    (2 ** 20, 2 ** 12, 2 ** 18, 2 ** 12, 0),        # W = 8193 > p: wrapped bins
+    (2 ** 22, 2 ** 12, -5, 2 ** 13, 3),             # few workers, several m1 each
+    (6220800, 4000, -12345, 15360, 0),              # non-power-of-two P1 / P2
+    (2 ** 24, 2 ** 14, 2 ** 22, 2 ** 15, 0),        # C2c at the autotuned p: r = 14, two j groups
+])
+def test_k2_tail_matches_k2_grid(pft, oracle, N, M, mu, p, reducers):
+    """K2's work done by K1's last-arriving CTAs (one kernel, j in groups that fit K1's ring)
+    is bitwise the separate K2 grid's result (same FFT per column, same ascending-j fma chain),
+    and both pass the oracle gate."""
+    import torch
+    plan = pft.build_plan(N, M, mu, p, 1e-12)
+    a = pft.generate_signal(pft.KIND_UNIFORM, 41, N)
+    x = torch.from_numpy(a).cuda()
+    res = []
+    for tail, kind in ((1, "K2 tail"), (-1, "K2 grid")):
+        d = pft.DevicePlan(plan, k2_mode=1, k2_tail=tail, reducers=reducers)
+        assert d.tail_kind() == kind
+        out = torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda")
+        for _ in range(3):  # counters re-arm between executes
+            d.execute_ptr(x.data_ptr(), out.data_ptr())
+        torch.cuda.synchronize()
+        res.append(out.cpu().numpy())
+    assert np.array_equal(res[0], res[1])
+    assert rel_l2(res[0], oracle.execute(plan, a)) <= GATE
 
 
 EDGE = [
