@@ -21,7 +21,7 @@ from ._capi import c128
 __all__ = [
     "PftError", "ApproxPoly", "ScopeTable", "CostEstimate", "TargetRange", "PartialSpectrum", "PftPlan",
     "DevicePlan", "best_approx", "scope_xi", "translate_poly", "divisors", "min_terms", "select_divisor", "select_divisor_device", "autotune_divisor",
-    "Pft2dPlan", "PartialSpectrum2d", "build_plan_2d", "execute_2d", "parenthesization",
+    "Pft2dPlan", "PartialSpectrum2d", "build_plan_2d", "execute_2d", "parenthesization", "autotune_2d",
     "build_plan", "execute", "mod_index", "l1_norm", "generate_signal", "sparse_tones", "shard_layout",
     "shard_gather",
     "device_count", "lib",
@@ -383,6 +383,23 @@ def build_plan_2d(N1: int, N2: int, M1: int, M2: int, mu1: int, mu2: int, p1: Op
         if 2 * M > N:
             raise PftValueError(1, "build_plan_2d: M_d > N_d / 2")
     return Pft2dPlan(build_plan(N1, M1, mu1, p1, epsilon, table), build_plan(N2, M2, mu2, p2, epsilon, table))
+
+
+def autotune_2d(plan: Pft2dPlan, d_in: int, device: int = 0, candidates: int = 8) -> Pft2dPlan:
+    """Device-measured p per axis (SURVEY.md §8(f) row 1 applied to Algorithm 3).  SPEC's CPU
+    cost model picks each p_d for one length-N_d signal; on the GPU the axis-2 pass runs N1
+    short signals as one batch and the axis-1 pass 2M2+1 of them, where the per-signal FFT and
+    tail costs decide (tools/probe_2d.py: 4096 x 4096, M = 64: rows p = 64 208 us vs SPEC's 128
+    232 us, columns p = 256 33 us vs 80 us).  Each axis is timed with pft_autotune_divisor at
+    its batch: the rows over the caller's device grid `d_in` (N1 x N2 complex128), the columns
+    over the first (2M2+1) x N1 elements of the same buffer (timing only).  Returns a new plan
+    with those p; the oracle must be given that plan."""
+    p1, p2 = plan.plan1, plan.plan2
+    pr, _ = autotune_divisor(p2.N, p2.M, p2.mu, d_in, epsilon=p2.epsilon, device=device, candidates=candidates,
+                             batch=p1.N)
+    pc, _ = autotune_divisor(p1.N, p1.M, p1.mu, d_in, epsilon=p1.epsilon, device=device, candidates=candidates,
+                             batch=2 * p2.M + 1)
+    return Pft2dPlan(build_plan(p1.N, p1.M, p1.mu, pc, p1.epsilon), build_plan(p2.N, p2.M, p2.mu, pr, p2.epsilon))
 
 
 def execute_2d(plan: Pft2dPlan, a, device: int = 0) -> PartialSpectrum2d:

@@ -129,3 +129,19 @@ def test_execute_2d_device_pointers_and_nonfinite(pft, oracle):
     with pytest.raises(ValueError) as e:
         pft.execute_2d(P, a)
     assert e.value.status == 7
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N1,N2,M1,M2,mu1,mu2", [(1024, 2048, 16, 64, 3, -50), (512, 4096, 40, 100, -9, 7)])
+def test_autotune_2d_plan_parity(pft, oracle, N1, N2, M1, M2, mu1, mu2):
+    """autotune_2d picks p per axis on the device (rows at batch N1, columns at batch 2M2+1);
+    the tuned plan passes the same gate against the oracle run on that plan."""
+    import torch
+    P = pft.build_plan_2d(N1, N2, M1, M2, mu1, mu2)
+    a = grid(77, N1, N2)
+    x = torch.from_numpy(a).cuda()
+    T = pft.autotune_2d(P, x.data_ptr())
+    assert N1 % T.plan1.p == 0 and N2 % T.plan2.p == 0
+    assert (T.plan1.M, T.plan2.M, T.plan1.mu, T.plan2.mu) == (M1, M2, mu1, mu2)
+    gpu = pft.execute_2d(T, a).values
+    assert rel_l2(gpu, oracle.execute_2d(T.plan1, T.plan2, a, T.parenthesization)) <= GATE

@@ -40,7 +40,13 @@ METRICS = [
 
 
 def raw(rep: Path) -> dict:
-    out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # a capture too large to copy back is exported on the box (`ncu -i X --page raw --csv`)
+    alt = rep.with_name(rep.name.replace(".ncu-rep", ".raw.csv"))
+    if not rep.exists() and alt.exists():
+        out = alt.read_text()
+    else:
+        out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     units = dict(zip(rows[0], rows[1]))
     return {h: (v, units.get(h, "")) for h, v in zip(rows[0], rows[2])}
@@ -94,7 +100,7 @@ def main() -> None:
     traffic = {}
     for kern in ("k1", "k2"):
         rep = OUT / f"prof_{kern}_{a.tag}.ncu-rep"
-        if not rep.exists():
+        if not rep.exists() and not (OUT / f"prof_{kern}_{a.tag}.raw.csv").exists():
             continue
         d = raw(rep)
         lines += [f"## {kern.upper()} (`--set full`)", "", "| metric | value |", "|---|---|"]
