@@ -320,6 +320,10 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
         twc[t] = v;  // twc[P1 + t'] is tw2[t']
     }
     __syncthreads();
+    // One residue class per signal (P2 = 1: short batched signals, e.g. the 2-D passes): the
+    // row is the output; no row store, ready flag, ticket or read-back (same arithmetic as a
+    // one-row reduction: cadd(0, v) = v).
+    const bool direct = P.P2 == 1;
     double2* __restrict__ rowc = P.Y + ((size_t)b * P.P2 + c) * Q.W;
     for (uint64_t so = tid; so < Q.W; so += nt) {
         const uint64_t sr = so < Q.p ? so : (Q.W >> 32) ? so % Q.p : (uint64_t)((uint32_t)so % (uint32_t)Q.p);
@@ -340,8 +344,16 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
             acc.y = fma(v.y, tp, acc.y);
             if (j + 1 < R) tp *= x;
         }
-        rowc[so] = cmul(cmul(acc, twc[m1]), tw2[e2]);
+        const double2 v = cmul(cmul(acc, twc[m1]), tw2[e2]);
+        if (direct) {
+            const double2 o = cmul(v, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
+            Q.out[(size_t)b * Q.W + so] = o;
+            if (!isfinite(o.x) || !isfinite(o.y)) atomicOr(Q.status, 1);
+        } else {
+            rowc[so] = v;
+        }
     }
+    if (direct) return;
     // publish the row, then take a ticket: the last `reducers` arrivals of signal b reduce
     unsigned* ctl = P.arrivals + (size_t)b * (P.P2 + 2);  // {tickets, done, ready[P2]}
     unsigned* ready = ctl + 2;

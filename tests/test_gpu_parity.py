@@ -211,7 +211,8 @@ def test_autotuned_divisor_plan_parity(pft, oracle):
     assert rel_l2(got, oracle.execute(plan, a)) <= GATE
 
 
-@pytest.mark.parametrize("N,M,mu,p", [(2 ** 16, 256, 0, 256), (2 ** 16, 256, 0, 512), (2 ** 14, 100, -7, 128)])
+@pytest.mark.parametrize("N,M,mu,p", [(2 ** 16, 256, 0, 256), (2 ** 16, 256, 0, 512), (2 ** 14, 100, -7, 128),
+                                     (4096, 64, 5, 64), (4096, 64, -3, 128)])  # P2 = 1: direct output
 def test_batched_small_signals_sum_tail(pft, oracle, N, M, mu, p):
     """C3-style batches (BASELINE configs[2]): a large batch hint gives P2 = 2-4 CTAs per
     signal and the sum tail with W > p (the bins wrap mod p); every signal matches the oracle."""
