@@ -34,7 +34,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 HOST_FLAGS = ["-std=c++20", "-O3", "-march=x86-64-v3", "-fPIC", "-fopenmp", "-Wall", "-Wextra",
               "-Wno-unused-parameter"]
 NVCC_FLAGS = ["-std=c++20", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-fopenmp",
-              "-Xptxas", "-O3", "--expt-relaxed-constexpr", "-split-compile=0"]
+              "-Xptxas", "-O3", "--expt-relaxed-constexpr"]
 
 
 def _run(cmd: list[str], verbose: bool) -> None:

@@ -302,6 +302,95 @@ __device__ __forceinline__ void k1_tc_finish_row(const K1Params& P, double2 x0, 
 // deterministic), times e^{-pi i m / p}.  The transform is one kernel: under PDL the next
 // transform's K1 streams while these few CTAs finish, which a separate K2 (waiting for all of
 // K1) could not allow.
+// One entry of CTA c's residue row: e^{-2 pi i (m mod p) c / p} sum_j Y_c[m1][j] x^j at slot so.
+template <int R>
+__device__ __forceinline__ double2 k1_row_value(const K1Params& P, const double2* res, const double2* twc,
+                                                const double2* tw2, uint32_t c, uint64_t so, int64_t Mh,
+                                                bool p1_pow2, bool p2_pow2, int lg_p1) {
+    const K2Params& Q = P.k2;
+    const uint64_t sr = so < Q.p ? so : (Q.W >> 32) ? so % Q.p : (uint64_t)((uint32_t)so % (uint32_t)Q.p);
+    uint32_t mp = (uint32_t)(Q.first_mod_p + sr);
+    if (mp >= Q.p) mp -= (uint32_t)Q.p;
+    const uint32_t m1 = p1_pow2 ? mp & (P.P1 - 1) : mp % P.P1;
+    const uint32_t m2 = p1_pow2 ? mp >> lg_p1 : mp / P.P1;
+    const uint32_t e2 = p2_pow2 ? (m2 * c) & (P.P2 - 1) : (m2 * c) % P.P2;  // m2 c < p
+    // x = (m - mu)/p; 1/p is exact for power-of-two p (then x^j is bit-identical to the
+    // planner's post_powers), else within an ulp
+    const double x = (double)((int64_t)so - Mh) * Q.inv_p;
+    double2 acc = res[m1];
+    double tp = x;
+#pragma unroll
+    for (int j = 1; j < R; ++j) {  // ascending j, powers by repeated multiplication
+        const double2 v = res[(size_t)j * P.P1 + m1];
+        acc.x = fma(v.x, tp, acc.x);
+        acc.y = fma(v.y, tp, acc.y);
+        if (j + 1 < R) tp *= x;
+    }
+    return cmul(cmul(acc, twc[m1]), tw2[e2]);
+}
+
+// The small-P2 last-arrival reduction (see `fast` in k1_sum_tail).  Compiled only into the
+// tensor-core K1 instantiations (r = 12..18: C3, the 2-D passes): present in the vector-path
+// kernels it cost C1 9% and C4 4% though they never take it (same box A/B); out of line
+// (__noinline__) the call's stack traffic cost every config 8-35%.
+template <int R>
+__device__ __forceinline__ void k1_sum_tail_fast(const K1Params& P, const double2* res, uint32_t c, uint32_t b,
+                                              const double2* twc, double2* tw2, int64_t Mh, bool p1_pow2,
+                                              bool p2_pow2, int lg_p1) {
+    constexpr int FAST_OUT = 4, FAST_P2 = 8;
+    const K2Params& Q = P.k2;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    double2* __restrict__ rowc = P.Y + ((size_t)b * P.P2 + c) * Q.W;
+    double2 keep[FAST_OUT];
+#pragma unroll
+    for (int i = 0; i < FAST_OUT; ++i) {
+        const uint64_t so = (uint64_t)tid + (uint64_t)i * nt;
+        if (so < Q.W) {
+            keep[i] = k1_row_value<R>(P, res, twc, tw2, c, so, Mh, p1_pow2, p2_pow2, lg_p1);
+            rowc[so] = keep[i];
+        }
+    }
+    unsigned* ctl = P.arrivals + (size_t)b * (P.P2 + 2);  // {tickets, ...}
+    unsigned* s_last = reinterpret_cast<unsigned*>(tw2 + P.P2);
+    __syncthreads();  // every row store precedes thread 0's fence and ticket
+    PFT_STAMP(5)
+    if (tid == 0) {
+        __threadfence();
+        *s_last = atomicAdd(ctl, 1u) == P.P2 - 1;
+    }
+    __syncthreads();
+    PFT_STAMP2(0)
+    if (!*s_last) {
+        PFT_STAMP2(3)
+        return;
+    }
+    __threadfence();  // the other rows were fenced before their tickets (threadFenceReduction)
+    PFT_STAMP2(1)
+    const double2* __restrict__ rows = P.Y + (size_t)b * P.P2 * Q.W;
+#pragma unroll
+    for (int i = 0; i < FAST_OUT; ++i) {
+        const uint64_t so = (uint64_t)tid + (uint64_t)i * nt;
+        if (so < Q.W) {
+            double2 v[FAST_P2];
+#pragma unroll
+            for (int r = 0; r < FAST_P2; ++r)
+                v[r] = (uint32_t)r >= P.P2 ? make_double2(0.0, 0.0)
+                       : (uint32_t)r == c  ? keep[i]
+                                           : __ldcg(rows + (size_t)r * Q.W + so);
+            double2 tot = v[0];
+#pragma unroll
+            for (int r = 1; r < FAST_P2; ++r)
+                if ((uint32_t)r < P.P2) tot = cadd(tot, v[r]);  // fixed order c = 0, 1, ...
+            const double2 o = cmul(tot, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
+            Q.out[(size_t)b * Q.W + so] = o;
+            if (!isfinite(o.x) || !isfinite(o.y)) atomicOr(Q.status, 1);
+        }
+    }
+    PFT_STAMP2(2)
+    if (tid == 0) ctl[0] = 0;  // every CTA of the signal has taken its ticket: re-arm
+    PFT_STAMP2(3)
+}
+
 template <int R>
 __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* res, uint32_t c, uint32_t b,
                                          unsigned char* scratch, double2 tail_tw) {
@@ -324,27 +413,22 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     // row is the output; no row store, ready flag, ticket or read-back (same arithmetic as a
     // one-row reduction: cadd(0, v) = v).
     const bool direct = P.P2 == 1;
+    // Few residue classes and few outputs (batched short signals, e.g. C3: P2 = 2, W = 513):
+    // only the last CTA of the signal to arrive reduces, each thread summing the P2 rows of its
+    // own outputs with all loads in flight at once and its own row's values from registers;
+    // the others exit at their ticket.  (The general reducers loop over 64-output groups with a
+    // block barrier each: at C3 fence + wait + reduce took 10.5 of a CTA's 35.6 us.)
+    constexpr int FAST_OUT = 4, FAST_P2 = 8;
+    const bool fast = k1_tc(R) && !direct && P.P2 <= FAST_P2 && Q.W <= (uint64_t)FAST_OUT * nt;
     double2* __restrict__ rowc = P.Y + ((size_t)b * P.P2 + c) * Q.W;
-    for (uint64_t so = tid; so < Q.W; so += nt) {
-        const uint64_t sr = so < Q.p ? so : (Q.W >> 32) ? so % Q.p : (uint64_t)((uint32_t)so % (uint32_t)Q.p);
-        uint32_t mp = (uint32_t)(Q.first_mod_p + sr);
-        if (mp >= Q.p) mp -= (uint32_t)Q.p;
-        const uint32_t m1 = p1_pow2 ? mp & (P.P1 - 1) : mp % P.P1;
-        const uint32_t m2 = p1_pow2 ? mp >> lg_p1 : mp / P.P1;
-        const uint32_t e2 = p2_pow2 ? (m2 * c) & (P.P2 - 1) : (m2 * c) % P.P2;  // m2 c < p
-        // x = (m - mu)/p; 1/p is exact for power-of-two p (then x^j is bit-identical to the
-        // planner's post_powers), else within an ulp
-        const double x = (double)((int64_t)so - Mh) * Q.inv_p;
-        double2 acc = res[m1];
-        double tp = x;
-#pragma unroll
-        for (int j = 1; j < R; ++j) {  // ascending j, powers by repeated multiplication
-            const double2 v = res[(size_t)j * P.P1 + m1];
-            acc.x = fma(v.x, tp, acc.x);
-            acc.y = fma(v.y, tp, acc.y);
-            if (j + 1 < R) tp *= x;
+    if constexpr (k1_tc(R)) {
+        if (fast) {
+            k1_sum_tail_fast<R>(P, res, c, b, twc, tw2, Mh, p1_pow2, p2_pow2, lg_p1);
+            return;
         }
-        const double2 v = cmul(cmul(acc, twc[m1]), tw2[e2]);
+    }
+    for (uint64_t so = tid; so < Q.W; so += nt) {
+        const double2 v = k1_row_value<R>(P, res, twc, tw2, c, so, Mh, p1_pow2, p2_pow2, lg_p1);
         if (direct) {
             const double2 o = cmul(v, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
             Q.out[(size_t)b * Q.W + so] = o;
@@ -372,8 +456,12 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
 #ifdef PFT_DEV_NO_REDUCE  // development A/B only: the sum tail without the reduction
     return;
 #endif
+    PFT_STAMP2(0)  // sum-tail timeline (K2's ring is unused here): ticket taken
     const uint32_t t = *s_ticket, K = P.reducers;
-    if (t + K < P.P2) return;
+    if (t + K < P.P2) {
+        PFT_STAMP2(3)
+        return;
+    }
     // Reducer k sums rows c = 0..P2-1 (fixed order per warp: c = warp, warp + nw, ...) for
     // its slice of outputs once the warp's rows are flagged ready (most are by now).
     const uint32_t k = t + K - P.P2;
@@ -383,6 +471,7 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     for (uint32_t r = warp + (uint32_t)lane * nw; r < P.P2; r += 32u * nw)
         while (ld_acquire_u32(ready + r) == 0) __nanosleep(32);
     __syncwarp();
+    PFT_STAMP2(1)  // (thread 0's warp) its rows are ready
     for (uint64_t g0 = s0; g0 < s1; g0 += 64) {  // two 32-output groups per pass
         const uint64_t sa = g0 + lane, sb = g0 + 32 + lane;
         const bool oka = sa < s1, okb = sb < s1;
@@ -417,6 +506,7 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
         }
         __syncthreads();
     }
+    PFT_STAMP2(2)  // reduction done
     // the last reducer to finish re-arms the signal's counters and flags
     if (tid == 0) *s_ticket = atomicAdd(ctl + 1, 1u) == K - 1;
     __syncthreads();
@@ -428,6 +518,7 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
         }
         __threadfence();
     }
+    PFT_STAMP2(3)
 }
 
 // Last-arrival K2 tail (many output bins, e.g. C2c): K2's work -- the length-P2 pass for one
