@@ -564,7 +564,10 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     const size_t batch_hint = opts && opts->batch_hint > 1 ? (size_t)opts->batch_hint : 1;
     if (!p2 && (forced_mode == 0 || forced_mode == 5)) {  // sum tail, when it pays (or forced)
         p2 = choose_p2_sum(H.p, H.r, prop.multiProcessorCount, batch_hint);
-        if (p2 && forced_mode == 0 && !sum_tail_pays(H.N, d->W, p2, H.r)) p2 = 0;
+        // batched plans (batch_hint > 1) always take the sum tail when it fits: a K2 grid of
+        // P1 x batch CTAs was 2.5-16x slower at every batched shape measured
+        // (tools/probe_cols.py: 129 x 4096, M = 64: 31 vs 12 us; 513 x 1024, M = 32: 92 vs 11 us)
+        if (p2 && forced_mode == 0 && batch_hint <= 1 && !sum_tail_pays(H.N, d->W, p2, H.r)) p2 = 0;
     }
     if (!p2) p2 = choose_p2(H.p, H.r, batch_hint);
     if (p2 == 0 || H.p % p2 != 0) fail(PFT_ERR_INVALID_ARGUMENT, "dplan_create: p2 must divide p");
@@ -612,7 +615,7 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         const bool fits = sizeof(double2) * H.r * d->P1 +
                               pftdev::k1_sum_scratch_bytes((uint32_t)d->P1, (uint32_t)d->P2) <=
                           pftdev::k1_min_ring_bytes(H.r);
-        d->sum_tail = fits && (forced == 5 || (forced == 0 && sum_tail_pays(H.N, d->W, d->P2, H.r)));
+        d->sum_tail = fits && (forced == 5 || (forced == 0 && (batch_hint > 1 || sum_tail_pays(H.N, d->W, d->P2, H.r))));
         // reducing CTAs per signal: one per 64 outputs (measured best at C2b/C4: 32; more
         // reducers hold more SM slots from the next transform), opts override
         d->reducers = (uint32_t)std::min<uint64_t>(d->P2, std::max<uint64_t>(1, (d->W + 63) / 64));
