@@ -763,13 +763,19 @@ def anomaly_from_coeffs(x, coeffs, M: int, k: int) -> tuple[np.ndarray, np.ndarr
     return idx.astype(np.int64), sc, fit
 
 
+_ANOMALY_PLANS: dict = {}
+
+
 def anomaly(x, M: int, k: int, p: Optional[int] = None, epsilon: float = DEFAULT_EPSILON,
             device: int = 0) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
     """cmd_anomaly with source = pft: coefficients on R_{0,M} from one GPU execute, then the
     scoring of anomaly_from_coeffs (inside the library: pft_anomaly)."""
     xv = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
-    plan = build_plan(xv.size, M, 0, p, epsilon)
-    d = DevicePlan(plan, device=device)
+    key = (xv.size, M, p, epsilon, device)
+    d = _ANOMALY_PLANS.get(key)
+    if d is None:  # plans are immutable and reusable (SPEC.md:188): one per shape, not per call
+        d = DevicePlan(build_plan(xv.size, M, 0, p, epsilon), device=device)
+        _ANOMALY_PLANS[key] = d
     idx = np.zeros(k, dtype=np.uint64)
     sc = np.zeros(k, dtype=np.float64)
     fit = np.zeros(xv.size, dtype=np.float64)

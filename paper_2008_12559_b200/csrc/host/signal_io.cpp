@@ -249,13 +249,21 @@ pft_status pft_anomaly_from_coeffs(const double* x, uint64_t N, const pft_c128* 
     PFT_REQUIRE(2 * M <= N, "anomaly: M > N/2");
     // coeffs[s] = a_{s - M}, s in [0, 2M]; a_0 = coeffs[M]
     std::vector<double> score(N), fit(N);
+    // e^{2 pi i t / N} for every residue t, each evaluated once with the exact-angle rule
+    // (SPEC.md:377); term (m, n) then reads t = (m n) mod N, stepped by n without a 128-bit
+    // modulo -- the same values as evaluating cispi per term (N + N M work instead of N M
+    // angle evaluations)
+    std::vector<cplx> tab(N);
+#pragma omp parallel for schedule(static)
+    for (long long t = 0; t < (long long)N; ++t) tab[t] = cispi_frac(2 * (__int128)t, N);
 #pragma omp parallel for schedule(static)
     for (long long n = 0; n < (long long)N; ++n) {
         double acc = coeffs[M].re;
+        uint64_t red = 0;  // (m n) mod N
         for (uint64_t m = 1; m <= M; ++m) {
-            // e^{2 pi i m n / N} with (m n) mod N exact (SPEC.md:377 exact-angle rule)
-            const uint64_t red = (uint64_t)(((unsigned __int128)m * (uint64_t)n) % N);
-            const cplx e = cispi_frac(2 * (__int128)red, N);
+            red += (uint64_t)n;
+            if (red >= N) red -= N;
+            const cplx& e = tab[red];
             acc += 2.0 * (coeffs[M + m].re * e.real() - coeffs[M + m].im * e.imag());
         }
         fit[n] = acc / (double)N;
