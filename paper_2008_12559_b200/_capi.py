@@ -134,7 +134,11 @@ def load() -> C.CDLL:
                           "(there is no pure-Python fallback)")
     lib = C.CDLL(str(path))
     for name, (res, args) in SIGNATURES.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None:  # an older development build (PFT_LIB) without this entry point
+            if path == LIB_PATH:
+                raise ImportError(f"{path} does not export {name}: rebuild it")
+            continue
         fn.restype = res
         fn.argtypes = args
     _lib = lib

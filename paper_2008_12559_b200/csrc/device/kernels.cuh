@@ -188,6 +188,9 @@ inline size_t ctrl_bytes(size_t batch, size_t per_signal) {
 inline size_t k1_sum_scratch_bytes(uint32_t P1, uint32_t P2) {
     return 16 * ((size_t)P1 + P2) + (size_t)K1_THREADS / 32 * 64 * 16 + 16;
 }
+// r values with a K2-tail K1 instantiation: the long single transforms it pays for (C5: r = 6
+// at p = 2^18-2^19; SPEC's pick for N = 2^30 has r = 4).  Other r run the K2 grid.
+__host__ __device__ constexpr bool k1_k2_tail_instantiated(int r) { return r >= 4 && r <= 7; }
 // K1's last-arrival K2 tail: Z + scratch for `group` columns, omega_P2 + four-step twiddles,
 // ticket word
 inline size_t k1_k2_tail_bytes(uint32_t group, uint32_t P2) {

@@ -628,7 +628,8 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         // the stream: C5 (2^30) gains 6% (3099 -> 2907 us), C2c (2^24, 2 rounds) loses (67 -> 77
         // us at 1 round).  reserved[3]: 3 forces it on (if feasible), 4 off (separate K2 grid).
         const int want_tail = opts_k2_tail(opts);
-        if (!d->sum_tail && d->k2_mode == pftdev::K2_FFT && !d->allow_fuse && want_tail != 4) {
+        if (!d->sum_tail && d->k2_mode == pftdev::K2_FFT && !d->allow_fuse && want_tail != 4 &&
+            pftdev::k1_k2_tail_instantiated(H.r)) {
             const size_t ring = (size_t)d->k1_stages * pftdev::k1_stage_bytes(H.r);
             const size_t fixed = pftdev::k1_k2_tail_bytes(0, (uint32_t)d->P2);
             const size_t per_col = 2 * sizeof(double2) * d->P2;

@@ -412,7 +412,11 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     // One residue class per signal (P2 = 1: short batched signals, e.g. the 2-D passes): the
     // row is the output; no row store, ready flag, ticket or read-back (same arithmetic as a
     // one-row reduction: cadd(0, v) = v).
+#ifdef PFT_NO_DIRECT  // development A/B
+    const bool direct = false;
+#else
     const bool direct = P.P2 == 1;
+#endif
     // Few residue classes and few outputs (batched short signals, e.g. C3: P2 = 2, W = 513):
     // only the last CTA of the signal to arrive reduces, each thread summing the P2 rows of its
     // own outputs with all loads in flight at once and its own row's values from registers;
@@ -646,7 +650,7 @@ __device__ __forceinline__ void k1_k2_tail(const K1Params& P, uint32_t c, uint32
     }
 }
 
-template <int R, bool MU0>
+template <int R, bool MU0, bool K2T = false>
 __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_constant__ CUtensorMap tmap,
                                                                   const K1Params P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -848,9 +852,13 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         Y[((size_t)m1 * P.P2 + c) * R + j] = res[(size_t)j * P.P1 + m1];
     }
     PFT_STAMP(5)
-    if (P.k2_tail) {
-        k1_k2_tail<R>(P, c, b, reinterpret_cast<double2*>(ring));
-        return;
+    // the K2 tail lives in its own instantiations (K2T, k1_k2_tail_instantiated(R)): its code in
+    // every K1 cost C2b 2% (same-box A/B: 43.0 vs 42.2 us) though C2b never takes it
+    if constexpr (K2T) {
+        if (P.k2_tail) {
+            k1_k2_tail<R>(P, c, b, reinterpret_cast<double2*>(ring));
+            return;
+        }
     }
     if (P.fused) {
         // Fused K2: once every residue's slab is in L2, CTA (c, b) finishes bins m1 = c,
@@ -1226,6 +1234,13 @@ static cudaError_t launch_k1_r(const CUtensorMap& map, const K1Params& P, dim3 g
     }
     cfg.attrs = attr;
     cfg.numAttrs = n;
+    if constexpr (k1_k2_tail_instantiated(R)) {
+        if (P.k2_tail) {
+            if (mu0) return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, true, true>, map, P);
+            return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, false, true>, map, P);
+        }
+    }
+    if (P.k2_tail) return cudaErrorInvalidValue;  // no K2-tail instantiation for this r
     if (mu0) return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, true>, map, P);
     return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, false>, map, P);
 }
@@ -1235,6 +1250,11 @@ static cudaError_t configure_k1_r(size_t smem, bool mu0) {
     const auto a = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e = mu0 ? cudaFuncSetAttribute(k1_contract_fft<R, true>, a, (int)smem)
                         : cudaFuncSetAttribute(k1_contract_fft<R, false>, a, (int)smem);
+    if constexpr (k1_k2_tail_instantiated(R)) {
+        if (e == cudaSuccess)
+            e = mu0 ? cudaFuncSetAttribute(k1_contract_fft<R, true, true>, a, (int)smem)
+                    : cudaFuncSetAttribute(k1_contract_fft<R, false, true>, a, (int)smem);
+    }
     return e;
 }
 

@@ -164,7 +164,8 @@ def test_batched_workspace_and_tail_forms(pft, oracle, form):
     oracle runs."""
     import torch
     N, M, mu, batch = 2 ** 16, 128, 77, 3
-    plan = pft.build_plan(N, M, mu, None, 1e-12)
+    # the K2 tail has K1 instantiations for r = 4..7 only (k1_k2_tail_instantiated): p = 4096, r = 7
+    plan = pft.build_plan(N, M, mu, 4096 if form.startswith("k2-tail") else None, 1e-12)
     kw = {"fused": dict(fuse=True, k2_mode=1), "k2": dict(k2_mode=1, k2_tail=-1),
           "k2-tail": dict(k2_mode=1, k2_tail=1), "k2-tail-1": dict(k2_mode=1, k2_tail=1, reducers=1),
           "sum": dict(k2_mode=5), "sum-all-reduce": dict(k2_mode=5, reducers=1 << 20)}[form]
@@ -272,10 +273,10 @@ def test_every_second_pass_form(pft, oracle, mode):
 
 
 @pytest.mark.parametrize("N,M,mu,p,reducers", [
-    (2 ** 20, 2 ** 12, 2 ** 18, 2 ** 12, 0),        # W = 8193 > p: wrapped bins
-    (2 ** 22, 2 ** 12, -5, 2 ** 13, 3),             # few workers, several m1 each
-    (6220800, 4000, -12345, 15360, 0),              # non-power-of-two P1 / P2
-    (2 ** 24, 2 ** 14, 2 ** 22, 2 ** 15, 0),        # C2c at the autotuned p: r = 14, two j groups
+    (2 ** 22, 2 ** 8, 5, 2 ** 13, 0),               # r = 7
+    (2 ** 22, 2 ** 9, -5, 2 ** 15, 3),              # few workers, several m1 each
+    (6220800, 300, -12345, 15360, 0),               # non-power-of-two P1 / P2
+    (2 ** 24, 2 ** 12, 2 ** 22, 2 ** 18, 0),        # C5-like: W = 8193, P1 = 512 m1 rounds
 ])
 def test_k2_tail_matches_k2_grid(pft, oracle, N, M, mu, p, reducers):
     """K2's work done by K1's last-arriving CTAs (one kernel, j in groups that fit K1's ring)
