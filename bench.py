@@ -244,9 +244,9 @@ def run_ours(args):
     else:
         p_src = "config"
     plan = pft.build_plan(N, M, mu, p, EPS)
-    d = pft.DevicePlan(plan, device=local, p2=args.p2, pdl=not args.no_pdl, fuse=args.fuse, batch_hint=B,
-                       k2_mode=args.k2_mode, k2_tail={"auto": 0, "on": 1, "off": -1}[args.k2_tail],
-                       reducers=args.reducers, k2_ctas=args.k2_ctas)
+    d = pft.DevicePlan(plan, device=local, p2=args.p2, batch_hint=B, second_pass=args.second_pass,
+                       k2_at=args.k2_at, tail_ctas=args.tail_ctas, k2_grid_ctas=args.k2_grid_ctas)
+    overlap = not args.no_pdl  # independent inputs: PFT_EXEC_OVERLAP_PREVIOUS is the caller's promise
     launches = d.launches_per_execute()
 
     stream = torch.cuda.Stream(device=dev)
@@ -264,14 +264,14 @@ def run_ours(args):
     def step(i):
         if args.streams == 1:
             d.execute_ptr(bufs[i % nbuf].data_ptr(), out.data_ptr(), batch=B, in_stride=N,
-                          d_ws=ws[0].data_ptr(), stream=sp)
+                          d_ws=ws[0].data_ptr(), stream=sp, overlap=overlap)
             return
         if i % 2 == 0:
             fork.record(stream)
             side.wait_event(fork)
         st = stream if i % 2 == 0 else side
         d.execute_ptr(bufs[i % nbuf].data_ptr(), outs[i % 2].data_ptr(), batch=B, in_stride=N,
-                      d_ws=ws[i % 2].data_ptr(), stream=st.cuda_stream)
+                      d_ws=ws[i % 2].data_ptr(), stream=st.cuda_stream, overlap=overlap)
         if i % 2 == 1 or i == args.steps - 1:
             join.record(st)
             stream.wait_event(join)
@@ -311,11 +311,26 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
-    # single-execute latency (one stream, executes back to back)
+    # chained latency: one stream, executes back to back (the overlap flag as in the timed chain)
     n_lat = min(args.steps, 200)
     lat_graph = capture(lambda i: d.execute_ptr(bufs[i % nbuf].data_ptr(), out.data_ptr(), batch=B, in_stride=N,
-                                                d_ws=ws[0].data_ptr(), stream=sp), n_lat)
+                                                d_ws=ws[0].data_ptr(), stream=sp, overlap=overlap), n_lat)
     latency_us = timed(lat_graph) / n_lat * 1e3
+    # isolated latency: ONE execute on an idle device (synchronised before, CUDA events around
+    # it, no overlap with any other transform), input rotated so it is not L2-resident; median
+    iso = []
+    for i in range(max(5, min(args.steps, 30))):
+        torch.cuda.synchronize(dev)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a0.record(stream)
+            d.execute_ptr(bufs[(i + 1) % nbuf].data_ptr(), out.data_ptr(), batch=B, in_stride=N,
+                          d_ws=ws[0].data_ptr(), stream=sp)
+            a1.record(stream)
+        torch.cuda.synchronize(dev)
+        iso.append(a0.elapsed_time(a1) * 1e3)
+    iso.sort()
+    latency_iso_us = iso[len(iso) // 2]
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -341,9 +356,28 @@ def run_ours(args):
     else:
         k1_note = "K1 timed alone (slab output) in a chain of launches"
 
-    # parity spot-check of this run's output against the oracle is in tests/; here only
-    # the non-finite status word is checked
-    status = d.status(stream=sp)
+    status = d.status(stream=sp, d_ws=ws[0].data_ptr())
+    # parity of this run: the last timed input through the same plan (untimed, no overlap) vs the
+    # CPU oracle on the same plan (batched: the first <= 64 signals)
+    parity = None
+    if rank == 0 and not args.no_parity:
+        import numpy as np
+        import oracle
+        src = bufs[(args.steps - 1) % nbuf]
+        d.execute_ptr(src.data_ptr(), out.data_ptr(), batch=B, in_stride=N, d_ws=ws[0].data_ptr(), stream=sp)
+        torch.cuda.synchronize(dev)
+        nb = min(B, 64)
+        got = out[:W * nb].cpu().numpy().reshape(nb, W)
+        t0 = time.perf_counter()
+        worst = 0.0
+        for b in range(nb):
+            ref = oracle.execute(plan, src[b * N:(b + 1) * N].cpu().numpy())
+            worst = max(worst, float(np.linalg.norm(got[b] - ref) / np.linalg.norm(ref)))
+        parity = {"rel_l2_vs_oracle": worst, "gate": 1e-11, "pass": worst <= 1e-11,
+                  "signals_checked": nb, "oracle_seconds": time.perf_counter() - t0,
+                  "what": "last timed input, same plan (p, r, P1, P2, tail), CPU oracle oracle/oracle.cpp"}
+        if worst > 1e-11:
+            log(f"PARITY FAILURE: rel_l2 {worst:.3e} > 1e-11")
 
     line = None
     if rank == 0:
@@ -404,7 +438,7 @@ def run_ours(args):
                        "l2": (f"one input of {16 * N * B / 2**30:.2f} GiB (> L2 126 MiB)" if nbuf == 1 else
                               f"{nbuf} rotating inputs of {16 * N / 2**20:.0f} MiB (> L2 126 MiB)"),
                        "timing": "CUDA graph of K steps, CUDA events on the launch stream",
-                       "streams": args.streams, "pdl": not args.no_pdl, "fused_k2": args.fuse,
+                       "streams": args.streams, "overlap_previous": overlap,
                        "tail": {"sum tail": "sum tail in K1 (one kernel per execute)",
                                 "K2 tail": "K2 work by K1's last-arriving CTAs (one kernel per execute)",
                                 "fused K2": "K2 in K1 behind a grid barrier (one kernel per execute)"}.get(
@@ -413,7 +447,10 @@ def run_ours(args):
                                      "workspaces" if args.streams == 2 else
                                      "single stream; execute i+1's K1 starts streaming while execute "
                                      "i finishes, via programmatic dependent launch"},
-            "latency_us_single_stream": latency_us,
+            "latency_us_isolated": latency_iso_us,
+            "latency_us_chained": latency_us,
+            "parity_rel_l2": parity["rel_l2_vs_oracle"] if parity else None,
+            "parity": parity,
             "input_gbs": value * 16 * N / 1e9,
             "input_gbs_frac_of_peak": value * 16 * N / 1e9 / world / peak,
             "roofline": {"bound": "hbm", "kernel": "k1_contract_fft", "achieved": k1_gbs, "peak": peak,
@@ -436,39 +473,63 @@ def run_ours(args):
 
 def run_sharded(args, world, rank, local, dev):
     """One huge transform split along the contraction axis: every rank
-    runs K1 on its column slice into a partial slab, NCCL reduces the slabs onto rank 0, which
-    runs K2.  Strong scaling: value = whole-job transforms/s, time = max over ranks."""
+    runs pft_execute_sharded -- K1 on its column slice into a partial slab, ncclReduce of the
+    slabs onto rank 0 over NVLink, K2 on rank 0 -- as ONE library call per step, K steps captured
+    in one CUDA graph.  Strong scaling: value = whole-job transforms/s, time = max over ranks."""
     import torch
     import torch.distributed as dist
     import paper_2008_12559_b200 as pft
-    from paper_2008_12559_b200.sharded import ShardedTransform, gather_local_device
+    from paper_2008_12559_b200.sharded import ShardedTransform, gather_local_device, init_comm, select_divisor_sharded
 
     N, M, mu, p, kind, desc = CONFIGS[args.config]
     W = 2 * M + 1
-    p = args.p or pft.select_divisor_device(N, M, epsilon=EPS)[0]
+    if args.p:
+        p, p_src = args.p, "--p"
+    else:
+        p, _, est = select_divisor_sharded(N, M, world, epsilon=EPS)
+        p_src = f"pft_select_divisor_sharded (model incl. the collective: {est:.0f} us at {world} GPUs)"
     plan = pft.build_plan(N, M, mu, p, EPS)
     st = ShardedTransform(plan, world, rank, root=0, device=local, p2=args.p2)
+    comm = init_comm(world, rank, local)
     # this rank's slice of the (device-generated) global signal; setup, not timed
     full = torch.empty(N, dtype=torch.complex128, device=dev)
     make_input_device(pft, full, N, mu, M, SEEDS[args.config], kind, N=N)
     x = gather_local_device(full, plan.p, plan.q, world, rank)
+    ref = None
+    if world == 1:  # --force-sharded on one GPU: checked against the plain execute below
+        ref = torch.empty(W, dtype=torch.complex128, device=dev)
+        st.dplan.execute_ptr(full.data_ptr(), ref.data_ptr())
+        torch.cuda.synchronize(dev)
     del full
     torch.cuda.empty_cache()
     slab = torch.empty(plan.p * plan.r, dtype=torch.complex128, device=dev)
     out = torch.empty(W, dtype=torch.complex128, device=dev)
-    launches = 2 if rank == 0 else 1
-    for _ in range(args.warmup):
-        st.execute(x, slab, out)
+    stream = torch.cuda.Stream(device=dev)
+    sp = stream.cuda_stream
+    launches = 2 if rank == 0 else 1  # K1 (+ K2 on the root); the NCCL kernel is NCCL's
+
+    def step():
+        st.execute_nccl(comm, x.data_ptr(), slab.data_ptr(), out.data_ptr(), stream=sp)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize(dev)
+    with torch.cuda.stream(stream):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(args.steps):
+                step()
+        g.replay()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk, torch.cuda.stream(stream):
         torch.cuda.synchronize(dev)
-        e0.record()
-        for _ in range(args.steps):  # eager: the NCCL reduce sits between K1 and K2
-            st.execute(x, slab, out)
-        e1.record()
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
         torch.cuda.synchronize(dev)
     t = torch.tensor([e0.elapsed_time(e1)], device=dev)
     if world > 1:
@@ -479,10 +540,7 @@ def run_sharded(args, world, rank, local, dev):
     peak, peak_src = measured_hbm_peak()
     local_bytes = 16 * plan.p * st.layout.row_len
     check = None
-    if world == 1:  # --force-sharded on one GPU: the partial/finalize path against plain execute
-        ref = torch.empty_like(out)
-        st.dplan.execute_ptr(x.data_ptr(), ref.data_ptr())
-        torch.cuda.synchronize(dev)
+    if ref is not None:
         check = float(torch.linalg.vector_norm(out - ref) / torch.linalg.vector_norm(ref))
     status = st.dplan.status() if rank == 0 else 0
     if rank == 0:
@@ -492,11 +550,12 @@ def run_sharded(args, world, rank, local, dev):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
             "config": {"workload": f"{args.config}: {desc}", "N": N, "M": M, "mu": mu, "epsilon": EPS,
                        "p": plan.p, "q": plan.q, "r": plan.r, "P1": st.dplan.P1, "P2": st.dplan.P2,
-                       "p_choice": "--p" if args.p else "pft_select_divisor_device (model)",
-                       "parallelism": f"contraction axis split over {world} GPUs + NCCL reduce of the "
-                                      f"{16 * plan.p * plan.r / 2**20:.1f} MiB partial slab",
+                       "p_choice": p_src,
+                       "parallelism": f"contraction axis split over {world} GPUs + ncclReduce of the "
+                                      f"{16 * plan.p * plan.r / 2**20:.1f} MiB partial slab inside pft_execute_sharded",
                        "l2": f"per-rank slice of {local_bytes / 2**30:.2f} GiB (> L2 126 MiB)",
-                       "timing": "eager steps (K1 | NCCL reduce | K2 on rank 0), CUDA events, max over ranks"},
+                       "timing": "CUDA graph of K pft_execute_sharded steps (K1 | ncclReduce | K2 on rank 0), "
+                                 "CUDA events, max over ranks"},
             "input_gbs": value * 16 * N / 1e9,
             "input_gbs_frac_of_peak": value * 16 * N / 1e9 / world / peak,
             "roofline": {"bound": "hbm", "kernel": "k1_contract_fft", "achieved": local_bytes / (ms_step * 1e-3) / 1e9,
@@ -512,6 +571,7 @@ def run_sharded(args, world, rank, local, dev):
             "sharded_vs_plain_rel_l2": check,
         }
         print(json.dumps(line), flush=True)
+    comm.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -529,16 +589,17 @@ def main():
     ap.add_argument("--streams", type=int, default=1, choices=[1, 2],
                     help="1 (default): one stream; consecutive transforms overlap through programmatic "
                          "dependent launch (K2 releases the next K1).  2: alternate two streams")
-    ap.add_argument("--k2-mode", type=int, default=0,
-                    help="second-pass form (0 auto; 1 K2 fft, 2 dot, 3 direct, 4 L2, 5 sum tail)")
+    ap.add_argument("--second-pass", default="auto", choices=["auto", "sum", "k2-fft", "k2-dot", "k2-direct", "k2-l2"],
+                    help="second-pass form (PFT_PASS2_*)")
     ap.add_argument("--force-sharded", action="store_true",
                     help="c5: run the contraction-axis sharded path even on one GPU (checks it)")
-    ap.add_argument("--no-pdl", action="store_true", help="plain stream order between kernels")
-    ap.add_argument("--fuse", action="store_true", help="fuse K2 into K1's tail (grid barrier)")
-    ap.add_argument("--k2-tail", default="auto", choices=["auto", "on", "off"],
-                    help="K2's work by K1's last-arriving CTAs instead of a K2 grid (many output bins)")
-    ap.add_argument("--k2-ctas", type=int, default=0, help="K2 grid width (L2 form)")
-    ap.add_argument("--reducers", type=int, default=0, help="sum tail / K2 tail working CTAs per signal (0 = plan)")
+    ap.add_argument("--no-pdl", action="store_true",
+                    help="no PFT_EXEC_OVERLAP_PREVIOUS: each execute waits for the previous one")
+    ap.add_argument("--k2-at", default="auto", choices=["auto", "grid", "tail", "fused"],
+                    help="where the K2 FFT form runs (PFT_K2_AT_*)")
+    ap.add_argument("--k2-grid-ctas", type=int, default=0, help="K2 grid width (L2 form)")
+    ap.add_argument("--tail-ctas", type=int, default=0, help="sum tail / K2 tail working CTAs per signal (0 = plan)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the untimed oracle check of the output")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

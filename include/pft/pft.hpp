@@ -13,7 +13,9 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -178,7 +180,9 @@ inline std::pair<std::size_t, double> autotune_divisor(std::size_t N, std::size_
 }
 
 // Frozen configuration.  Tables are host copies; the device upload is
-// made lazily by execute() and cached in the plan.
+// made on first use per device and cached in the plan.  A plan is shareable across threads
+// (SPEC.md:188, 263-265): the cache is guarded by a mutex and shared by copies of the plan, and
+// device plans are never replaced once created (a call on another device adds its own).
 struct PftPlan {
     std::size_t N = 0, M = 0;
     std::int64_t mu = 0;
@@ -192,20 +196,24 @@ struct PftPlan {
     TargetRange range() const { return TargetRange{mu, M}; }
     pft_hplan_t handle() const { return host_.get(); }
     pft_dplan_t device_plan(int device = 0) const {
-        if (!device_ || device_dev_ != device) {
-            pft_dplan_opts o{};
-            o.device = device;
-            pft_dplan_t d = nullptr;
-            detail_api::check(pft_dplan_create(host_.get(), &o, &d));
-            device_ = std::shared_ptr<pft_dplan_s>(d, [](pft_dplan_s* x) { pft_dplan_destroy(x); });
-            device_dev_ = device;
-        }
-        return device_.get();
+        std::lock_guard<std::mutex> lk(devices_->mu);
+        auto it = devices_->plans.find(device);
+        if (it != devices_->plans.end()) return it->second.get();
+        pft_dplan_opts o{};
+        o.device = device;
+        pft_dplan_t d = nullptr;
+        detail_api::check(pft_dplan_create(host_.get(), &o, &d));
+        auto& slot = devices_->plans[device];
+        slot = std::shared_ptr<pft_dplan_s>(d, [](pft_dplan_s* x) { pft_dplan_destroy(x); });
+        return slot.get();
     }
 
+    struct DeviceCache {
+        std::mutex mu;
+        std::map<int, std::shared_ptr<pft_dplan_s>> plans;
+    };
     std::shared_ptr<pft_hplan_s> host_;
-    mutable std::shared_ptr<pft_dplan_s> device_;
-    mutable int device_dev_ = -1;
+    std::shared_ptr<DeviceCache> devices_ = std::make_shared<DeviceCache>();
 };
 
 inline PftPlan build_plan(std::size_t N, std::size_t M, std::int64_t mu, std::optional<std::size_t> p,
@@ -246,8 +254,10 @@ inline std::string plan_json(const PftPlan& P) {
 // ---------------------------------------------------------------- transform
 
 // execute(plan, a) -> PartialSpectrum: host vector in, host spectrum out;
-// the transform runs on the GPU (H2D, K1, K2, D2H).  Throws std::invalid_argument on a
-// length mismatch or non-finite input.
+// the transform runs on the GPU (H2D, kernels, D2H through a staging set the device plan keeps,
+// so repeated calls do not allocate).  Re-entrant: concurrent calls on one plan use distinct
+// staging sets and status words.  Throws std::invalid_argument on a length mismatch or
+// non-finite input, pft::DeviceError without a usable sm_100 GPU.
 inline PartialSpectrum execute(const PftPlan& plan, const ComplexVec& a, int device = 0) {
     if (a.size() != plan.N)
         throw std::invalid_argument("execute: length mismatch (a.len=" + std::to_string(a.size()) +
@@ -262,12 +272,13 @@ inline PartialSpectrum execute(const PftPlan& plan, const ComplexVec& a, int dev
 }
 
 // Device-pointer form: asynchronous on `stream`, no allocation when `workspace` is given
-// (pft_workspace_bytes), graph-capturable.
+// (pft_workspace_bytes), graph-capturable.  flags: PFT_EXEC_OVERLAP_PREVIOUS lets K1 stream
+// while the preceding kernel on the stream finishes (d_in must not be that kernel's output).
 inline void execute_device(const PftPlan& plan, const cplx* d_in, cplx* d_out, void* stream = nullptr,
                            void* workspace = nullptr, std::size_t batch = 1, std::size_t in_stride = 0,
-                           int device = 0) {
-    detail_api::check(pft_execute(plan.device_plan(device), detail_api::c(d_in), batch, in_stride,
-                                  detail_api::c(d_out), workspace, stream));
+                           int device = 0, unsigned flags = PFT_EXEC_DEFAULT) {
+    detail_api::check(pft_execute_ex(plan.device_plan(device), detail_api::c(d_in), batch, in_stride,
+                                     detail_api::c(d_out), workspace, stream, flags));
 }
 
 }  // namespace pft

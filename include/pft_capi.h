@@ -151,11 +151,30 @@ pft_status pft_plan_json(pft_hplan_t plan, char* buf, size_t cap, size_t* needed
 
 typedef struct pft_dplan_s* pft_dplan_t;
 
+/* Second pass (the length-P2 FFT over the residue classes, pruned to the 2M+1 bins, fused with
+ * the Eq. (7) post-process).  AUTO picks by the shape. */
+#define PFT_PASS2_AUTO 0
+#define PFT_PASS2_SUM_TAIL 1   /* inside K1: residue rows summed by K1's last arrivals (few bins) */
+#define PFT_PASS2_K2_FFT 2     /* K2: length-P2 Stockham FFT in shared memory                  */
+#define PFT_PASS2_K2_DOT 3     /* K2: direct dot over P2 from shared memory (few bins per m1)  */
+#define PFT_PASS2_K2_DIRECT 4  /* K2: direct sum over P2 from global memory (any P2)           */
+#define PFT_PASS2_K2_L2 5      /* K2: one warp per bin over the L2-resident slab, no smem       */
+/* Where the K2 work of the PFT_PASS2_K2_FFT form runs. */
+#define PFT_K2_AT_AUTO 0
+#define PFT_K2_AT_GRID 1       /* a separate K2 launch after K1                                 */
+#define PFT_K2_AT_TAIL 2       /* by K1's last-arriving CTAs (r = 4..7)                         */
+#define PFT_K2_AT_FUSED 3      /* in K1 behind a grid-wide barrier (cooperative launch)         */
+
 typedef struct pft_dplan_opts {
-    int device;        /* CUDA ordinal                                              */
-    uint64_t p2;       /* residue classes for K1 (0 = auto); must divide p          */
-    int k1_stages;     /* K1 TMA ring depth, 4..8 (0 = deepest that keeps 2 CTAs/SM) */
-    int reserved[6];   /* development A/B knobs, 0 = default (see DevicePlan in __init__.py) */
+    int device;          /* CUDA ordinal                                                      */
+    uint64_t p2;         /* residue classes for K1 (0 = auto); must divide p                  */
+    int k1_stages;       /* K1 TMA ring depth, 3..8 (0 = deepest that keeps 2 CTAs/SM)         */
+    int second_pass;     /* PFT_PASS2_*                                                        */
+    int k2_at;           /* PFT_K2_AT_*                                                        */
+    int tail_ctas;       /* sum-tail reducers / K2-tail workers per signal (0 = plan); always
+                            capped below the co-resident K1 capacity (forward progress)       */
+    int k2_grid_ctas;    /* grid width of the PFT_PASS2_K2_L2 form (0 = SM count)              */
+    int reserved[2];     /* must be 0                                                          */
     uint64_t batch_hint; /* typical batch per execute (0/1 = single signal): sizes the K1 grid */
 } pft_dplan_opts;
 
@@ -164,18 +183,34 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
 void pft_dplan_destroy(pft_dplan_t d);
 /* Chosen decomposition p = P1 * P2 (P1 = local FFT length per residue class). */
 pft_status pft_dplan_layout(pft_dplan_t d, uint64_t* p1, uint64_t* p2);
-/* Device workspace bytes for `batch` independent transforms (zero it once before first use;
- * the library leaves it in a reusable state). */
+/* Device workspace bytes for up to `batch` independent transforms per call.  Zero it once
+ * before first use; every execute leaves it re-armed.  Layout: a 256-byte header (grid-barrier
+ * words, the non-finite status word) then one block per signal (control words, data), so a
+ * workspace sized for batch B serves every call with batch <= B. */
 pft_status pft_workspace_bytes(pft_dplan_t d, size_t batch, size_t* bytes);
 /* Bytes of one partial slab (the reducible intermediate, p*r complex128 per transform). */
 pft_status pft_partial_bytes(pft_dplan_t d, size_t batch, size_t* bytes);
 
+/* execute flags */
+#define PFT_EXEC_DEFAULT 0u
+/* Programmatic dependent launch (PDL): K1 may start streaming its input while the preceding
+ * kernel on `stream` is still finishing -- the throughput mode for a stream of independent
+ * transforms (execute i+1 streams while execute i reduces its last bins).  The caller
+ * guarantees that d_in is NOT written by the preceding kernel on the stream (for example the
+ * previous execute's d_out, or a kernel that triggers its dependents early, such as a PDL-enabled
+ * GEMM).  Without the flag K1 starts only after the preceding work on the stream completed. */
+#define PFT_EXEC_OVERLAP_PREVIOUS 1u
+
 /* execute: d_in holds `batch` signals of N complex128, signal b at d_in + b*in_stride;
  * d_out receives batch x (2M+1) values, signal b at d_out + b*(2M+1).
- * d_ws: pft_workspace_bytes(batch) bytes of device memory, or NULL to use the plan's
- * own workspace (then calls on the plan must be serialised).  stream: cudaStream_t. */
+ * d_ws: pft_workspace_bytes(>= batch) bytes of device memory, or NULL to use the plan's
+ * own batch-1 workspace (then calls on the plan must be serialised).  stream: cudaStream_t.
+ * Asynchronous, allocation-free, graph-capturable.  Non-finite input sets bit 0 of the
+ * workspace's status word (pft_workspace_status / pft_status_query). */
 pft_status pft_execute(pft_dplan_t d, const pft_c128* d_in, size_t batch, size_t in_stride,
                        pft_c128* d_out, void* d_ws, void* stream);
+pft_status pft_execute_ex(pft_dplan_t d, const pft_c128* d_in, size_t batch, size_t in_stride,
+                          pft_c128* d_out, void* d_ws, void* stream, unsigned flags);
 
 /* Sharded single transform (contraction-axis split, BASELINE.json configs[4]).
  * Columns of A are owned in mirror pairs (l, q-l), l in [1, ceil(q/2)), split contiguously
@@ -184,7 +219,8 @@ pft_status pft_execute(pft_dplan_t d, const pft_c128* d_in, size_t batch, size_t
  * execute_partial contracts the local slice and applies K1's FFT pass, writing a reducible
  * partial slab of pft_partial_bytes (the sum over ranks == the unsharded slab, e.g. via
  * ncclReduce/ncclAllReduce with ncclDouble/ncclSum); finalize turns the reduced slab into
- * the 2M+1 outputs.  world == 1 is the natural (unsharded) layout. */
+ * the 2M+1 outputs.  world == 1 is the natural (unsharded) layout.  pft_execute_sharded
+ * below does all three steps with the NCCL reduce inside the library. */
 typedef struct pft_shard_info {
     uint64_t pair_begin, pair_end; /* global pair indices [pair_begin, pair_end)            */
     uint64_t row_len;              /* local columns per row                                 */
@@ -203,14 +239,46 @@ pft_status pft_execute_partial(pft_dplan_t d, const pft_c128* d_in_local, int wo
 pft_status pft_finalize(pft_dplan_t d, const pft_c128* d_partial, size_t batch, pft_c128* d_out,
                         void* stream);
 
-/* Status word written by the kernels (non-finite output => non-finite input).
- * Synchronises `stream`; *flags bit0 = non-finite seen since the last reset. */
+/* The sharded transform with its collective inside the library (SURVEY.md §8(b),(e)): on
+ * every rank of `comm`, K1 on the local slice (pft_execute_partial) -> ncclReduce(sum, ncclDouble)
+ * of the partial slab onto `root` over NVLink/NVSwitch -> on the root, K2 (pft_finalize) into
+ * d_out.  One asynchronous call per rank on `stream` (graph-capturable).  d_slab:
+ * pft_partial_bytes(d, 1) bytes on every rank (reduced in place); d_out (2M+1 values) is only
+ * written on the root (may be NULL elsewhere).  The device plan must live on the
+ * communicator's device.  World size and rank are the communicator's.  NCCL is loaded at run
+ * time (libnccl.so.2; the copy already in the process when there is one), so `comm` may come
+ * from the caller's own NCCL or from pft_nccl_comm_init.                                       */
+struct ncclComm; /* NCCL's communicator: ncclComm_t == struct ncclComm* */
+#define PFT_NCCL_UNIQUE_ID_BYTES 128
+pft_status pft_nccl_available(int* available);
+pft_status pft_nccl_get_unique_id(unsigned char* id /* [PFT_NCCL_UNIQUE_ID_BYTES] */);
+pft_status pft_nccl_comm_init(int world, int rank, const unsigned char* id, int device, struct ncclComm** comm);
+pft_status pft_nccl_comm_destroy(struct ncclComm* comm);
+pft_status pft_execute_sharded(pft_dplan_t d, const pft_c128* d_in_local, uint64_t row_stride,
+                               struct ncclComm* comm, int root, pft_c128* d_slab, pft_c128* d_out,
+                               void* stream);
+/* Device-aware p for the sharded transform over `world` GPUs: the single-GPU time model on the
+ * per-rank slice (q/world columns per row) plus the collective (reduce of the 16 p r-byte slab:
+ * latency + bytes over NVLink) and the root's K2 -- large p shrinks the contraction's row
+ * overhead but grows the slab every rank must reduce. */
+pft_status pft_select_divisor_sharded(pft_table_t t, uint64_t N, uint64_t M, double epsilon, int n_sms,
+                                      int world, uint64_t* p, int* r, double* est_us);
+/* CUDA ordinal a device plan lives on. */
+pft_status pft_dplan_device(pft_dplan_t d, int* device);
+
+/* Status word of a workspace (bit 0 = non-finite output, i.e. non-finite input, since the last
+ * reset).  Synchronises `stream`.  pft_status_query reads the plan's own workspace (executes
+ * with d_ws == NULL, and pft_finalize). */
+pft_status pft_workspace_status(pft_dplan_t d, void* d_ws, void* stream, int* flags, int reset);
 pft_status pft_status_query(pft_dplan_t d, void* stream, int* flags, int reset);
 
 /* End-to-end convenience used by the C++ API and the e2e benchmark: copies h_in
  * (pinned or pageable) H2D, executes, copies the result D2H, synchronises and maps
  * a non-finite flag to PFT_ERR_NON_FINITE.  d_in/d_out are device staging buffers of
- * batch*N and batch*(2M+1) elements (NULL = allocate/free internally). */
+ * batch*N and batch*(2M+1) elements, or NULL: then staging comes from the plan's pool
+ * (allocated on first use, reused, one set per concurrent caller).  Thread-safe: concurrent
+ * calls on one plan use distinct workspaces and status words.  stream NULL = the staging
+ * set's own stream. */
 pft_status pft_execute_host(pft_dplan_t d, const pft_c128* h_in, size_t batch, pft_c128* h_out,
                             pft_c128* d_in, pft_c128* d_out, void* stream);
 

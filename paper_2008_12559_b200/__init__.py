@@ -527,25 +527,31 @@ def device_count() -> int:
     return n.value
 
 
+PASS2 = {"auto": 0, "sum": 1, "k2-fft": 2, "k2-dot": 3, "k2-direct": 4, "k2-l2": 5}  # PFT_PASS2_*
+K2_AT = {"auto": 0, "grid": 1, "tail": 2, "fused": 3}                                 # PFT_K2_AT_*
+EXEC_OVERLAP_PREVIOUS = 1                                                             # PFT_EXEC_*
+
+
 class DevicePlan:
     """A plan uploaded to one B200 (pft_dplan_t).  Device buffers are passed as raw
-    pointers (e.g. torch.Tensor.data_ptr() of complex128 CUDA tensors)."""
+    pointers (e.g. torch.Tensor.data_ptr() of complex128 CUDA tensors).
 
-    def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0, k1_stages: int = 0, k2_mode: int = 0,
-                 k2_ctas: int = 0, pdl: bool = True, fuse: bool = False, reducers: int = 0, batch_hint: int = 1,
-                 k2_tail: int = 0):
+    second_pass: "auto" | "sum" (sum tail in K1) | "k2-fft" | "k2-dot" | "k2-direct" | "k2-l2"
+    k2_at: where the k2-fft form runs: "auto" | "grid" (own launch) | "tail" (K1's last
+    arrivals) | "fused" (K1 behind a grid barrier).  tail_ctas: sum-tail reducers / K2-tail
+    workers per signal (0 = plan).  batch_hint: typical batch per execute."""
+
+    def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0, k1_stages: int = 0, second_pass: str = "auto",
+                 k2_at: str = "auto", tail_ctas: int = 0, k2_grid_ctas: int = 0, batch_hint: int = 1):
         self.plan = plan
         opts = _capi.DPlanOpts()
         opts.device = device
         opts.p2 = p2
         opts.k1_stages = k1_stages
-        opts.reserved[0] = k2_mode  # 0 auto, 1 fft, 2 dot, 3 direct, 4 l2, 5 sum tail (A/B testing)
-        opts.reserved[1] = k2_ctas  # K2 grid width for the L2 form (0 = default)
-        opts.reserved[2] = 0 if pdl else 1  # PDL chaining of consecutive transforms
-        # K2 fused into K1's tail (grid barrier, opt-in); else K2 tail by last arrivals: auto (0),
-        # forced on (k2_tail > 0), off (k2_tail < 0)
-        opts.reserved[3] = 2 if fuse else (3 if k2_tail > 0 else 4 if k2_tail < 0 else 0)
-        opts.reserved[4] = reducers  # sum tail / K2 tail: working CTAs per signal (0 = default)
+        opts.second_pass = PASS2[second_pass]
+        opts.k2_at = K2_AT[k2_at]
+        opts.tail_ctas = tail_ctas
+        opts.k2_grid_ctas = k2_grid_ctas
         opts.batch_hint = batch_hint
         h = C.c_void_p()
         _check(lib().pft_dplan_create(plan.handle, C.byref(opts), C.byref(h)))
@@ -590,9 +596,12 @@ class DevicePlan:
         return self.TAIL_KINDS[n.value]
 
     def execute_ptr(self, d_in: int, d_out: int, batch: int = 1, in_stride: int = 0, d_ws: int = 0,
-                    stream: int = 0) -> None:
-        _check(lib().pft_execute(self._h, C.c_void_p(d_in), batch, in_stride, C.c_void_p(d_out),
-                                 C.c_void_p(d_ws or None), C.c_void_p(stream or None)))
+                    stream: int = 0, overlap: bool = False) -> None:
+        """pft_execute_ex.  overlap=True (PFT_EXEC_OVERLAP_PREVIOUS): K1 may stream while the
+        preceding kernel on the stream finishes; d_in must not be that kernel's output."""
+        _check(lib().pft_execute_ex(self._h, C.c_void_p(d_in), batch, in_stride, C.c_void_p(d_out),
+                                    C.c_void_p(d_ws or None), C.c_void_p(stream or None),
+                                    EXEC_OVERLAP_PREVIOUS if overlap else 0))
 
     def execute_partial_ptr(self, d_in_local: int, d_partial: int, world: int = 1, rank: int = 0,
                             row_stride: int = 0, stream: int = 0) -> None:
@@ -604,9 +613,11 @@ class DevicePlan:
         _check(lib().pft_finalize(self._h, C.c_void_p(d_partial), batch, C.c_void_p(d_out),
                                   C.c_void_p(stream or None)))
 
-    def status(self, stream: int = 0, reset: bool = True) -> int:
+    def status(self, stream: int = 0, reset: bool = True, d_ws: int = 0) -> int:
+        """Non-finite flag word of workspace d_ws (0 = the plan's own workspace)."""
         f = C.c_int()
-        _check(lib().pft_status_query(self._h, C.c_void_p(stream or None), C.byref(f), int(reset)))
+        _check(lib().pft_workspace_status(self._h, C.c_void_p(d_ws or None), C.c_void_p(stream or None), C.byref(f),
+                                          int(reset)))
         return f.value
 
     def execute_host(self, a: np.ndarray, batch: int = 1) -> np.ndarray:

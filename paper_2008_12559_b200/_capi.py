@@ -25,7 +25,8 @@ class PlanInfo(C.Structure):
 
 
 class DPlanOpts(C.Structure):
-    _fields_ = [("device", C.c_int), ("p2", C.c_uint64), ("k1_stages", C.c_int), ("reserved", C.c_int * 6),
+    _fields_ = [("device", C.c_int), ("p2", C.c_uint64), ("k1_stages", C.c_int), ("second_pass", C.c_int),
+                ("k2_at", C.c_int), ("tail_ctas", C.c_int), ("k2_grid_ctas", C.c_int), ("reserved", C.c_int * 2),
                 ("batch_hint", C.c_uint64)]
 
 
@@ -92,6 +93,8 @@ SIGNATURES: dict[str, tuple] = {
     "pft_workspace_bytes": (ST, [P, SZ, C.POINTER(SZ)]),
     "pft_partial_bytes": (ST, [P, SZ, C.POINTER(SZ)]),
     "pft_execute": (ST, [P, P, SZ, SZ, P, P, P]),
+    "pft_execute_ex": (ST, [P, P, SZ, SZ, P, P, P, C.c_uint]),
+    "pft_workspace_status": (ST, [P, P, P, C.POINTER(I), I]),
     "pft_execute_partial": (ST, [P, P, I, I, U64, P, P]),
     "pft_finalize": (ST, [P, P, SZ, P, P]),
     "pft_shard_layout": (ST, [U64, I, I, C.POINTER(ShardInfo)]),
@@ -111,6 +114,13 @@ SIGNATURES: dict[str, tuple] = {
     "pft_anomaly_from_coeffs": (ST, [P, U64, P, U64, U64, P, P, P]),
     "pft_anomaly": (ST, [P, P, U64, P, P, P]),
     "pft_dplan_shape": (ST, [P, C.POINTER(U64), C.POINTER(U64), C.POINTER(I64)]),
+    "pft_dplan_device": (ST, [P, C.POINTER(I)]),
+    "pft_nccl_available": (ST, [C.POINTER(I)]),
+    "pft_nccl_get_unique_id": (ST, [P]),
+    "pft_nccl_comm_init": (ST, [I, I, P, I, C.POINTER(P)]),
+    "pft_nccl_comm_destroy": (ST, [P]),
+    "pft_execute_sharded": (ST, [P, P, U64, P, I, P, P, P]),
+    "pft_select_divisor_sharded": (ST, [P, U64, U64, D, I, I, C.POINTER(U64), C.POINTER(I), PD]),
 }
 
 STATUS_NAMES = {

@@ -16,6 +16,7 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -31,8 +32,9 @@ NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # x86-64-v3 (AVX2/FMA): the library is built here and executed on the GPU box's host.
+CUDA_INC = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(NVCC))), "include")
 HOST_FLAGS = ["-std=c++20", "-O3", "-march=x86-64-v3", "-fPIC", "-fopenmp", "-Wall", "-Wextra",
-              "-Wno-unused-parameter"]
+              "-Wno-unused-parameter", "-I", CUDA_INC]
 NVCC_FLAGS = ["-std=c++20", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-fopenmp",
               "-Xptxas", "-O3", "--expt-relaxed-constexpr"]
 
@@ -84,22 +86,27 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
     _write_table_blob()
     objs: list[Path] = []
+    jobs: list[list] = []
     incs = ["-I", INCLUDE, "-I", CSRC, "-I", BUILD / "gen"]
     for src in sorted((CSRC / "host").glob("*.cpp")):
         obj = BUILD / f"host_{src.stem}_{_deps_hash(src)}.o"
         if force or not obj.exists():
-            _run([CXX, *HOST_FLAGS, *incs, "-c", src, "-o", obj], verbose)
+            jobs.append([CXX, *HOST_FLAGS, *incs, "-c", src, "-o", obj])
         objs.append(obj)
     for src in sorted((CSRC / "device").glob("*.cu")):
         obj = BUILD / f"dev_{src.stem}_{_deps_hash(src)}.o"
         if force or not obj.exists():
-            _run([NVCC, *NVCC_FLAGS, *incs, "-c", src, "-o", obj], verbose)
+            jobs.append([NVCC, *NVCC_FLAGS, *incs, "-c", src, "-o", obj])
         objs.append(obj)
+    # translation units compile concurrently (the kernel instantiations dominate)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(_run, j, verbose) for j in jobs]:
+            f.result()
     stamp = "".join(sorted(o.name for o in objs))
     stamp_file = BUILD / "link.stamp"
     if force or not LIB.exists() or not stamp_file.exists() or stamp_file.read_text() != stamp:
         tmp = LIB.with_suffix(".so.tmp")
-        _run([NVCC, "-shared", *ARCH, "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp"], verbose)
+        _run([NVCC, "-shared", *ARCH, "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp", "-ldl"], verbose)
         os.replace(tmp, LIB)
         stamp_file.write_text(stamp)
     # drop stale objects

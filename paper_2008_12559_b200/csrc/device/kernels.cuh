@@ -68,7 +68,8 @@ enum K2Mode { K2_DIRECT = 0, K2_FFT = 1, K2_DOT = 2, K2_L2 = 3 };
 
 
 struct K2Params {
-    const double2* Y;              // [batch][P1][P2][r]
+    const double2* Y;              // signal b's slab [P1][P2][r] at Y + b * y_stride
+    uint64_t y_stride;             // elements between consecutive signals' slabs
     const double* post_powers;     // [W][r]
     const double2* post_twiddles;  // [W]
     const double2* omega;          // [p]
@@ -84,7 +85,7 @@ struct K2Params {
     uint32_t tl_seq;               // launch sequence number (PFT_TIMELINE instrumentation only)
     FftRadices fft2;               // radices of P2
     double2* out;                  // [batch][W]
-    int* status;
+    int* status;                   // non-finite flag word of the workspace (bit 0)
 };
 
 // Pair-table entry (host-built): phase_l = e^{-2 pi i mu (l - q/2)/N}, t_l = 1 - 2l/q and
@@ -131,16 +132,20 @@ struct K1Params {
     FftRadices fft;             // radices of P1
     uint32_t stages;            // ring depth (K1_MIN_STAGES..K1_MAX_STAGES)
     int pdl;                    // launched with programmatic stream serialization
-    double2* Y;                 // [batch][P1][P2][r] slab, or [batch][P2][W] residue rows (sum_tail)
+    double2* Y;                 // signal b's [P1][P2][r] slab, or [P2][W] residue rows (sum_tail),
+                                // at Y + b * y_stride
+    uint64_t y_stride;          // elements between consecutive signals' data
     int sum_tail;               // sum tail: no slab, no K2 (see k1_sum_tail)
     uint32_t reducers;          // sum tail: the last `reducers` CTAs of a signal reduce its rows
-    unsigned* arrivals;         // sum tail: per signal {tickets, done, ready[P2]} (zeroed once)
+    unsigned* arrivals;         // signal b's control words at arrivals + b * ctl_stride (zeroed once):
+                                // sum tail {tickets, done, ready[P2]}, K2 tail {tickets, done}
+    uint64_t ctl_stride;        // words between consecutive signals' control words
     uint32_t tl_seq;            // launch sequence number (PFT_TIMELINE instrumentation only)
     int k2_tail;                // K2 work done by the last `reducers` CTAs of a signal to write
                                 // their slab (last-arrival, no grid-wide wait; see k1_k2_tail)
     uint32_t k2_group;          // k2_tail: columns j per FFT group (the group's Z + scratch fit the ring)
     int fused;                  // run K2 in K1's tail behind a grid barrier (cooperative launch)
-    unsigned* bar;              // grid-barrier state {count, generation} (workspace tail, zeroed once)
+    unsigned* bar;              // grid-barrier state {count, generation} (workspace header, zeroed once)
     K2Params k2;                // K2 parameters for the fused tail
 };
 
@@ -177,12 +182,14 @@ inline size_t k2_dot_smem_bytes(int r, uint32_t P2) { return sizeof(double2) * (
 cudaError_t configure_k1(int r, uint32_t P1, bool mu0);
 
 int k1_max_active_per_sm(int r, uint32_t P1, uint32_t stages, bool mu0);
-constexpr size_t kBarrierBytes = 256;  // grid-barrier words at the end of a workspace
-// workspace control words after the data: grid barrier (256 B), then the sum tail's
-// arrival counters (`per_signal` words per signal)
-inline size_t ctrl_bytes(size_t batch, size_t per_signal) {
-    return kBarrierBytes + ((4 * per_signal * batch + 255) & ~size_t(255));
-}
+// Workspace layout (zeroed once by the caller; every kernel leaves it re-armed):
+//   [header, 256 B: grid-barrier {count, generation}, status word, unused]
+//   per signal b: [control words, padded to 256 B][data: slab or residue rows, padded to 256 B]
+// A signal's control words and data sit at the same offsets whatever the batch of the call, so a
+// workspace sized for batch B serves any batch <= B (remainder batches).
+constexpr size_t kWsHeaderBytes = 256;
+constexpr size_t kWsStatusOffset = 8;  // bytes into the header
+inline size_t ws_align(size_t b) { return (b + 255) & ~size_t(255); }
 // sum-tail scratch in the (idle) ring after the FFT scratch: twiddle tables, per-warp
 // reducer partials, ticket
 inline size_t k1_sum_scratch_bytes(uint32_t P1, uint32_t P2) {

@@ -138,9 +138,6 @@ uint64_t choose_p2_sum(uint64_t p, int r, int n_sms, size_t batch) {
 // Choose P2 | p (K1 grid = P2 x batch CTAs; P1 = p / P2 is K1's in-CTA FFT length, P2 is
 // K2's).  Prefer decompositions where both FFT passes fit shared memory, then the
 // smallest P2 that still gives >= kTargetCtas CTAs (fewer residue classes = less K2 work).
-// development knob reserved[3]: 2 grid-barrier fusion, 3 K2 tail on, 4 K2 tail off
-int opts_k2_tail(const pft_dplan_opts* o) { return o ? o->reserved[3] : 0; }
-
 uint64_t choose_p2(uint64_t p, int r, size_t batch) {
     const auto divs = divisors(p);
     const size_t nb = std::max<size_t>(batch, 1);
@@ -223,6 +220,59 @@ std::vector<DivisorChoice> rank_divisors_device(const Table& t, uint64_t N, uint
     return all;
 }
 
+// The sharded transform over `world` GPUs (pft_execute_sharded): each rank streams its slice of
+// ceil(pairs / world) column pairs per row (rank 0 also the unpaired columns), the p x r slab
+// (16 p r bytes) is reduced onto the root, and the root runs K2.  Per p:
+//   t = 2 us + max(t_mem, t_fp) over the slice      (the single-GPU K1 terms on q_local columns)
+//     + t_reduce = 15 us + 16 p r (world - 1) / world / 400 GB/s      (NCCL reduce over NVLink)
+//     + t_k2     = 8 us + 32 p r / BW                                  (root: slab read + FFT)
+// Large p shortens the rows each rank streams less than it grows the slab every rank reduces, so
+// the pick is a smaller p than the SPEC cost model's (avoid p = 2^22's 268 MB
+// slab).  world = 1 is the unsharded K1 + K2 pair.
+std::vector<DivisorChoice> rank_divisors_sharded(const Table& t, uint64_t N, uint64_t M, double eps, int n_sms,
+                                                 int world) {
+    if (N <= 1) fail(PFT_ERR_INVALID_ARGUMENT, "select_divisor_sharded: N = 1 has no non-trivial split");
+    if (M > N) fail(PFT_ERR_INVALID_ARGUMENT, "select_divisor_sharded: M > N");
+    if (world < 1) fail(PFT_ERR_INVALID_ARGUMENT, "select_divisor_sharded: world < 1");
+    if (!t.has_eps(eps)) fail(PFT_ERR_EPSILON_NOT_IN_TABLE, "select_divisor_sharded: table has no entries for epsilon");
+    constexpr double BW = 6.6e12, F = 6.6e12, LINK = 400e9;
+    std::vector<DivisorChoice> all;
+    for (uint64_t p : divisors(N)) {
+        if (p <= 1) continue;
+        int r;
+        try {
+            r = min_terms(t, eps, M, p);
+        } catch (const Error& e) {
+            if (e.status == PFT_ERR_RATIO_OUT_OF_RANGE) continue;
+            throw;
+        }
+        const uint64_t q = N / p;
+        if (q < 2) continue;
+        const uint64_t P2 = choose_p2(p, r, 1), P1 = p / P2;
+        if (!k1_feasible(P1, r)) continue;
+        const uint64_t pairs = (q - 1) / 2, lpairs = std::max<uint64_t>(1, (pairs + world - 1) / world);
+        const double ql = 2.0 * static_cast<double>(lpairs) + 2.0;
+        const double rows = static_cast<double>(P1) / (32.0 * static_cast<double>((P1 + 31) / 32));
+        const double pad = 16.0 * static_cast<double>((lpairs + 15) / 16) / static_cast<double>(lpairs);
+        const double bw = std::min(BW, 55e9 * static_cast<double>(std::min<uint64_t>(P2, 2ull * n_sms)));
+        const double elems = static_cast<double>(p) * ql;
+        const double t_mem = 16.0 * elems / bw * pad * (1.0 + 48.0 / ql) / rows;
+        const double t_fp = elems * (3.0 * r + 10.0) / 2.0 / F / rows;
+        const double slab = 16.0 * static_cast<double>(p) * r;
+        const double t_red = world > 1 ? 15e-6 + slab * (world - 1) / world / LINK : 0.0;
+        const double t_k2 = 8e-6 + 2.0 * slab / BW;
+        DivisorChoice c;
+        c.p = p;
+        c.r = r;
+        c.cost = (2e-6 + std::max(t_mem, t_fp) + t_red + t_k2) * 1e6;
+        all.push_back(c);
+    }
+    if (all.empty()) fail(PFT_ERR_RATIO_OUT_OF_RANGE, "select_divisor_sharded: no feasible divisor p");
+    std::stable_sort(all.begin(), all.end(),
+                     [](const DivisorChoice& a, const DivisorChoice& b) { return a.cost < b.cost; });
+    return all;
+}
+
 DivisorChoice select_divisor_device(const Table& t, uint64_t N, uint64_t M, double eps, int n_sms) {
     return rank_divisors_device(t, N, M, eps, n_sms).front();
 }
@@ -238,7 +288,6 @@ struct pft_dplan_s {
     uint32_t k1_stages = pftdev::K1_MIN_STAGES;
     int k2_mode = pftdev::K2_DIRECT;
     uint32_t k2_ctas = 0;
-    bool pdl_chain = true;  // K2 releases the next K1 early (programmatic dependent launch)
     bool allow_fuse = false; // K2 fused into K1's tail (opt-in; measured slower at C2b/C4)
     bool sum_tail = false;   // unsharded execute: K1 sum tail, no K2 (few output bins)
     bool k2_tail = false;    // unsharded execute: K2's work by K1's last arrivals (many bins)
@@ -256,27 +305,66 @@ struct pft_dplan_s {
     double2* d_omega = nullptr;
     double* d_post_powers = nullptr;
     double2* d_post_twiddles = nullptr;
-    double2* d_ws = nullptr;  // batch-1 workspace
-    int* d_status = nullptr;
+    void* d_ws = nullptr;  // the plan's own batch-1 workspace (executes with d_ws == NULL, finalize)
+
+    // Staging sets of pft_execute_host: device input/output buffers, a workspace and a stream,
+    // allocated on first use and reused; one set per concurrent caller (SPEC.md:263-265:
+    // concurrent executes on one plan), so no call allocates in the steady state.
+    struct Staging {
+        size_t batch = 0;
+        double2 *din = nullptr, *dout = nullptr;
+        void* ws = nullptr;
+        cudaStream_t st = nullptr;
+    };
+    std::mutex staging_mu;
+    std::vector<Staging*> staging_free;
+    std::vector<Staging*> staging_all;
 
     ~pft_dplan_s() {
-        if (tables) {
-            int prev = 0;
-            cudaGetDevice(&prev);
-            cudaSetDevice(device);
-            cudaFree(tables);
-            cudaFree(d_ws);
-            cudaFree(d_status);
-            cudaSetDevice(prev);
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        for (Staging* s : staging_all) {
+            cudaFree(s->din);
+            cudaFree(s->dout);
+            cudaFree(s->ws);
+            if (s->st) cudaStreamDestroy(s->st);
+            delete s;
         }
+        if (tables) cudaFree(tables);
+        if (d_ws) cudaFree(d_ws);
+        cudaSetDevice(prev);
     }
 
     size_t slab_elems() const { return (size_t)host.p * host.r; }
     size_t counters_per_signal() const { return sum_tail ? P2 + 2 : k2_tail ? 2 : 0; }
     size_t data_elems() const { return sum_tail ? std::max<size_t>(slab_elems(), (size_t)P2 * W) : slab_elems(); }
+    // workspace layout (kernels.cuh): header, then per signal {control words, data}
+    size_t ctl_bytes() const { return pftdev::ws_align(4 * counters_per_signal()); }
+    size_t signal_bytes() const { return ctl_bytes() + pftdev::ws_align(data_elems() * sizeof(double2)); }
     size_t workspace_bytes(size_t batch) const {
-        return data_elems() * sizeof(double2) * batch + pftdev::ctrl_bytes(batch, counters_per_signal());
+        return pftdev::kWsHeaderBytes + std::max<size_t>(batch, 1) * signal_bytes();
     }
+    struct WsView {
+        unsigned* bar;       // grid barrier {count, generation}
+        int* status;         // non-finite flag word
+        unsigned* arrivals;  // signal 0's control words
+        double2* Y;          // signal 0's data
+        uint64_t y_stride;   // elements per signal block
+        uint64_t ctl_stride; // words per signal block
+    };
+    WsView ws_view(void* base) const {
+        char* b = static_cast<char*>(base);
+        WsView v;
+        v.bar = reinterpret_cast<unsigned*>(b);
+        v.status = reinterpret_cast<int*>(b + pftdev::kWsStatusOffset);
+        v.arrivals = reinterpret_cast<unsigned*>(b + pftdev::kWsHeaderBytes);
+        v.Y = reinterpret_cast<double2*>(b + pftdev::kWsHeaderBytes + ctl_bytes());
+        v.y_stride = signal_bytes() / sizeof(double2);
+        v.ctl_stride = signal_bytes() / sizeof(unsigned);
+        return v;
+    }
+    int* own_status() const { return ws_view(d_ws).status; }
     bool fused(size_t batch) const {
         return allow_fuse && !sum_tail && k2_mode == pftdev::K2_FFT &&
                pftdev::k2_smem_bytes(host.r, (uint32_t)P2) <= (size_t)k1_stages * pftdev::k1_stage_bytes(host.r) &&
@@ -284,7 +372,7 @@ struct pft_dplan_s {
     }
 
     pftdev::K1Params k1_params(const ShardLayout& v, const double2* a, uint64_t row_stride, size_t batch_stride,
-                               double2* Y) const {
+                               double2* Y, uint64_t y_stride, bool pdl) const {
         pftdev::K1Params P{};
         P.a = a;
         P.row_stride = row_stride;
@@ -305,14 +393,16 @@ struct pft_dplan_s {
         P.P2 = (uint32_t)P2;
         P.fft = fft;
         P.stages = k1_stages;
-        P.pdl = pdl_chain ? 1 : 0;
+        P.pdl = pdl ? 1 : 0;
         P.Y = Y;
+        P.y_stride = y_stride;
         return P;
     }
 
-    pftdev::K2Params k2_params(const double2* Y, double2* out) const {
+    pftdev::K2Params k2_params(const double2* Y, uint64_t y_stride, double2* out, int* status) const {
         pftdev::K2Params P{};
         P.Y = Y;
+        P.y_stride = y_stride;
         P.post_powers = d_post_powers;
         P.post_twiddles = d_post_twiddles;
         P.omega = d_omega;
@@ -326,10 +416,10 @@ struct pft_dplan_s {
         P.inv_p = 1.0 / (double)host.p;
         P.mode = k2_mode;
         P.k2_ctas = k2_ctas;
-        P.release_next = pdl_chain ? 1 : 0;
+        P.release_next = 1;  // a following K1 only streams early when its execute asked for it
         P.fft2 = fft2;
         P.out = out;
-        P.status = d_status;
+        P.status = status;
         return P;
     }
 };
@@ -391,20 +481,23 @@ CUtensorMap make_input_map(const pft_dplan_s* d, const void* base, uint64_t row_
     return map;
 }
 
-// Y: workspace of workspace_bytes(batch) (slab then the zero-initialised barrier words).
-void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stride, double2* out, double2* Y,
-                 cudaStream_t st) {
+// ws: a workspace of workspace_bytes(>= batch) bytes (header + per-signal blocks, zeroed once).
+// pdl: K1 may start streaming before the preceding kernel on `st` completes
+// (PFT_EXEC_OVERLAP_PREVIOUS: the caller guarantees `in` is not that kernel's output).
+void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stride, double2* out, void* ws,
+                 cudaStream_t st, bool pdl) {
     const ShardLayout v = shard_layout(d->host.q, 1, 0);
     const CUtensorMap map = make_input_map(d, in, v.row_len, d->host.q, batch, in_stride);
-    auto P1 = d->k1_params(v, in, d->host.q, in_stride, Y);
-    auto P2 = d->k2_params(Y, out);
+    const pft_dplan_s::WsView w = d->ws_view(ws);
+    auto P1 = d->k1_params(v, in, d->host.q, in_stride, w.Y, w.y_stride, pdl);
+    auto P2 = d->k2_params(w.Y, w.y_stride, out, w.status);
     static std::atomic<uint32_t> seq{0};  // PFT_TIMELINE ring index
     P1.tl_seq = P2.tl_seq = seq.fetch_add(1, std::memory_order_relaxed);
+    P1.arrivals = w.arrivals;
+    P1.ctl_stride = w.ctl_stride;
     if (d->sum_tail) {
         P1.sum_tail = 1;
         P1.reducers = d->reducers;
-        P1.arrivals = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(Y + d->data_elems() * batch) +
-                                                  pftdev::kBarrierBytes);
         P1.k2 = P2;
         cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
         return;
@@ -413,15 +506,13 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
         P1.k2_tail = 1;
         P1.k2_group = d->k2_group;
         P1.reducers = d->reducers;
-        P1.arrivals = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(Y + d->data_elems() * batch) +
-                                                  pftdev::kBarrierBytes);
         P1.k2 = P2;
         cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 (K2 tail) launch");
         return;
     }
     if (d->fused(batch)) {
         P1.fused = 1;
-        P1.bar = reinterpret_cast<unsigned*>(Y + d->data_elems() * batch);
+        P1.bar = w.bar;
         P1.k2 = P2;
         cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 (fused) launch");
         return;
@@ -445,6 +536,25 @@ pft_status pft_select_divisor_device(pft_table_t t, uint64_t N, uint64_t M, doub
     if (p) *p = c.p;
     if (r) *r = c.r;
     if (est_us) *est_us = c.cost;
+    PFT_API_END
+}
+
+pft_status pft_select_divisor_sharded(pft_table_t t, uint64_t N, uint64_t M, double eps, int n_sms, int world,
+                                      uint64_t* p, int* r, double* est_us) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(t != nullptr, "null table handle");
+    PFT_REQUIRE(n_sms > 0, "n_sms must be positive");
+    const DivisorChoice c = rank_divisors_sharded(t->table, N, M, eps, n_sms, world).front();
+    if (p) *p = c.p;
+    if (r) *r = c.r;
+    if (est_us) *est_us = c.cost;
+    PFT_API_END
+}
+
+pft_status pft_dplan_device(pft_dplan_t d, int* device) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(d != nullptr && device != nullptr, "dplan_device: bad arguments");
+    *device = d->device;
     PFT_API_END
 }
 
@@ -495,18 +605,20 @@ pft_status pft_autotune_divisor(pft_table_t t, uint64_t N, uint64_t M, int64_t m
         if (pft_dplan_create(&hp, &o, &dpl) != PFT_OK) continue;  // infeasible decomposition
         std::unique_ptr<pft_dplan_s> guard_plan(dpl);
         const auto* in = reinterpret_cast<const double2*>(d_in);
-        double2* ws = dpl->d_ws;
+        void* ws = dpl->d_ws;
         if (batch > 1) {
             if (res.ws) cudaFree(res.ws);
             res.ws = nullptr;
             const size_t wb = dpl->workspace_bytes(batch);
             cuda_check(cudaMalloc(&res.ws, wb), "cudaMalloc(workspace)");
             cuda_check(cudaMemset(res.ws, 0, wb), "cudaMemset(workspace)");
-            ws = static_cast<double2*>(res.ws);
+            ws = res.ws;
         }
-        for (int w = 0; w < 3; ++w) run_execute(dpl, in, batch, N, res.out, ws, res.st);
+        // the same input every time (never written by the previous execute): PDL overlap on,
+        // as in a stream of independent transforms
+        for (int w = 0; w < 3; ++w) run_execute(dpl, in, batch, N, res.out, ws, res.st, true);
         cuda_check(cudaEventRecord(res.e0, res.st), "cudaEventRecord");
-        for (int k = 0; k < reps; ++k) run_execute(dpl, in, batch, N, res.out, ws, res.st);
+        for (int k = 0; k < reps; ++k) run_execute(dpl, in, batch, N, res.out, ws, res.st, true);
         cuda_check(cudaEventRecord(res.e1, res.st), "cudaEventRecord");
         cuda_check(cudaEventSynchronize(res.e1), "cudaEventSynchronize");
         float ms = 0.f;
@@ -559,15 +671,21 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     d->host.achieved_epsilon = H.achieved_epsilon;
     d->host.plan_id = H.plan_id;
     d->W = 2 * H.M + 1;
-    const int forced_mode = opts ? opts->reserved[0] : 0;
+    PFT_REQUIRE(!opts || (opts->reserved[0] == 0 && opts->reserved[1] == 0), "dplan_create: reserved options must be 0");
+    const int pass2 = opts ? opts->second_pass : PFT_PASS2_AUTO;
+    const int k2_at = opts ? opts->k2_at : PFT_K2_AT_AUTO;
+    PFT_REQUIRE(pass2 >= PFT_PASS2_AUTO && pass2 <= PFT_PASS2_K2_L2, "dplan_create: unknown second_pass");
+    PFT_REQUIRE(k2_at >= PFT_K2_AT_AUTO && k2_at <= PFT_K2_AT_FUSED, "dplan_create: unknown k2_at");
+    PFT_REQUIRE(!opts || (opts->tail_ctas >= 0 && opts->k2_grid_ctas >= 0), "dplan_create: negative CTA count");
+    const int tail_ctas = opts ? opts->tail_ctas : 0;
     uint64_t p2 = opts && opts->p2 ? opts->p2 : 0;
     const size_t batch_hint = opts && opts->batch_hint > 1 ? (size_t)opts->batch_hint : 1;
-    if (!p2 && (forced_mode == 0 || forced_mode == 5)) {  // sum tail, when it pays (or forced)
+    if (!p2 && (pass2 == PFT_PASS2_AUTO || pass2 == PFT_PASS2_SUM_TAIL)) {  // sum tail, when it pays (or forced)
         p2 = choose_p2_sum(H.p, H.r, prop.multiProcessorCount, batch_hint);
         // batched plans (batch_hint > 1) always take the sum tail when it fits: a K2 grid of
         // P1 x batch CTAs was 2.5-16x slower at every batched shape measured
         // (tools/probe_cols.py: 129 x 4096, M = 64: 31 vs 12 us; 513 x 1024, M = 32: 92 vs 11 us)
-        if (p2 && forced_mode == 0 && batch_hint <= 1 && !sum_tail_pays(H.N, d->W, p2, H.r)) p2 = 0;
+        if (p2 && pass2 == PFT_PASS2_AUTO && batch_hint <= 1 && !sum_tail_pays(H.N, d->W, p2, H.r)) p2 = 0;
     }
     if (!p2) p2 = choose_p2(H.p, H.r, batch_hint);
     if (p2 == 0 || H.p % p2 != 0) fail(PFT_ERR_INVALID_ARGUMENT, "dplan_create: p2 must divide p");
@@ -586,17 +704,16 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     {
         const bool fft_ok = k2_fft_feasible(d->P2, H.r);
         const bool dot_ok = pftdev::k2_dot_smem_bytes(H.r, (uint32_t)d->P2) <= kK2SmemLimit;
-        const int forced = opts ? opts->reserved[0] : 0;  // 1 fft, 2 dot, 3 direct, 4 l2, 5 sum tail (A/B)
         // L2 form when there are few output bins per m1 (W <= 2 P1, e.g. C1); it needs no shared
         // memory and parks beside K1 under PDL.  Otherwise the FFT form (the L2 form is
         // latency-bound at C2b/C4's 2049 / 2001 bins) -- unless the sum tail below applies
         // (measured C2b 49 vs 54 us, C4 35 vs 45 us per transform).
         const bool l2_ok = d->P2 <= 1024 && double(d->W) * d->P2 <= 64.0 * 1024 * 1024;
-        if (forced == 1 && fft_ok) d->k2_mode = pftdev::K2_FFT;
-        else if (forced == 2 && dot_ok) d->k2_mode = pftdev::K2_DOT;
-        else if (forced == 3) d->k2_mode = pftdev::K2_DIRECT;
-        else if (forced == 4) d->k2_mode = pftdev::K2_L2;
-        else if (forced == 5) d->k2_mode = pftdev::K2_FFT;  // with the sum tail below
+        if (pass2 == PFT_PASS2_K2_FFT && fft_ok) d->k2_mode = pftdev::K2_FFT;
+        else if (pass2 == PFT_PASS2_K2_DOT && dot_ok) d->k2_mode = pftdev::K2_DOT;
+        else if (pass2 == PFT_PASS2_K2_DIRECT) d->k2_mode = pftdev::K2_DIRECT;
+        else if (pass2 == PFT_PASS2_K2_L2) d->k2_mode = pftdev::K2_L2;
+        else if (pass2 == PFT_PASS2_SUM_TAIL) d->k2_mode = pftdev::K2_FFT;  // with the sum tail below
         else if (l2_ok && d->W <= 2 * d->P1) d->k2_mode = pftdev::K2_L2;  // few bins per m1 (C1)
         else if (fft_ok) d->k2_mode = pftdev::K2_FFT;
         else if (dot_ok) d->k2_mode = pftdev::K2_DOT;
@@ -606,29 +723,28 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
             else d->fft2.n = 1;
         }
         // K2 CTAs (each loops over m1): few enough to all be resident beside K1 (opts override)
-        d->k2_ctas = opts && opts->reserved[1] > 0 ? (uint32_t)opts->reserved[1] : 0;
-        d->pdl_chain = !(opts && opts->reserved[2] == 1);  // reserved[2] == 1: plain stream order
-        d->allow_fuse = opts && opts->reserved[3] == 2;
+        d->k2_ctas = opts && opts->k2_grid_ctas > 0 ? (uint32_t)opts->k2_grid_ctas : 0;
+        d->allow_fuse = k2_at == PFT_K2_AT_FUSED;
         // Sum tail when it pays (sum_tail_pays): K1 finishes the transform itself (see
         // k1_sum_tail).  Needs the ring to hold the FFT scratch and the tail scratch.  Forced
-        // off by modes 1-4, forced on (if feasible) by 5.
+        // off by the K2 forms, forced on (if feasible) by PFT_PASS2_SUM_TAIL.
         const bool fits = sizeof(double2) * H.r * d->P1 +
                               pftdev::k1_sum_scratch_bytes((uint32_t)d->P1, (uint32_t)d->P2) <=
                           pftdev::k1_min_ring_bytes(H.r);
-        d->sum_tail = fits && (forced == 5 || (forced == 0 && (batch_hint > 1 || sum_tail_pays(H.N, d->W, d->P2, H.r))));
+        d->sum_tail = fits && (pass2 == PFT_PASS2_SUM_TAIL ||
+                               (pass2 == PFT_PASS2_AUTO && (batch_hint > 1 || sum_tail_pays(H.N, d->W, d->P2, H.r))));
         // reducing CTAs per signal: one per 64 outputs (measured best at C2b/C4: 32; more
         // reducers hold more SM slots from the next transform), opts override
         d->reducers = (uint32_t)std::min<uint64_t>(d->P2, std::max<uint64_t>(1, (d->W + 63) / 64));
-        if (opts && opts->reserved[4] > 0) d->reducers = (uint32_t)std::min<uint64_t>(d->P2, opts->reserved[4]);
+        if (tail_ctas > 0) d->reducers = (uint32_t)std::min<uint64_t>(d->P2, (uint64_t)tail_ctas);
         // Last-arrival K2 tail (k1_k2_tail) when K2 takes the FFT form and the tail is short
         // against the stream: the columns go through the FFT in groups whose Z + scratch fit
         // the ring.  Workers hold their SM slots, and a K1 CTA of the next transform that starts
         // late finishes late (each CTA streams a fixed 1/P2 of the input), so the tail's m1
         // rounds (~15 us each beside a streaming CTA, PFT_TIMELINE at C2c) must stay <= 10% of
         // the stream: C5 (2^30) gains 6% (3099 -> 2907 us), C2c (2^24, 2 rounds) loses (67 -> 77
-        // us at 1 round).  reserved[3]: 3 forces it on (if feasible), 4 off (separate K2 grid).
-        const int want_tail = opts_k2_tail(opts);
-        if (!d->sum_tail && d->k2_mode == pftdev::K2_FFT && !d->allow_fuse && want_tail != 4 &&
+        // us at 1 round).  k2_at: PFT_K2_AT_TAIL forces it on (if feasible), _GRID off.
+        if (!d->sum_tail && d->k2_mode == pftdev::K2_FFT && !d->allow_fuse && k2_at != PFT_K2_AT_GRID &&
             pftdev::k1_k2_tail_instantiated(H.r)) {
             const size_t ring = (size_t)d->k1_stages * pftdev::k1_stage_bytes(H.r);
             const size_t fixed = pftdev::k1_k2_tail_bytes(0, (uint32_t)d->P2);
@@ -640,11 +756,11 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
                 d->k2_tail = true;
                 // workers per signal: all m1 in one round when P1 is small, else 64 (opts override)
                 d->reducers = (uint32_t)std::min<uint64_t>(d->P1, std::min<uint64_t>(d->P2, 64));
-                if (opts && opts->reserved[4] > 0)
-                    d->reducers = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(d->P1, d->P2), opts->reserved[4]);
+                if (tail_ctas > 0)
+                    d->reducers = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(d->P1, d->P2), (uint64_t)tail_ctas);
                 const double rounds = (double)((d->P1 + d->reducers - 1) / d->reducers);
                 const double stream_us = 16.0 * (double)H.N * (double)batch_hint / 6.5e6;
-                if (want_tail != 3 && rounds * 15.0 > 0.10 * stream_us) d->k2_tail = false;
+                if (k2_at != PFT_K2_AT_TAIL && rounds * 15.0 > 0.10 * stream_us) d->k2_tail = false;
             }
         }
     }
@@ -714,17 +830,22 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     cuda_check(pftdev::configure_k1(H.r, (uint32_t)d->P1, d->mu0), "configure K1 (early)");
     cuda_check(cudaMalloc(&d->d_ws, d->workspace_bytes(1)), "cudaMalloc(workspace)");
     cuda_check(cudaMemset(d->d_ws, 0, d->workspace_bytes(1)), "cudaMemset(workspace)");
-    cuda_check(cudaMalloc(&d->d_status, sizeof(int)), "cudaMalloc(status)");
-    cuda_check(cudaMemset(d->d_status, 0, sizeof(int)), "cudaMemset(status)");
     cuda_check(pftdev::configure_k1(H.r, (uint32_t)d->P1, d->mu0), "configure K1");
     cuda_check(pftdev::configure_k2(H.r, (uint32_t)d->P2), "configure K2");
     d->k1_capacity = (uint64_t)pftdev::k1_max_active_per_sm(H.r, (uint32_t)d->P1, d->k1_stages, d->mu0) *
                      (uint64_t)prop.multiProcessorCount;
-    // Reducers hold their SM slots until the last row of the signal lands; more of them than
-    // the slots a transform leaves free (capacity - P2) delays the next transform's K1 CTAs
-    // (measured: 40 reducers 46.4 us, 48 reducers 53.9 us per transform at C2b).
-    if (d->sum_tail && !(opts && opts->reserved[4] > 0) && d->k1_capacity > d->P2)
-        d->reducers = (uint32_t)std::min<uint64_t>(d->reducers, d->k1_capacity - d->P2);
+    // Reducers (sum tail) and K2-tail workers hold their SM slots while they wait for the rest
+    // of their signal's CTAs.  Forward progress needs a free slot for those CTAs: with CTAs
+    // dispatched in launch order only the highest signal in flight can have undispatched CTAs,
+    // and its waiting CTAs number at most `reducers`, so reducers < capacity suffices (a PDL
+    // dependent grid gets slots only after every CTA of this grid has been dispatched).  The
+    // sum tail also keeps them within the slots a transform leaves free (capacity - P2):
+    // measured 40 reducers 46.4 us, 48 reducers 53.9 us per transform at C2b.  Caller overrides
+    // (tail_ctas) are capped the same way.
+    if (d->k1_capacity > 1) {
+        const uint64_t cap = d->sum_tail && d->k1_capacity > d->P2 ? d->k1_capacity - d->P2 : d->k1_capacity - 1;
+        d->reducers = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(d->reducers, cap));
+    }
     *out = d.release();
     PFT_API_END
 }
@@ -777,24 +898,30 @@ pft_status pft_dplan_tail_kind(pft_dplan_t d, int* kind) {
     PFT_API_END
 }
 
-pft_status pft_execute(pft_dplan_t dh, const pft_c128* d_in, size_t batch, size_t in_stride, pft_c128* d_out,
-                       void* d_ws, void* stream) {
+pft_status pft_execute_ex(pft_dplan_t dh, const pft_c128* d_in, size_t batch, size_t in_stride, pft_c128* d_out,
+                          void* d_ws, void* stream, unsigned flags) {
     PFT_API_BEGIN
     pft_dplan_s* d = dp(dh);
     if (batch == 0) return PFT_OK;
     PFT_REQUIRE(d_in && d_out, "execute: null buffer");
     PFT_REQUIRE(batch <= 65535, "execute: batch > 65535 per call");
+    PFT_REQUIRE((flags & ~PFT_EXEC_OVERLAP_PREVIOUS) == 0, "execute: unknown flags");
     if (in_stride == 0) in_stride = d->host.N;
     PFT_REQUIRE(in_stride >= d->host.N || batch == 1, "execute: in_stride < N");
-    double2* Y = static_cast<double2*>(d_ws);
-    if (!Y) {
+    void* ws = d_ws;
+    if (!ws) {
         PFT_REQUIRE(batch == 1, "execute: batch > 1 needs a caller workspace (pft_workspace_bytes)");
-        Y = d->d_ws;
+        ws = d->d_ws;
     }
     DeviceGuard guard(d->device);
-    run_execute(d, reinterpret_cast<const double2*>(d_in), batch, in_stride, reinterpret_cast<double2*>(d_out), Y,
-                static_cast<cudaStream_t>(stream));
+    run_execute(d, reinterpret_cast<const double2*>(d_in), batch, in_stride, reinterpret_cast<double2*>(d_out), ws,
+                static_cast<cudaStream_t>(stream), (flags & PFT_EXEC_OVERLAP_PREVIOUS) != 0);
     PFT_API_END
+}
+
+pft_status pft_execute(pft_dplan_t dh, const pft_c128* d_in, size_t batch, size_t in_stride, pft_c128* d_out,
+                       void* d_ws, void* stream) {
+    return pft_execute_ex(dh, d_in, batch, in_stride, d_out, d_ws, stream, PFT_EXEC_DEFAULT);
 }
 
 // ------------------------------------------------------------------ 2-D PFT
@@ -820,6 +947,17 @@ Ws2d ws2d(const pft_dplan_s* rows, const pft_dplan_s* cols) {
     w.total = w.rows_ws + w.cols_ws + w.x + w.xt + w.z;
     return w;
 }
+
+int read_status(const int* d_status, bool reset, cudaStream_t st) {
+    int f = 0;
+    cuda_check(cudaMemcpyAsync(&f, d_status, sizeof(int), cudaMemcpyDeviceToHost, st), "read status");
+    cuda_check(cudaStreamSynchronize(st), "stream synchronize");
+    if (reset && f) {
+        cuda_check(cudaMemsetAsync(const_cast<int*>(d_status), 0, sizeof(int), st), "reset status");
+        cuda_check(cudaStreamSynchronize(st), "stream synchronize");
+    }
+    return f;
+}
 }  // namespace
 
 pft_status pft_workspace_bytes_2d(pft_dplan_t rows, pft_dplan_t cols, size_t* bytes) {
@@ -842,16 +980,16 @@ pft_status pft_execute_2d(pft_dplan_t rows_h, pft_dplan_t cols_h, const pft_c128
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const Ws2d w = ws2d(rows, cols);
     char* base = static_cast<char*>(d_ws);
-    double2* ws_rows = reinterpret_cast<double2*>(base);
-    double2* ws_cols = reinterpret_cast<double2*>(base + w.rows_ws);
+    void* ws_rows = base;
+    void* ws_cols = base + w.rows_ws;
     double2* X = reinterpret_cast<double2*>(base + w.rows_ws + w.cols_ws);
     double2* XT = reinterpret_cast<double2*>(base + w.rows_ws + w.cols_ws + w.x);
     double2* Z = reinterpret_cast<double2*>(base + w.rows_ws + w.cols_ws + w.x + w.xt);
     // axis 2: every row (contiguous, length N2) -> X[n1][m2]
-    run_execute(rows, reinterpret_cast<const double2*>(d_in), N1, N2, X, ws_rows, st);
+    run_execute(rows, reinterpret_cast<const double2*>(d_in), N1, N2, X, ws_rows, st, false);
     cuda_check(pftdev::launch_transpose(X, XT, N1, W2, st), "transpose");
     // axis 1: every column of X (now a contiguous row of X^T, length N1) -> Z[m2][m1]
-    run_execute(cols, XT, W2, N1, Z, ws_cols, st);
+    run_execute(cols, XT, W2, N1, Z, ws_cols, st, false);
     cuda_check(pftdev::launch_transpose(Z, reinterpret_cast<double2*>(d_out), W2, W1, st), "transpose");
     PFT_API_END
 }
@@ -863,32 +1001,30 @@ pft_status pft_execute_2d_host(pft_dplan_t rows_h, pft_dplan_t cols_h, const pft
     PFT_REQUIRE(h_in && h_out, "execute_2d_host: null host buffer");
     DeviceGuard guard(rows->device);
     const size_t n_in = cols->host.N * rows->host.N, n_out = cols->W * rows->W;
-    const size_t wb = ws2d(rows, cols).total;
+    const Ws2d w2 = ws2d(rows, cols);
     struct Bufs {
         void *in = nullptr, *out = nullptr, *ws = nullptr;
+        cudaStream_t st = nullptr;
         ~Bufs() {
+            if (st) cudaStreamDestroy(st);
             cudaFree(in);
             cudaFree(out);
             cudaFree(ws);
         }
     } b;
+    cuda_check(cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaMalloc(&b.in, n_in * sizeof(pft_c128)), "cudaMalloc(input)");
     cuda_check(cudaMalloc(&b.out, n_out * sizeof(pft_c128)), "cudaMalloc(output)");
-    cuda_check(cudaMalloc(&b.ws, wb), "cudaMalloc(workspace)");
-    cuda_check(cudaMemset(b.ws, 0, wb), "cudaMemset(workspace)");
-    cuda_check(cudaMemcpy(b.in, h_in, n_in * sizeof(pft_c128), cudaMemcpyHostToDevice), "H2D input");
+    cuda_check(cudaMalloc(&b.ws, w2.total), "cudaMalloc(workspace)");
+    cuda_check(cudaMemsetAsync(b.ws, 0, w2.total, b.st), "cudaMemset(workspace)");
+    cuda_check(cudaMemcpyAsync(b.in, h_in, n_in * sizeof(pft_c128), cudaMemcpyHostToDevice, b.st), "H2D input");
     const pft_status s = pft_execute_2d(rows_h, cols_h, static_cast<const pft_c128*>(b.in),
-                                        static_cast<pft_c128*>(b.out), b.ws, nullptr);
+                                        static_cast<pft_c128*>(b.out), b.ws, b.st);
     if (s != PFT_OK) return s;
-    cuda_check(cudaMemcpy(h_out, b.out, n_out * sizeof(pft_c128), cudaMemcpyDeviceToHost), "D2H output");
-    int f1 = 0, f2 = 0;
-    cuda_check(cudaMemcpy(&f1, rows->d_status, sizeof(int), cudaMemcpyDeviceToHost), "read status");
-    cuda_check(cudaMemcpy(&f2, cols->d_status, sizeof(int), cudaMemcpyDeviceToHost), "read status");
-    if (f1 || f2) {
-        cudaMemset(rows->d_status, 0, sizeof(int));
-        cudaMemset(cols->d_status, 0, sizeof(int));
-        fail(PFT_ERR_NON_FINITE, "execute_2d: non-finite input entries (non-finite output detected)");
-    }
+    cuda_check(cudaMemcpyAsync(h_out, b.out, n_out * sizeof(pft_c128), cudaMemcpyDeviceToHost, b.st), "D2H output");
+    const int f1 = read_status(rows->ws_view(b.ws).status, false, b.st);
+    const int f2 = read_status(cols->ws_view(static_cast<char*>(b.ws) + w2.rows_ws).status, false, b.st);
+    if (f1 || f2) fail(PFT_ERR_NON_FINITE, "execute_2d: non-finite input entries (non-finite output detected)");
     PFT_API_END
 }
 
@@ -903,7 +1039,7 @@ pft_status pft_execute_partial(pft_dplan_t dh, const pft_c128* d_in_local, int w
     DeviceGuard guard(d->device);
     const CUtensorMap map = make_input_map(d, d_in_local, v.row_len, row_stride, 1, 0);
     const auto P = d->k1_params(v, reinterpret_cast<const double2*>(d_in_local), row_stride, 0,
-                                reinterpret_cast<double2*>(d_partial));
+                                reinterpret_cast<double2*>(d_partial), d->slab_elems(), false);
     cuda_check(pftdev::launch_k1(map, P, d->host.r, 1, d->mu0, static_cast<cudaStream_t>(stream)), "K1 launch");
     PFT_API_END
 }
@@ -914,21 +1050,23 @@ pft_status pft_finalize(pft_dplan_t dh, const pft_c128* d_partial, size_t batch,
     if (batch == 0) return PFT_OK;
     PFT_REQUIRE(d_partial && d_out, "finalize: null buffer");
     DeviceGuard guard(d->device);
-    const auto P = d->k2_params(reinterpret_cast<const double2*>(d_partial), reinterpret_cast<double2*>(d_out));
+    const auto P = d->k2_params(reinterpret_cast<const double2*>(d_partial), d->slab_elems(),
+                                reinterpret_cast<double2*>(d_out), d->own_status());
     cuda_check(pftdev::launch_k2(P, d->host.r, (uint32_t)batch, static_cast<cudaStream_t>(stream)), "K2 launch");
     PFT_API_END
 }
 
-pft_status pft_status_query(pft_dplan_t dh, void* stream, int* flags, int reset) {
+pft_status pft_workspace_status(pft_dplan_t dh, void* d_ws, void* stream, int* flags, int reset) {
     PFT_API_BEGIN
     pft_dplan_s* d = dp(dh);
     PFT_REQUIRE(flags != nullptr, "flags is null");
     DeviceGuard guard(d->device);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cuda_check(cudaStreamSynchronize(st), "stream synchronize");
-    cuda_check(cudaMemcpy(flags, d->d_status, sizeof(int), cudaMemcpyDeviceToHost), "read status");
-    if (reset) cuda_check(cudaMemset(d->d_status, 0, sizeof(int)), "reset status");
+    *flags = read_status(d->ws_view(d_ws ? d_ws : d->d_ws).status, reset != 0, static_cast<cudaStream_t>(stream));
     PFT_API_END
+}
+
+pft_status pft_status_query(pft_dplan_t dh, void* stream, int* flags, int reset) {
+    return pft_workspace_status(dh, nullptr, stream, flags, reset);
 }
 
 pft_status pft_execute_host(pft_dplan_t dh, const pft_c128* h_in, size_t batch, pft_c128* h_out, pft_c128* d_in,
@@ -937,45 +1075,50 @@ pft_status pft_execute_host(pft_dplan_t dh, const pft_c128* h_in, size_t batch, 
     pft_dplan_s* d = dp(dh);
     if (batch == 0) return PFT_OK;
     PFT_REQUIRE(h_in && h_out, "execute_host: null host buffer");
+    PFT_REQUIRE(batch <= 65535, "execute_host: batch > 65535 per call");
     DeviceGuard guard(d->device);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t n_in = d->host.N * batch, n_out = d->W * batch;
-    pft_c128* din = d_in;
-    pft_c128* dout = d_out;
-    double2* ws = nullptr;
-    bool own_in = false, own_out = false;
-    struct Cleanup {
-        pft_c128*& a; pft_c128*& b; double2*& w; bool& oa; bool& ob;
-        ~Cleanup() {
-            if (oa) cudaFree(a);
-            if (ob) cudaFree(b);
-            if (w) cudaFree(w);
+    // check a staging set out of the plan's pool (or allocate one): its workspace and status
+    // word are this call's alone
+    pft_dplan_s::Staging* sg = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(d->staging_mu);
+        for (size_t i = 0; i < d->staging_free.size(); ++i)
+            if (d->staging_free[i]->batch >= batch) {
+                sg = d->staging_free[i];
+                d->staging_free.erase(d->staging_free.begin() + (std::ptrdiff_t)i);
+                break;
+            }
+    }
+    if (!sg) {
+        auto fresh = std::make_unique<pft_dplan_s::Staging>();
+        fresh->batch = batch;
+        cuda_check(cudaStreamCreateWithFlags(&fresh->st, cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaMalloc(&fresh->ws, d->workspace_bytes(batch)), "cudaMalloc(workspace)");
+        cuda_check(cudaMemsetAsync(fresh->ws, 0, d->workspace_bytes(batch), fresh->st), "cudaMemset(workspace)");
+        cuda_check(cudaMalloc(&fresh->din, n_in * sizeof(double2)), "cudaMalloc(input)");
+        cuda_check(cudaMalloc(&fresh->dout, n_out * sizeof(double2)), "cudaMalloc(output)");
+        cuda_check(cudaStreamSynchronize(fresh->st), "stream synchronize");
+        std::lock_guard<std::mutex> lk(d->staging_mu);
+        d->staging_all.push_back(fresh.get());
+        sg = fresh.release();
+    }
+    struct Return {
+        pft_dplan_s* d;
+        pft_dplan_s::Staging* s;
+        ~Return() {
+            std::lock_guard<std::mutex> lk(d->staging_mu);
+            d->staging_free.push_back(s);
         }
-    } cleanup{din, dout, ws, own_in, own_out};
-    if (!din) {
-        cuda_check(cudaMalloc(&din, n_in * sizeof(pft_c128)), "cudaMalloc(input)");
-        own_in = true;
-    }
-    if (!dout) {
-        cuda_check(cudaMalloc(&dout, n_out * sizeof(pft_c128)), "cudaMalloc(output)");
-        own_out = true;
-    }
-    double2* Y = d->d_ws;
-    if (batch > 1) {
-        cuda_check(cudaMalloc(&ws, d->workspace_bytes(batch)), "cudaMalloc(workspace)");
-        cuda_check(cudaMemsetAsync(ws, 0, d->workspace_bytes(batch), st), "cudaMemset(workspace)");
-        Y = ws;
-    }
+    } give_back{d, sg};
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : sg->st;
+    double2* din = d_in ? reinterpret_cast<double2*>(d_in) : sg->din;
+    double2* dout = d_out ? reinterpret_cast<double2*>(d_out) : sg->dout;
     cuda_check(cudaMemcpyAsync(din, h_in, n_in * sizeof(pft_c128), cudaMemcpyHostToDevice, st), "H2D input");
-    run_execute(d, reinterpret_cast<const double2*>(din), batch, d->host.N, reinterpret_cast<double2*>(dout), Y, st);
+    run_execute(d, din, batch, d->host.N, dout, sg->ws, st, false);
     cuda_check(cudaMemcpyAsync(h_out, dout, n_out * sizeof(pft_c128), cudaMemcpyDeviceToHost, st), "D2H output");
-    cuda_check(cudaStreamSynchronize(st), "stream synchronize");
-    int flags = 0;
-    cuda_check(cudaMemcpy(&flags, d->d_status, sizeof(int), cudaMemcpyDeviceToHost), "read status");
-    if (flags) {
-        cuda_check(cudaMemset(d->d_status, 0, sizeof(int)), "reset status");
+    if (read_status(d->ws_view(sg->ws).status, true, st))
         fail(PFT_ERR_NON_FINITE, "execute: non-finite input entries (non-finite output detected)");
-    }
     PFT_API_END
 }
 

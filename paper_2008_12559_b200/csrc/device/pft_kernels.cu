@@ -28,34 +28,10 @@
 #include "../common/rng.h"
 #include "fft_smem.cuh"
 #include "kernels.cuh"
+#include "timeline.cuh"
 #include "tma.cuh"
 
 namespace pftdev {
-
-#ifdef PFT_TIMELINE
-// Development instrumentation: per-CTA %globaltimer stamps at phase boundaries, kept for the
-// last 4 executes (ring indexed by the launch sequence number) so a PDL chain can be read back.
-__device__ unsigned long long g_pft_timeline[4][4096][6];
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define PFT_STAMP(slot) \
-    if (threadIdx.x == 0 && blockIdx.x + blockIdx.y * gridDim.x < 4096) \
-        g_pft_timeline[P.tl_seq & 3][blockIdx.x + blockIdx.y * gridDim.x][slot] = gtimer();
-__device__ unsigned long long g_pft_timeline2[4][4096][6];
-#define PFT_STAMP2(slot) \
-    if (threadIdx.x == 0 && blockIdx.x + blockIdx.y * gridDim.x < 4096) \
-        g_pft_timeline2[P.tl_seq & 3][blockIdx.x + blockIdx.y * gridDim.x][slot] = gtimer();
-// K2-tail worker k of signal 0 (k1_k2_tail)
-#define PFT_STAMPW(k, slot) \
-    if (threadIdx.x == 0 && blockIdx.y == 0 && (k) < 4096) g_pft_timeline2[P.tl_seq & 3][(k)][slot] = gtimer();
-#else
-#define PFT_STAMP(slot)
-#define PFT_STAMP2(slot)
-#define PFT_STAMPW(k, slot)
-#endif
 
 // Grid-wide barrier for K1's fused K2 tail (all CTAs are co-resident: cooperative launch).
 // Self-resetting: the last arriver zeroes the count and bumps the generation, so the state
@@ -340,7 +316,7 @@ __device__ __forceinline__ void k1_sum_tail_fast(const K1Params& P, const double
     constexpr int FAST_OUT = 4, FAST_P2 = 8;
     const K2Params& Q = P.k2;
     const int tid = threadIdx.x, nt = blockDim.x;
-    double2* __restrict__ rowc = P.Y + ((size_t)b * P.P2 + c) * Q.W;
+    double2* __restrict__ rowc = P.Y + (size_t)b * P.y_stride + (size_t)c * Q.W;
     double2 keep[FAST_OUT];
 #pragma unroll
     for (int i = 0; i < FAST_OUT; ++i) {
@@ -350,7 +326,7 @@ __device__ __forceinline__ void k1_sum_tail_fast(const K1Params& P, const double
             rowc[so] = keep[i];
         }
     }
-    unsigned* ctl = P.arrivals + (size_t)b * (P.P2 + 2);  // {tickets, ...}
+    unsigned* ctl = P.arrivals + (size_t)b * P.ctl_stride;  // {tickets, ...}
     unsigned* s_last = reinterpret_cast<unsigned*>(tw2 + P.P2);
     __syncthreads();  // every row store precedes thread 0's fence and ticket
     PFT_STAMP(5)
@@ -366,7 +342,7 @@ __device__ __forceinline__ void k1_sum_tail_fast(const K1Params& P, const double
     }
     __threadfence();  // the other rows were fenced before their tickets (threadFenceReduction)
     PFT_STAMP2(1)
-    const double2* __restrict__ rows = P.Y + (size_t)b * P.P2 * Q.W;
+    const double2* __restrict__ rows = P.Y + (size_t)b * P.y_stride;
 #pragma unroll
     for (int i = 0; i < FAST_OUT; ++i) {
         const uint64_t so = (uint64_t)tid + (uint64_t)i * nt;
@@ -412,11 +388,7 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     // One residue class per signal (P2 = 1: short batched signals, e.g. the 2-D passes): the
     // row is the output; no row store, ready flag, ticket or read-back (same arithmetic as a
     // one-row reduction: cadd(0, v) = v).
-#ifdef PFT_NO_DIRECT  // development A/B
-    const bool direct = false;
-#else
     const bool direct = P.P2 == 1;
-#endif
     // Few residue classes and few outputs (batched short signals, e.g. C3: P2 = 2, W = 513):
     // only the last CTA of the signal to arrive reduces, each thread summing the P2 rows of its
     // own outputs with all loads in flight at once and its own row's values from registers;
@@ -424,7 +396,7 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     // block barrier each: at C3 fence + wait + reduce took 10.5 of a CTA's 35.6 us.)
     constexpr int FAST_OUT = 4, FAST_P2 = 8;
     const bool fast = k1_tc(R) && !direct && P.P2 <= FAST_P2 && Q.W <= (uint64_t)FAST_OUT * nt;
-    double2* __restrict__ rowc = P.Y + ((size_t)b * P.P2 + c) * Q.W;
+    double2* __restrict__ rowc = P.Y + (size_t)b * P.y_stride + (size_t)c * Q.W;
     if constexpr (k1_tc(R)) {
         if (fast) {
             k1_sum_tail_fast<R>(P, res, c, b, twc, tw2, Mh, p1_pow2, p2_pow2, lg_p1);
@@ -443,7 +415,7 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     }
     if (direct) return;
     // publish the row, then take a ticket: the last `reducers` arrivals of signal b reduce
-    unsigned* ctl = P.arrivals + (size_t)b * (P.P2 + 2);  // {tickets, done, ready[P2]}
+    unsigned* ctl = P.arrivals + (size_t)b * P.ctl_stride;  // {tickets, done, ready[P2]}
     unsigned* ready = ctl + 2;
     double2* part = tw2 + P.P2;                           // [nw][64] reducer partials
     unsigned* s_ticket = reinterpret_cast<unsigned*>(part + (size_t)nw * 64);
@@ -457,9 +429,6 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
         *s_ticket = atomicAdd(ctl, 1u);
     }
     __syncthreads();
-#ifdef PFT_DEV_NO_REDUCE  // development A/B only: the sum tail without the reduction
-    return;
-#endif
     PFT_STAMP2(0)  // sum-tail timeline (K2's ring is unused here): ticket taken
     const uint32_t t = *s_ticket, K = P.reducers;
     if (t + K < P.P2) {
@@ -470,7 +439,7 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     // its slice of outputs once the warp's rows are flagged ready (most are by now).
     const uint32_t k = t + K - P.P2;
     const uint64_t s0 = (uint64_t)k * Q.W / K, s1 = (uint64_t)(k + 1) * Q.W / K;
-    const double2* __restrict__ rows = P.Y + (size_t)b * P.P2 * Q.W;
+    const double2* __restrict__ rows = P.Y + (size_t)b * P.y_stride;
     // this warp's rows c = warp, warp + nw, ...: all flags checked at once (one lane per row)
     for (uint32_t r = warp + (uint32_t)lane * nw; r < P.P2; r += 32u * nw)
         while (ld_acquire_u32(ready + r) == 0) __nanosleep(32);
@@ -545,7 +514,7 @@ __device__ __forceinline__ void k1_k2_tail(const K1Params& P, uint32_t c, uint32
     double2* tw2 = scratch + (size_t)G * P.P2;    // omega_P2^t
     double2* pre = tw2 + P.P2;                    // omega_p^{m1 c}
     unsigned* s_t = reinterpret_cast<unsigned*>(pre + P.P2);
-    unsigned* ctl = P.arrivals + (size_t)b * 2;   // {tickets, done}
+    unsigned* ctl = P.arrivals + (size_t)b * P.ctl_stride;   // {tickets, done}
     __syncthreads();  // the CTA's slab stores precede thread 0's fence and ticket
     if (tid == 0) {
         __threadfence();
@@ -588,7 +557,7 @@ __device__ __forceinline__ void k1_k2_tail(const K1Params& P, uint32_t c, uint32
             prefetch(m1);
             __syncthreads();
         }
-        const double2* __restrict__ Ym = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
+        const double2* __restrict__ Ym = P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R;
         for (uint32_t j0 = 0; j0 < (uint32_t)R; j0 += G) {
             const uint32_t g = min(G, (uint32_t)R - j0), n = P.P2 * g;
             // Z[jj][c] = omega_p^{m1 c} Y[c][j0 + jj]; all of a thread's L2 loads in flight first
@@ -846,7 +815,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         return;
     }
     // Y[b][m1][c][j]: the slab for one m1 is contiguous over (c, j) for K2.
-    double2* __restrict__ Y = P.Y + (size_t)b * P.P1 * P.P2 * R;
+    double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride;
     for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) {
         const uint32_t m1 = idx / R, j = idx - m1 * R;
         Y[((size_t)m1 * P.P2 + c) * R + j] = res[(size_t)j * P.P1 + m1];
@@ -914,7 +883,7 @@ __device__ __forceinline__ void k2_fft_block(const K2Params& P, uint32_t m1, uin
         pre[c] = __ldg(P.omega + (size_t)m1 * c);    // four-step twiddle; m1 c < p
     }
     __syncthreads();
-    const double2* __restrict__ Y = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
+    const double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R;
     load_twiddled_slab<R>(Y, P.P2, m1, pre, Z);
     __syncthreads();
     const double2* res = Z;
@@ -972,7 +941,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     PFT_STAMP2(2)
-    const double2* __restrict__ Y = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
+    const double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R;
     load_twiddled_slab<R>(Y, P.P2, m1, pre, Z);
     __syncthreads();
     PFT_STAMP2(3)
@@ -1030,7 +999,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_dot_post(K2Params P) {
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
-    const double2* __restrict__ Y = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
+    const double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R;
     load_twiddled_slab<R>(Y, P.P2, m1, pre, Z);
     __syncthreads();
     const bool p2_pow2 = (P.P2 & (P.P2 - 1)) == 0;
@@ -1082,7 +1051,7 @@ __global__ void __launch_bounds__(K2L_THREADS) k2_l2_post(K2Params P) {
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const bool p_pow2 = (P.p & (P.p - 1)) == 0;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's slab complete and visible
-    const double2* __restrict__ Yb = P.Y + (size_t)b * P.P1 * P.P2 * R;
+    const double2* __restrict__ Yb = P.Y + (size_t)b * P.y_stride;
     double2* __restrict__ out = P.out + (size_t)b * P.W;
     for (uint64_t s = gwarp; s < P.W; s += nwarps) {
         uint64_t mp = P.first_mod_p + s % P.p;
@@ -1130,7 +1099,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_direct_post(K2Params P) {
     const int warp = threadIdx.x >> 5;
     constexpr int NW = K2_THREADS / 32;
     const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
-    const double2* __restrict__ Y = P.Y + ((size_t)b * P.P1 + m1) * (size_t)P.P2 * R;
+    const double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R;
     double2* __restrict__ out = P.out + (size_t)b * P.W;
     if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");

@@ -107,13 +107,29 @@ int main() {
     assert res.returncode == 0, res.stderr
 
 
-def test_cpp_api_demo_builds_and_runs(tmp_path, pft):
-    """examples/cpp_api_demo.cpp uses the reference's interface from C++ (pft/pft.hpp)."""
+def _demo(tmp_path):
     exe = tmp_path / "demo"
-    _compile(["g++", "-std=c++20", "-Wall", "-Werror", "-I", str(ROOT / "include"),
+    _compile(["g++", "-std=c++20", "-Wall", "-Werror", "-pthread", "-I", str(ROOT / "include"),
               str(ROOT / "examples" / "cpp_api_demo.cpp"), "-L", str(LIB.parent), "-lpft_b200",
               f"-Wl,-rpath,{LIB.parent}"], exe)
+    return exe
+
+
+def test_cpp_api_demo_builds_and_runs(tmp_path, pft):
+    """examples/cpp_api_demo.cpp uses the reference's interface from C++ (pft/pft.hpp)."""
+    exe = _demo(tmp_path)
     res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
     assert '"p": 32768' in res.stdout
     assert "device p = 16384, r = 8" in res.stdout  # pft_select_divisor_device at C2b
+
+
+@pytest.mark.gpu
+def test_cpp_api_demo_executes_on_the_gpu(tmp_path, pft):
+    """The C++ drop-in path end to end on the B200: pft::execute (host vectors, the plan's staging
+    pool), 4 threads x 3 executes sharing one plan, non-finite input -> std::invalid_argument.
+    --require-gpu turns a pft::DeviceError into a failure (exit 6)."""
+    exe = _demo(tmp_path)
+    res = subprocess.run([str(exe), "--require-gpu"], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "4 threads x 3 executes on one plan" in res.stdout

@@ -166,9 +166,10 @@ def test_batched_workspace_and_tail_forms(pft, oracle, form):
     N, M, mu, batch = 2 ** 16, 128, 77, 3
     # the K2 tail has K1 instantiations for r = 4..7 only (k1_k2_tail_instantiated): p = 4096, r = 7
     plan = pft.build_plan(N, M, mu, 4096 if form.startswith("k2-tail") else None, 1e-12)
-    kw = {"fused": dict(fuse=True, k2_mode=1), "k2": dict(k2_mode=1, k2_tail=-1),
-          "k2-tail": dict(k2_mode=1, k2_tail=1), "k2-tail-1": dict(k2_mode=1, k2_tail=1, reducers=1),
-          "sum": dict(k2_mode=5), "sum-all-reduce": dict(k2_mode=5, reducers=1 << 20)}[form]
+    kw = {"fused": dict(k2_at="fused", second_pass="k2-fft"), "k2": dict(second_pass="k2-fft", k2_at="grid"),
+          "k2-tail": dict(second_pass="k2-fft", k2_at="tail"),
+          "k2-tail-1": dict(second_pass="k2-fft", k2_at="tail", tail_ctas=1),
+          "sum": dict(second_pass="sum"), "sum-all-reduce": dict(second_pass="sum", tail_ctas=1 << 20)}[form]
     d = pft.DevicePlan(plan, **kw)
     assert d.launches_per_execute() == (2 if form == "k2" else 1)
     fuse = form
@@ -236,7 +237,7 @@ def test_batched_small_signals_sum_tail(pft, oracle, N, M, mu, p):
 
 @pytest.mark.parametrize("N,M,mu,p", [(2 ** 20, 64, 0, 2048), (2 ** 22, 1000, -3, 2 ** 13)])
 def test_sum_tail_and_k2_forms_agree(pft, oracle, N, M, mu, p):
-    """The same plan through the sum tail (k2_mode 5) and through K2 (k2_mode 1): both at the
+    """The same plan through the sum tail and through the K2 FFT form: both at the
     oracle, and the two device forms agree far below the gate."""
     import torch
     plan = pft.build_plan(N, M, mu, p, 1e-12)
@@ -244,8 +245,8 @@ def test_sum_tail_and_k2_forms_agree(pft, oracle, N, M, mu, p):
     x = torch.from_numpy(a).cuda()
     ref = oracle.execute(plan, a)
     res = []
-    for mode, launches in ((5, 1), (1, 2)):
-        d = pft.DevicePlan(plan, k2_mode=mode, k2_tail=-1)
+    for mode, launches in (("sum", 1), ("k2-fft", 2)):
+        d = pft.DevicePlan(plan, second_pass=mode, k2_at="grid")
         assert d.launches_per_execute() == launches
         out = torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda")
         d.execute_ptr(x.data_ptr(), out.data_ptr())
@@ -255,16 +256,16 @@ def test_sum_tail_and_k2_forms_agree(pft, oracle, N, M, mu, p):
     assert rel_l2(res[0], res[1]) <= 1e-13
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("mode", ["k2-fft", "k2-dot", "k2-direct", "k2-l2", "sum"])
 def test_every_second_pass_form(pft, oracle, mode):
-    """Each second-pass form forced on the same plan (K2 FFT 1, dot 2, direct 3, L2 4; sum tail
-    5) matches the oracle: the auto selection only picks among them by speed."""
+    """Each second-pass form forced on the same plan (K2 FFT, dot, direct, L2; sum tail) matches
+    the oracle: the auto selection only picks among them by speed."""
     import torch
     N, M, mu, p = 2 ** 20, 100, 777, 4096
     plan = pft.build_plan(N, M, mu, p, 1e-12)
     a = pft.generate_signal(pft.KIND_UNIFORM, 12, N)
     x = torch.from_numpy(a).cuda()
-    d = pft.DevicePlan(plan, k2_mode=mode)
+    d = pft.DevicePlan(plan, second_pass=mode)
     out = torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda")
     for _ in range(2):
         d.execute_ptr(x.data_ptr(), out.data_ptr())
@@ -287,8 +288,8 @@ def test_k2_tail_matches_k2_grid(pft, oracle, N, M, mu, p, reducers):
     a = pft.generate_signal(pft.KIND_UNIFORM, 41, N)
     x = torch.from_numpy(a).cuda()
     res = []
-    for tail, kind in ((1, "K2 tail"), (-1, "K2 grid")):
-        d = pft.DevicePlan(plan, k2_mode=1, k2_tail=tail, reducers=reducers)
+    for at, kind in (("tail", "K2 tail"), ("grid", "K2 grid")):
+        d = pft.DevicePlan(plan, second_pass="k2-fft", k2_at=at, tail_ctas=reducers)
         assert d.tail_kind() == kind
         out = torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda")
         for _ in range(3):  # counters re-arm between executes

@@ -214,3 +214,24 @@ def test_shard_layout_errors(pft):
         pft.shard_layout(512, 2, 2)
     with pytest.raises(ValueError):
         pft.shard_layout(0, 1, 0)
+
+
+def test_select_divisor_sharded_collective_term(pft):
+    """pft_select_divisor_sharded (the comm-aware planner): C5 (N = 2^30,
+    M = 2^12) over 1..8 GPUs.  The pick divides N and is feasible; the modelled time falls with
+    G; the reduced slab (16 p r bytes) stays far below SPEC's p = 2^22 choice (268 MB, SURVEY.md
+    §8(e)); and with G > 1 the collective term never favours a larger slab than G = 1 does."""
+    from paper_2008_12559_b200.sharded import select_divisor_sharded
+    N, M = 2 ** 30, 2 ** 12
+    prev_us, slab1 = None, None
+    for G in (1, 2, 4, 8):
+        p, r, us = select_divisor_sharded(N, M, G)
+        assert N % p == 0 and r == pft.min_terms(1e-12, M, p)
+        slab = 16 * p * r
+        assert slab <= 64 * 2 ** 20
+        if prev_us is not None:
+            assert us < prev_us
+            assert slab <= slab1
+        else:
+            slab1 = slab
+        prev_us = us
