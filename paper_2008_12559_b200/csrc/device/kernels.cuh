@@ -82,7 +82,6 @@ struct K2Params {
     int mode;                      // K2_DIRECT / K2_FFT / K2_DOT
     uint32_t k2_ctas;              // K2_L2 grid width (0 = 148)
     int release_next;              // trigger the next launch at K2 start (1) / end (2) (PDL chaining)
-    uint32_t tl_seq;               // launch sequence number (PFT_TIMELINE instrumentation only)
     FftRadices fft2;               // radices of P2
     double2* out;                  // [batch][W]
     int* status;                   // non-finite flag word of the workspace (bit 0)
@@ -140,7 +139,6 @@ struct K1Params {
     unsigned* arrivals;         // signal b's control words at arrivals + b * ctl_stride (zeroed once):
                                 // sum tail {tickets, done, ready[P2]}, K2 tail {tickets, done}
     uint64_t ctl_stride;        // words between consecutive signals' control words
-    uint32_t tl_seq;            // launch sequence number (PFT_TIMELINE instrumentation only)
     int k2_tail;                // K2 work done by the last `reducers` CTAs of a signal to write
                                 // their slab (last-arrival, no grid-wide wait; see k1_k2_tail)
     uint32_t k2_group;          // k2_tail: columns j per FFT group (the group's Z + scratch fit the ring)

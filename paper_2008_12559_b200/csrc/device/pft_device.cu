@@ -491,8 +491,6 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
     const pft_dplan_s::WsView w = d->ws_view(ws);
     auto P1 = d->k1_params(v, in, d->host.q, in_stride, w.Y, w.y_stride, pdl);
     auto P2 = d->k2_params(w.Y, w.y_stride, out, w.status);
-    static std::atomic<uint32_t> seq{0};  // PFT_TIMELINE ring index
-    P1.tl_seq = P2.tl_seq = seq.fetch_add(1, std::memory_order_relaxed);
     P1.arrivals = w.arrivals;
     P1.ctl_stride = w.ctl_stride;
     if (d->sum_tail) {
@@ -741,7 +739,7 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         // against the stream: the columns go through the FFT in groups whose Z + scratch fit
         // the ring.  Workers hold their SM slots, and a K1 CTA of the next transform that starts
         // late finishes late (each CTA streams a fixed 1/P2 of the input), so the tail's m1
-        // rounds (~15 us each beside a streaming CTA, PFT_TIMELINE at C2c) must stay <= 10% of
+        // rounds (~15 us each beside a streaming CTA, per-CTA timestamps at C2c) must stay <= 10% of
         // the stream: C5 (2^30) gains 6% (3099 -> 2907 us), C2c (2^24, 2 rounds) loses (67 -> 77
         // us at 1 round).  k2_at: PFT_K2_AT_TAIL forces it on (if feasible), _GRID off.
         if (!d->sum_tail && d->k2_mode == pftdev::K2_FFT && !d->allow_fuse && k2_at != PFT_K2_AT_GRID &&
