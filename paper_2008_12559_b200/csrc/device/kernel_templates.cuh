@@ -1217,7 +1217,7 @@ cudaError_t launch_k1d_r(const CUtensorMap& map, const K1Params& P, dim3 grid, s
                          bool mu0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(K1_THREADS);
+    cfg.blockDim = dim3(K1D_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -1235,10 +1235,10 @@ int k1d_active_r(size_t smem, bool mu0) {
     int n = 0;
     if (mu0) {
         cudaFuncSetAttribute(k1d_contract<R, true>, a, (int)kMaxDynSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1d_contract<R, true>, K1_THREADS, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1d_contract<R, true>, K1D_THREADS, smem);
     } else {
         cudaFuncSetAttribute(k1d_contract<R, false>, a, (int)kMaxDynSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1d_contract<R, false>, K1_THREADS, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1d_contract<R, false>, K1D_THREADS, smem);
     }
     return n;
 }

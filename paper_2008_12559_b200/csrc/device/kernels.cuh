@@ -14,6 +14,9 @@ namespace pftdev {
 // {Re phase_l, Im phase_l, t_l, 0}.  Two K1 CTAs share an SM.
 constexpr int K1_CONSUMER_WARPS = 8;
 constexpr int K1_THREADS = 32 * (K1_CONSUMER_WARPS + 1);
+constexpr int K1D_THREADS = K1_THREADS + 32;  // dynamic K1: + the class-ticket warp
+constexpr int K1D_HR = 8;   // dynamic K1: item hand-off ring (consumers -> ticket lane)
+constexpr int K1D_JQ = 32;  // dynamic K1: finisher-job queue (ticket lane -> consumers)
 #ifndef PFT_K1_BR
 #define PFT_K1_BR 32
 #endif
@@ -159,6 +162,7 @@ struct K1Params {
     double2* Cpart;             // signal b: [P2][nseg][R][P1] at Cpart + b * y_stride
     double2* rows;              // signal b: sum-tail rows [P2][W] or the K2 slab [P1][P2][R], + b * y_stride
     unsigned* cls;              // signal b: class counters [P2], then the signal ticket, + b * ctl_stride
+    uint32_t dev_flags;         // development A/B only (PFT_DYN_DEV): 1 no finisher, 2 no tickets, 4 no partial stores
 };
 
 
@@ -223,7 +227,7 @@ inline size_t k1d_smem_bytes(int r, uint32_t P1, uint32_t stages, uint32_t group
     const size_t p1 = P1 ? P1 : 1;
     return k1_ring_align_slack(r) + (size_t)stages * k1_stage_bytes(r) +
            sizeof(double2) * ((size_t)r * p1 + (size_t)group * p1 + p1 + r) + 2 * stages * sizeof(uint64_t) +
-           4 * (size_t)stages + 16;
+           4 * (size_t)stages + 16 + 16 * K1D_HR + 4 * K1D_HR + 4 * K1D_JQ + 16;
 }
 int k1d_max_active_per_sm(int r, size_t smem, bool mu0);
 cudaError_t launch_k1d(const CUtensorMap& map, const K1Params& P, int r, uint32_t grid, bool mu0, cudaStream_t st);

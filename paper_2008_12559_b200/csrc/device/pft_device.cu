@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -520,11 +521,12 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
         P1.Cpart = w.Y;
         P1.rows = rows;
         P1.cls = w.arrivals;
+        if (const char* e = std::getenv("PFT_DYN_DEV")) P1.dev_flags = (uint32_t)std::strtoul(e, nullptr, 10);
         P2.Y = rows;
         P1.k2 = P2;
         const uint32_t grid = (uint32_t)std::min<uint64_t>(d->dyn_capacity, P1.total_items);
         cuda_check(pftdev::launch_k1d(map, P1, d->host.r, grid, d->mu0, st), "K1 (dynamic) launch");
-        if (d->sum_kernel)
+        if (d->sum_kernel && !(P1.dev_flags & 8))
             cuda_check(pftdev::launch_sum_rows(P2, (uint32_t)d->P2, rows, w.y_stride, (uint32_t)batch, st), "row sum launch");
         else if (!d->sum_tail)
             cuda_check(pftdev::launch_k2(P2, d->host.r, (uint32_t)batch, st), "K2 launch");
@@ -561,9 +563,11 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
 // smaller K2 -- with a K2 FFT over P2 that fits shared memory when the second pass is K2's.
 // Ring depth first (>= 4 stages on the vector path), then the widest FFT column group.  Column
 // segments per 32-row block make >= 6 items per CTA slot so the claims balance.
-constexpr size_t kDynSmemBudget = (228 * 1024) / 2 - 1024;
+// two dynamic-K1 CTAs per SM, leaving room for the 1 KB reservation of a small co-resident CTA
+// (the row sum of the previous transform)
+constexpr size_t kDynSmemBudget = (228 * 1024) / 2 - 2048;
 
-bool plan_dynamic(pft_dplan_s* d, const HostPlan& H, size_t batch_hint, int n_sms, int pass2) {
+bool plan_dynamic(pft_dplan_s* d, const HostPlan& H, size_t batch_hint, int n_sms, int pass2, uint64_t force_p2) {
     const int r = H.r;
     const uint64_t W = d->W;
     const bool mu0 = std::all_of(H.phase.begin(), H.phase.end(), [](const cplx& z) { return z == cplx(1.0, 0.0); });
@@ -583,6 +587,7 @@ bool plan_dynamic(pft_dplan_s* d, const HostPlan& H, size_t batch_hint, int n_sm
         c.P1 = *it;
         const uint64_t P1 = c.P1, P2 = H.p / P1;
         if (P1 > 1024) continue;
+        if (force_p2 && P2 != force_p2) continue;
         if (P1 > 1 && !factor_radices((uint32_t)P1, c.fr)) continue;
         if (P1 <= 1) c.fr.n = 1;
         c.sum = pass2 == PFT_PASS2_SUM_TAIL ||
@@ -610,6 +615,7 @@ bool plan_dynamic(pft_dplan_s* d, const HostPlan& H, size_t batch_hint, int n_sm
         uint64_t nseg = std::min<uint64_t>(std::max<uint32_t>(1, nch / 4), (3 * c.cap + base - 1) / base);
         nseg = std::max<uint64_t>(nseg, 1);
         while (nseg > 1 && nseg * (uint64_t)r * P1 * sizeof(double2) > 64 * 1024) --nseg;
+        if (const char* e = std::getenv("PFT_DYN_NSEG")) nseg = std::max<uint64_t>(1, std::min<uint64_t>(nch, std::strtoull(e, nullptr, 10)));
         c.nseg = (uint32_t)nseg;
         c.items = base * nseg;
         // the largest P1 with >= 2 items per CTA slot; failing that, the most items
@@ -628,6 +634,7 @@ bool plan_dynamic(pft_dplan_s* d, const HostPlan& H, size_t batch_hint, int n_sm
     d->fft_group = best.grp;
     d->dyn_smem = best.smem;
     d->dyn_capacity = best.cap;
+    if (const char* e = std::getenv("PFT_DYN_GRID")) d->dyn_capacity = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
     d->sum_tail = best.sum;
     d->fast_reduce = best.sum && P2 > 1 && P2 <= 8 && W <= 4u * pftdev::K1_CONSUMER_WARPS * 32;
     d->sum_kernel = best.sum && P2 > 1 && !d->fast_reduce;
@@ -804,10 +811,10 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     uint64_t p2 = opts && opts->p2 ? opts->p2 : 0;
     const size_t batch_hint = opts && opts->batch_hint > 1 ? (size_t)opts->batch_hint : 1;
     // dynamic K1 unless the caller pins a static choice (P2, a K2 placement, a K2 form other than FFT)
-    if (schedule != PFT_K1_SCHEDULE_STATIC && !p2 && k2_at == PFT_K2_AT_AUTO &&
+    if (schedule != PFT_K1_SCHEDULE_STATIC && (!p2 || schedule == PFT_K1_SCHEDULE_DYNAMIC) && k2_at == PFT_K2_AT_AUTO &&
         (pass2 == PFT_PASS2_AUTO || pass2 == PFT_PASS2_SUM_TAIL || pass2 == PFT_PASS2_K2_FFT) &&
         (opts == nullptr || opts->k1_stages == 0))
-        plan_dynamic(d.get(), H, batch_hint, prop.multiProcessorCount, pass2);
+        plan_dynamic(d.get(), H, batch_hint, prop.multiProcessorCount, pass2, p2);
     if (schedule == PFT_K1_SCHEDULE_DYNAMIC && !d->dyn)
         fail(PFT_ERR_UNSUPPORTED, "dplan_create: no dynamic-K1 decomposition for this plan and options");
     if (!d->dyn) {

@@ -111,43 +111,32 @@ cudaError_t launch_k1d(const CUtensorMap& map, const K1Params& P, int r, uint32_
     return cudaErrorInvalidValue;
 }
 
-// Residue-row sum of the dynamic K1's sum tail: CTA (x, b) owns outputs s = 32 x + lane; warp w
-// sums rows c = w, w + 4, ... (8 loads in flight per lane), the 4 warp partials are added in a
-// fixed order: deterministic.  Launched right after K1 with programmatic dependent launch: it
-// releases the next launch at once and waits for K1's rows.
-constexpr int kSumThreads = 128;
+// Residue-row sum of the dynamic K1's sum tail: one warp per CTA owns 32 outputs (s = 32 x + lane)
+// and sums the P2 rows in ascending c with 8 loads in flight: deterministic.  Launched right after
+// K1 with programmatic dependent launch: it releases the next launch at once and waits for K1's
+// rows.  One warp, no shared memory, few registers: its CTAs fit beside two dynamic-K1 CTAs, so
+// they never hold an SM slot the next transform's K1 needs.
+constexpr int kSumThreads = 32;
 __global__ void __launch_bounds__(kSumThreads) k_sum_rows(const K2Params Q, uint32_t P2, const double2* rows0,
                                                          uint64_t y_stride) {
-    __shared__ double2 part[kSumThreads / 32][32];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int NW = kSumThreads / 32;
     const uint32_t b = blockIdx.y;
-    const uint64_t so = (uint64_t)blockIdx.x * 32 + lane;
-    const bool ok = so < Q.W;
-    const double2* __restrict__ rows = rows0 + (size_t)b * y_stride;
+    const uint64_t so = (uint64_t)blockIdx.x * 32 + threadIdx.x;
+    if (so >= Q.W) return;
+    const double2* __restrict__ rows = rows0 + (size_t)b * y_stride + so;
     double2 acc = make_double2(0.0, 0.0);
-    for (uint32_t c0 = warp; c0 < P2; c0 += 8 * NW) {
+    for (uint32_t c0 = 0; c0 < P2; c0 += 8) {
         double2 v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const uint32_t c = c0 + u * NW;
-            v[u] = (ok && c < P2) ? __ldcg(rows + (size_t)c * Q.W + so) : make_double2(0.0, 0.0);
-        }
+        for (int u = 0; u < 8; ++u) v[u] = c0 + u < P2 ? __ldcg(rows + (size_t)(c0 + u) * Q.W) : make_double2(0.0, 0.0);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc = cadd(acc, v[u]);
+        for (int u = 0; u < 8; ++u)
+            if (c0 + u < P2) acc = cadd(acc, v[u]);
     }
-    part[warp][lane] = acc;
-    __syncthreads();
-    if (warp == 0 && ok) {
-        double2 tot = part[0][lane];
-#pragma unroll
-        for (int w = 1; w < NW; ++w) tot = cadd(tot, part[w][lane]);
-        const double2 o = cmul(tot, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
-        Q.out[(size_t)b * Q.W + so] = o;
-        if (!isfinite(o.x) || !isfinite(o.y)) atomicOr(Q.status, 1);
-    }
+    const double2 o = cmul(acc, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
+    Q.out[(size_t)b * Q.W + so] = o;
+    if (!isfinite(o.x) || !isfinite(o.y)) atomicOr(Q.status, 1);
 }
 
 cudaError_t launch_sum_rows(const K2Params& Q, uint32_t P2, const double2* rows, uint64_t y_stride, uint32_t batch,
