@@ -432,7 +432,6 @@ def run_ours(args):
                               f"{nbuf} rotating inputs of {16 * N / 2**20:.0f} MiB (> L2 126 MiB)"),
                        "timing": "CUDA graph of K steps, CUDA events on the launch stream",
                        "streams": args.streams, "overlap_previous": overlap,
-                       "k1_schedule": d.schedule,
                        "tail": {"sum tail": "sum tail in K1 (one kernel per execute)",
                                 "K2 tail": "K2 work by K1's last-arriving CTAs (one kernel per execute)",
                                 "fused K2": "K2 in K1 behind a grid barrier (one kernel per execute)"}.get(
@@ -447,7 +446,7 @@ def run_ours(args):
             "parity": parity,
             "input_gbs": value * 16 * N / 1e9,
             "input_gbs_frac_of_peak": value * 16 * N / 1e9 / world / peak,
-            "roofline": {"bound": "hbm", "kernel": "k1d_contract" if d.schedule == "dynamic" else "k1_contract_fft", "achieved": k1_gbs, "peak": peak,
+            "roofline": {"bound": "hbm", "kernel": "k1_contract_fft", "achieved": k1_gbs, "peak": peak,
                          "unit": "GB/s", "frac": k1_gbs / peak, "peak_source": peak_src,
                          "traffic": committed_traffic(args.config),
                          "algorithmic_bytes_per_launch": 16 * N * B, "k1_ms": k1_ms,

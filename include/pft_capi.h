@@ -165,12 +165,6 @@ typedef struct pft_dplan_s* pft_dplan_t;
 #define PFT_K2_AT_TAIL 2       /* by K1's last-arriving CTAs (r = 4..7)                         */
 #define PFT_K2_AT_FUSED 3      /* in K1 behind a grid-wide barrier (cooperative launch)         */
 
-/* How K1 distributes the contraction over CTAs. */
-#define PFT_K1_SCHEDULE_AUTO 0     /* dynamic when the decomposition allows it                   */
-#define PFT_K1_SCHEDULE_STATIC 1   /* one CTA per (residue class, signal)                          */
-#define PFT_K1_SCHEDULE_DYNAMIC 2  /* persistent CTAs claim 32-row x column-segment work items;
-                                      the CTA completing a class runs its FFT pass and tail     */
-
 typedef struct pft_dplan_opts {
     int device;          /* CUDA ordinal                                                      */
     uint64_t p2;         /* residue classes for K1 (0 = auto); must divide p                  */
@@ -180,8 +174,7 @@ typedef struct pft_dplan_opts {
     int tail_ctas;       /* sum-tail reducers / K2-tail workers per signal (0 = plan); always
                             capped below the co-resident K1 capacity (forward progress)       */
     int k2_grid_ctas;    /* grid width of the PFT_PASS2_K2_L2 form (0 = SM count)              */
-    int schedule;        /* PFT_K1_SCHEDULE_*                                                  */
-    int reserved;        /* must be 0                                                          */
+    int reserved[2];     /* must be 0                                                          */
     uint64_t batch_hint; /* typical batch per execute (0/1 = single signal): sizes the K1 grid */
 } pft_dplan_opts;
 
@@ -331,8 +324,6 @@ pft_status pft_launches_per_execute(pft_dplan_t d, int* launches);
  * 0 separate K2 grid, 1 sum tail in K1 (few bins), 2 K2 work by K1's last arrivals (many
  * bins), 3 K2 in K1 behind a grid barrier (opt-in). */
 pft_status pft_dplan_tail_kind(pft_dplan_t d, int* kind);
-/* K1 schedule of a device plan: PFT_K1_SCHEDULE_STATIC or _DYNAMIC. */
-pft_status pft_dplan_schedule(pft_dplan_t d, int* schedule);
 
 /* ------------------------------------------------------------------ data formats and callers
  * The formats either side of execute and the pipeline that calls it (

@@ -503,10 +503,10 @@ class PftPlan:
         _check(lib().pft_plan_json(self._h, buf, need.value, C.byref(need)))
         return buf.value.decode()
 
-    def device_plan(self, device: int = 0, p2: int = 0, schedule: str = "auto") -> "DevicePlan":
-        key = (device, p2, schedule)
+    def device_plan(self, device: int = 0, p2: int = 0) -> "DevicePlan":
+        key = (device, p2)
         if key not in self._dplans:
-            self._dplans[key] = DevicePlan(self, device=device, p2=p2, schedule=schedule)
+            self._dplans[key] = DevicePlan(self, device=device, p2=p2)
         return self._dplans[key]
 
 
@@ -529,7 +529,6 @@ def device_count() -> int:
 
 PASS2 = {"auto": 0, "sum": 1, "k2-fft": 2, "k2-dot": 3, "k2-direct": 4, "k2-l2": 5}  # PFT_PASS2_*
 K2_AT = {"auto": 0, "grid": 1, "tail": 2, "fused": 3}                                 # PFT_K2_AT_*
-SCHEDULE = {"auto": 0, "static": 1, "dynamic": 2}                                     # PFT_K1_SCHEDULE_*
 EXEC_OVERLAP_PREVIOUS = 1                                                             # PFT_EXEC_*
 
 
@@ -540,12 +539,10 @@ class DevicePlan:
     second_pass: "auto" | "sum" (sum tail in K1) | "k2-fft" | "k2-dot" | "k2-direct" | "k2-l2"
     k2_at: where the k2-fft form runs: "auto" | "grid" (own launch) | "tail" (K1's last
     arrivals) | "fused" (K1 behind a grid barrier).  tail_ctas: sum-tail reducers / K2-tail
-    workers per signal (0 = plan).  batch_hint: typical batch per execute.  schedule: "auto" |
-    "static" (one K1 CTA per residue class) | "dynamic" (persistent CTAs claiming work items)."""
+    workers per signal (0 = plan).  batch_hint: typical batch per execute."""
 
     def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0, k1_stages: int = 0, second_pass: str = "auto",
-                 k2_at: str = "auto", tail_ctas: int = 0, k2_grid_ctas: int = 0, batch_hint: int = 1,
-                 schedule: str = "auto"):
+                 k2_at: str = "auto", tail_ctas: int = 0, k2_grid_ctas: int = 0, batch_hint: int = 1):
         self.plan = plan
         opts = _capi.DPlanOpts()
         opts.device = device
@@ -555,7 +552,6 @@ class DevicePlan:
         opts.k2_at = K2_AT[k2_at]
         opts.tail_ctas = tail_ctas
         opts.k2_grid_ctas = k2_grid_ctas
-        opts.schedule = SCHEDULE[schedule]
         opts.batch_hint = batch_hint
         h = C.c_void_p()
         _check(lib().pft_dplan_create(plan.handle, C.byref(opts), C.byref(h)))
@@ -598,12 +594,6 @@ class DevicePlan:
         n = C.c_int()
         _check(lib().pft_dplan_tail_kind(self._h, C.byref(n)))
         return self.TAIL_KINDS[n.value]
-
-    @property
-    def schedule(self) -> str:
-        n = C.c_int()
-        _check(lib().pft_dplan_schedule(self._h, C.byref(n)))
-        return {1: "static", 2: "dynamic"}[n.value]
 
     def execute_ptr(self, d_in: int, d_out: int, batch: int = 1, in_stride: int = 0, d_ws: int = 0,
                     stream: int = 0, overlap: bool = False) -> None:

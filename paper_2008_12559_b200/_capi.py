@@ -26,8 +26,7 @@ class PlanInfo(C.Structure):
 
 class DPlanOpts(C.Structure):
     _fields_ = [("device", C.c_int), ("p2", C.c_uint64), ("k1_stages", C.c_int), ("second_pass", C.c_int),
-                ("k2_at", C.c_int), ("tail_ctas", C.c_int), ("k2_grid_ctas", C.c_int), ("schedule", C.c_int),
-                ("reserved", C.c_int),
+                ("k2_at", C.c_int), ("tail_ctas", C.c_int), ("k2_grid_ctas", C.c_int), ("reserved", C.c_int * 2),
                 ("batch_hint", C.c_uint64)]
 
 
@@ -107,7 +106,6 @@ SIGNATURES: dict[str, tuple] = {
     "pft_sparse_tones": (ST, [U64, I, I64, I64, P, P]),
     "pft_launches_per_execute": (ST, [P, C.POINTER(I)]),
     "pft_dplan_tail_kind": (ST, [P, C.POINTER(I)]),
-    "pft_dplan_schedule": (ST, [P, C.POINTER(I)]),
     "pft_device_count": (ST, [C.POINTER(I)]),
     "pft_signal_read": (ST, [C.c_char_p, I, P, U64, C.POINTER(U64), C.POINTER(I)]),
     "pft_signal_write": (ST, [C.c_char_p, I, P, U64, I]),

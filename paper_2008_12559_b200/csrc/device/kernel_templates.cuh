@@ -1101,12 +1101,6 @@ __global__ void __launch_bounds__(K2_THREADS) k2_direct_post(K2Params P) {
     }
 }
 
-}  // namespace pftdev
-
-#include "k1d_kernel.cuh"
-
-namespace pftdev {
-
 // ----------------------------------------------------------------------------- launchers
 // Defined here, instantiated per r in the kinst_*.cu translation units (compiled in parallel);
 // pft_kernels.cu dispatches on r through the extern instantiations.
@@ -1212,44 +1206,11 @@ int k1_active_r(size_t smem, bool mu0) {
 }
 
 
-template <int R>
-cudaError_t launch_k1d_r(const CUtensorMap& map, const K1Params& P, dim3 grid, size_t smem, cudaStream_t st,
-                         bool mu0) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(K1D_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = P.pdl ? 1 : 0;
-    if (mu0) return cudaLaunchKernelEx(&cfg, k1d_contract<R, true>, map, P);
-    return cudaLaunchKernelEx(&cfg, k1d_contract<R, false>, map, P);
-}
-
-template <int R>
-int k1d_active_r(size_t smem, bool mu0) {
-    const auto a = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    int n = 0;
-    if (mu0) {
-        cudaFuncSetAttribute(k1d_contract<R, true>, a, (int)kMaxDynSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1d_contract<R, true>, K1D_THREADS, smem);
-    } else {
-        cudaFuncSetAttribute(k1d_contract<R, false>, a, (int)kMaxDynSmem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1d_contract<R, false>, K1D_THREADS, smem);
-    }
-    return n;
-}
-
 #define PFT_INSTANCES(R, EXT)                                                                                   \
     EXT template cudaError_t launch_k1_r<R>(const CUtensorMap&, const K1Params&, dim3, size_t, cudaStream_t, bool); \
     EXT template cudaError_t configure_k1_r<R>(size_t, bool);                                                  \
     EXT template int k1_active_r<R>(size_t, bool);                                                             \
     EXT template cudaError_t launch_k2_r<R>(const K2Params&, dim3, cudaStream_t);                              \
-    EXT template cudaError_t configure_k2_r<R>(size_t);                                                        \
-    EXT template cudaError_t launch_k1d_r<R>(const CUtensorMap&, const K1Params&, dim3, size_t, cudaStream_t, bool); \
-    EXT template int k1d_active_r<R>(size_t, bool);
+    EXT template cudaError_t configure_k2_r<R>(size_t);
 
 }  // namespace pftdev

@@ -14,9 +14,6 @@ namespace pftdev {
 // {Re phase_l, Im phase_l, t_l, 0}.  Two K1 CTAs share an SM.
 constexpr int K1_CONSUMER_WARPS = 8;
 constexpr int K1_THREADS = 32 * (K1_CONSUMER_WARPS + 1);
-constexpr int K1D_THREADS = K1_THREADS + 32;  // dynamic K1: + the class-ticket warp
-constexpr int K1D_HR = 8;   // dynamic K1: item hand-off ring (consumers -> ticket lane)
-constexpr int K1D_JQ = 32;  // dynamic K1: finisher-job queue (ticket lane -> consumers)
 #ifndef PFT_K1_BR
 #define PFT_K1_BR 32
 #endif
@@ -148,21 +145,6 @@ struct K1Params {
     int fused;                  // run K2 in K1's tail behind a grid barrier (cooperative launch)
     unsigned* bar;              // grid-barrier state {count, generation} (workspace header, zeroed once)
     K2Params k2;                // K2 parameters for the fused tail
-    // ---- dynamic K1 (k1d_contract): persistent CTAs claim work items (signal, residue class c,
-    // row block rb of 32 rows, column segment g) from a counter; per-item partial moments go to
-    // Cpart, the CTA that completes a class's last item (class counter) runs its FFT and tail.
-    uint32_t nrb;               // row blocks per class, ceil(P1 / 32)
-    uint32_t nseg;              // column segments G per row block
-    uint32_t nch;               // TMA chunks (16 pairs) per row of the view
-    uint32_t items_per_signal;  // P2 * nrb * nseg
-    uint32_t total_items;       // batch * items_per_signal
-    uint32_t fft_group;         // columns per FFT group (scratch = fft_group x P1)
-    int fast_reduce;            // sum tail: the class finisher that completes a signal sums its rows
-    unsigned* item_ctr;         // workspace header word (zero between launches; re-armed by the last claim)
-    double2* Cpart;             // signal b: [P2][nseg][R][P1] at Cpart + b * y_stride
-    double2* rows;              // signal b: sum-tail rows [P2][W] or the K2 slab [P1][P2][R], + b * y_stride
-    unsigned* cls;              // signal b: class counters [P2], then the signal ticket, + b * ctl_stride
-    uint32_t dev_flags;         // development A/B only (PFT_DYN_DEV): 1 no finisher, 2 no tickets, 4 no partial stores
 };
 
 
@@ -204,8 +186,7 @@ int k1_max_active_per_sm(int r, uint32_t P1, uint32_t stages, bool mu0);
 // A signal's control words and data sit at the same offsets whatever the batch of the call, so a
 // workspace sized for batch B serves any batch <= B (remainder batches).
 constexpr size_t kWsHeaderBytes = 256;
-constexpr size_t kWsStatusOffset = 8;   // bytes into the header
-constexpr size_t kWsItemCtrOffset = 16; // dynamic K1's work-item counter
+constexpr size_t kWsStatusOffset = 8;  // bytes into the header
 inline size_t ws_align(size_t b) { return (b + 255) & ~size_t(255); }
 // sum-tail scratch in the (idle) ring after the FFT scratch: twiddle tables, per-warp
 // reducer partials, ticket
@@ -221,20 +202,6 @@ inline size_t k1_k2_tail_bytes(uint32_t group, uint32_t P2) {
     return sizeof(double2) * (2 * (size_t)group * P2 + 2 * (size_t)P2) + 16;
 }
 cudaError_t configure_k2(int r, uint32_t P2);
-// dynamic K1: ring + C slab [r][P1] + FFT scratch [group][P1] + omega_P1 + w + 2S mbarriers +
-// the per-stage item ids and flags
-inline size_t k1d_smem_bytes(int r, uint32_t P1, uint32_t stages, uint32_t group) {
-    const size_t p1 = P1 ? P1 : 1;
-    return k1_ring_align_slack(r) + (size_t)stages * k1_stage_bytes(r) +
-           sizeof(double2) * ((size_t)r * p1 + (size_t)group * p1 + p1 + r) + 2 * stages * sizeof(uint64_t) +
-           4 * (size_t)stages + 16 + 16 * K1D_HR + 4 * K1D_HR + 4 * K1D_JQ + 16;
-}
-int k1d_max_active_per_sm(int r, size_t smem, bool mu0);
-cudaError_t launch_k1d(const CUtensorMap& map, const K1Params& P, int r, uint32_t grid, bool mu0, cudaStream_t st);
-// Sum of the residue rows of the dynamic K1's sum tail (P2 > 8): out[b][s] =
-// e^{-pi i m / p} sum_c rows[b][c][s], fixed order; one launch after K1 (programmatic dependent).
-cudaError_t launch_sum_rows(const K2Params& Q, uint32_t P2, const double2* rows, uint64_t y_stride, uint32_t batch,
-                            cudaStream_t st);
 cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t batch, bool mu0, cudaStream_t st);
 cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st);
 cudaError_t launch_k0(const GenParams& G, cudaStream_t st);

@@ -12,7 +12,6 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
-#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -295,13 +294,6 @@ struct pft_dplan_s {
     uint32_t k2_group = 0;   // k2_tail: columns j per FFT group
     uint32_t reducers = 0;   // sum tail: CTAs per signal that reduce the residue rows
     uint64_t k1_capacity = 0;  // co-resident K1 CTAs on the device
-    // dynamic K1 (k1d_contract): persistent CTAs over work items, class finishers
-    bool dyn = false;
-    uint32_t nseg = 1, nrb = 1, nch = 0, fft_group = 1;
-    size_t dyn_smem = 0;
-    uint64_t dyn_capacity = 0;  // co-resident dynamic-K1 CTAs on the device (the grid)
-    bool fast_reduce = false;   // sum tail: the signal's last class finisher sums the rows (P2 <= 8)
-    bool sum_kernel = false;    // sum tail: k_sum_rows sums the rows after K1 (P2 > 8)
     bool mu0 = false;
     uint64_t W = 0;
     // device allocations
@@ -345,14 +337,8 @@ struct pft_dplan_s {
     }
 
     size_t slab_elems() const { return (size_t)host.p * host.r; }
-    size_t counters_per_signal() const { return dyn ? P2 + 1 : sum_tail ? P2 + 2 : k2_tail ? 2 : 0; }
-    // dynamic K1: the per-item partials Cpart [P2][nseg][r][P1], then the rows or the K2 slab
-    size_t cpart_elems() const { return dyn ? (size_t)nseg * slab_elems() : 0; }
-    size_t tail_elems() const {
-        return dyn ? (sum_tail ? (size_t)P2 * W : slab_elems())
-                   : (sum_tail ? std::max<size_t>(slab_elems(), (size_t)P2 * W) : slab_elems());
-    }
-    size_t data_elems() const { return cpart_elems() + tail_elems(); }
+    size_t counters_per_signal() const { return sum_tail ? P2 + 2 : k2_tail ? 2 : 0; }
+    size_t data_elems() const { return sum_tail ? std::max<size_t>(slab_elems(), (size_t)P2 * W) : slab_elems(); }
     // workspace layout (kernels.cuh): header, then per signal {control words, data}
     size_t ctl_bytes() const { return pftdev::ws_align(4 * counters_per_signal()); }
     size_t signal_bytes() const { return ctl_bytes() + pftdev::ws_align(data_elems() * sizeof(double2)); }
@@ -507,31 +493,6 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
     auto P2 = d->k2_params(w.Y, w.y_stride, out, w.status);
     P1.arrivals = w.arrivals;
     P1.ctl_stride = w.ctl_stride;
-    if (d->dyn) {
-        double2* rows = w.Y + d->cpart_elems();
-        P1.sum_tail = d->sum_tail ? 1 : 0;
-        P1.nrb = d->nrb;
-        P1.nseg = d->nseg;
-        P1.nch = d->nch;
-        P1.items_per_signal = (uint32_t)(d->P2 * d->nrb * d->nseg);
-        P1.total_items = (uint32_t)(batch * P1.items_per_signal);
-        P1.fft_group = d->fft_group;
-        P1.fast_reduce = d->fast_reduce ? 1 : 0;
-        P1.item_ctr = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(w.bar) + pftdev::kWsItemCtrOffset);
-        P1.Cpart = w.Y;
-        P1.rows = rows;
-        P1.cls = w.arrivals;
-        if (const char* e = std::getenv("PFT_DYN_DEV")) P1.dev_flags = (uint32_t)std::strtoul(e, nullptr, 10);
-        P2.Y = rows;
-        P1.k2 = P2;
-        const uint32_t grid = (uint32_t)std::min<uint64_t>(d->dyn_capacity, P1.total_items);
-        cuda_check(pftdev::launch_k1d(map, P1, d->host.r, grid, d->mu0, st), "K1 (dynamic) launch");
-        if (d->sum_kernel && !(P1.dev_flags & 8))
-            cuda_check(pftdev::launch_sum_rows(P2, (uint32_t)d->P2, rows, w.y_stride, (uint32_t)batch, st), "row sum launch");
-        else if (!d->sum_tail)
-            cuda_check(pftdev::launch_k2(P2, d->host.r, (uint32_t)batch, st), "K2 launch");
-        return;
-    }
     if (d->sum_tail) {
         P1.sum_tail = 1;
         P1.reducers = d->reducers;
@@ -556,97 +517,6 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
     }
     cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
     cuda_check(pftdev::launch_k2(P2, d->host.r, (uint32_t)batch, st), "K2 launch");
-}
-
-// Dynamic-K1 decomposition (k1d_contract): the largest P1 = p / P2 (64-smooth, <= 1024) whose
-// ring + C slab + FFT scratch fit two CTAs per SM -- fewer classes mean fewer residue rows or a
-// smaller K2 -- with a K2 FFT over P2 that fits shared memory when the second pass is K2's.
-// Ring depth first (>= 4 stages on the vector path), then the widest FFT column group.  Column
-// segments per 32-row block make >= 6 items per CTA slot so the claims balance.
-// two dynamic-K1 CTAs per SM, leaving room for the 1 KB reservation of a small co-resident CTA
-// (the row sum of the previous transform)
-constexpr size_t kDynSmemBudget = (228 * 1024) / 2 - 2048;
-
-bool plan_dynamic(pft_dplan_s* d, const HostPlan& H, size_t batch_hint, int n_sms, int pass2, uint64_t force_p2) {
-    const int r = H.r;
-    const uint64_t W = d->W;
-    const bool mu0 = std::all_of(H.phase.begin(), H.phase.end(), [](const cplx& z) { return z == cplx(1.0, 0.0); });
-    const ShardLayout v = shard_layout(H.q, 1, 0);
-    const uint64_t npairs = v.pair_end > v.pair_begin ? v.pair_end - v.pair_begin : 0;
-    const uint32_t nch = (uint32_t)((npairs + pftdev::K1_CP - 1) / pftdev::K1_CP);
-    struct Cand {
-        uint64_t P1 = 0, items = 0, cap = 0;
-        pftdev::FftRadices fr{};
-        uint32_t S = 0, grp = 0, nrb = 0, nseg = 0;
-        size_t smem = 0;
-        bool sum = false;
-    } best;
-    const auto divs = divisors(H.p);
-    for (auto it = divs.rbegin(); it != divs.rend(); ++it) {
-        Cand c;
-        c.P1 = *it;
-        const uint64_t P1 = c.P1, P2 = H.p / P1;
-        if (P1 > 1024) continue;
-        if (force_p2 && P2 != force_p2) continue;
-        if (P1 > 1 && !factor_radices((uint32_t)P1, c.fr)) continue;
-        if (P1 <= 1) c.fr.n = 1;
-        c.sum = pass2 == PFT_PASS2_SUM_TAIL ||
-                (pass2 == PFT_PASS2_AUTO && (batch_hint > 1 || sum_tail_pays(H.N, W, P2, r)));
-        if (!c.sum && !k2_fft_feasible(P2, r)) continue;
-        const uint32_t gmin = c.sum ? (uint32_t)std::max<uint64_t>(1, (P1 + P2 + P1 - 1) / P1) : 1;
-        if (gmin > (uint32_t)r) continue;
-        const int smax = pftdev::k1_tc(r) ? 4 : 5;
-        for (int st = smax; st >= pftdev::k1_min_stages(r) && !c.S; --st)
-            for (uint32_t gq = (uint32_t)r; gq >= gmin && gq >= 1; --gq)
-                if (pftdev::k1d_smem_bytes(r, (uint32_t)P1, (uint32_t)st, gq) <= kDynSmemBudget) {
-                    c.S = (uint32_t)st;
-                    c.grp = gq;
-                    break;
-                }
-        if (!c.S) continue;
-        c.smem = pftdev::k1d_smem_bytes(r, (uint32_t)P1, c.S, c.grp);
-        const int per_sm = pftdev::k1d_max_active_per_sm(r, c.smem, mu0);
-        if (per_sm < 1) continue;
-        c.cap = (uint64_t)per_sm * (uint64_t)n_sms;
-        c.nrb = (uint32_t)((P1 + pftdev::K1_BR - 1) / pftdev::K1_BR);
-        const uint64_t base = std::max<uint64_t>(1, std::max<size_t>(batch_hint, 1) * P2 * c.nrb);
-        // >= 3 items per CTA slot, >= 4 chunks (64 pairs) per item, and a class's partials (the
-        // finisher's read) <= 64 KB
-        uint64_t nseg = std::min<uint64_t>(std::max<uint32_t>(1, nch / 4), (3 * c.cap + base - 1) / base);
-        nseg = std::max<uint64_t>(nseg, 1);
-        while (nseg > 1 && nseg * (uint64_t)r * P1 * sizeof(double2) > 64 * 1024) --nseg;
-        if (const char* e = std::getenv("PFT_DYN_NSEG")) nseg = std::max<uint64_t>(1, std::min<uint64_t>(nch, std::strtoull(e, nullptr, 10)));
-        c.nseg = (uint32_t)nseg;
-        c.items = base * nseg;
-        // the largest P1 with >= 2 items per CTA slot; failing that, the most items
-        const bool enough = c.items >= 2 * c.cap;
-        if (best.P1 == 0 || (enough && best.items < 2 * best.cap) || (!enough && best.items < 2 * best.cap && c.items > best.items))
-            best = c;
-        if (enough) break;
-    }
-    if (best.P1 == 0) return false;
-    const uint64_t P1 = best.P1, P2 = H.p / P1;
-    d->dyn = true;
-    d->P1 = P1;
-    d->P2 = P2;
-    d->fft = best.fr;
-    d->k1_stages = best.S;
-    d->fft_group = best.grp;
-    d->dyn_smem = best.smem;
-    d->dyn_capacity = best.cap;
-    if (const char* e = std::getenv("PFT_DYN_GRID")) d->dyn_capacity = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
-    d->sum_tail = best.sum;
-    d->fast_reduce = best.sum && P2 > 1 && P2 <= 8 && W <= 4u * pftdev::K1_CONSUMER_WARPS * 32;
-    d->sum_kernel = best.sum && P2 > 1 && !d->fast_reduce;
-    d->k2_mode = pftdev::K2_FFT;
-    if (!best.sum) {
-        if (P2 > 1) factor_radices((uint32_t)P2, d->fft2);
-        else d->fft2.n = 1;
-    }
-    d->nch = nch;
-    d->nrb = best.nrb;
-    d->nseg = best.nseg;
-    return true;
 }
 
 }  // namespace
@@ -799,25 +669,15 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     d->host.achieved_epsilon = H.achieved_epsilon;
     d->host.plan_id = H.plan_id;
     d->W = 2 * H.M + 1;
-    PFT_REQUIRE(!opts || opts->reserved == 0, "dplan_create: reserved options must be 0");
+    PFT_REQUIRE(!opts || (opts->reserved[0] == 0 && opts->reserved[1] == 0), "dplan_create: reserved options must be 0");
     const int pass2 = opts ? opts->second_pass : PFT_PASS2_AUTO;
     const int k2_at = opts ? opts->k2_at : PFT_K2_AT_AUTO;
     PFT_REQUIRE(pass2 >= PFT_PASS2_AUTO && pass2 <= PFT_PASS2_K2_L2, "dplan_create: unknown second_pass");
     PFT_REQUIRE(k2_at >= PFT_K2_AT_AUTO && k2_at <= PFT_K2_AT_FUSED, "dplan_create: unknown k2_at");
     PFT_REQUIRE(!opts || (opts->tail_ctas >= 0 && opts->k2_grid_ctas >= 0), "dplan_create: negative CTA count");
     const int tail_ctas = opts ? opts->tail_ctas : 0;
-    const int schedule = opts ? opts->schedule : PFT_K1_SCHEDULE_AUTO;
-    PFT_REQUIRE(schedule >= PFT_K1_SCHEDULE_AUTO && schedule <= PFT_K1_SCHEDULE_DYNAMIC, "dplan_create: unknown schedule");
     uint64_t p2 = opts && opts->p2 ? opts->p2 : 0;
     const size_t batch_hint = opts && opts->batch_hint > 1 ? (size_t)opts->batch_hint : 1;
-    // dynamic K1 unless the caller pins a static choice (P2, a K2 placement, a K2 form other than FFT)
-    if (schedule != PFT_K1_SCHEDULE_STATIC && (!p2 || schedule == PFT_K1_SCHEDULE_DYNAMIC) && k2_at == PFT_K2_AT_AUTO &&
-        (pass2 == PFT_PASS2_AUTO || pass2 == PFT_PASS2_SUM_TAIL || pass2 == PFT_PASS2_K2_FFT) &&
-        (opts == nullptr || opts->k1_stages == 0))
-        plan_dynamic(d.get(), H, batch_hint, prop.multiProcessorCount, pass2, p2);
-    if (schedule == PFT_K1_SCHEDULE_DYNAMIC && !d->dyn)
-        fail(PFT_ERR_UNSUPPORTED, "dplan_create: no dynamic-K1 decomposition for this plan and options");
-    if (!d->dyn) {
     if (!p2 && (pass2 == PFT_PASS2_AUTO || pass2 == PFT_PASS2_SUM_TAIL)) {  // sum tail, when it pays (or forced)
         p2 = choose_p2_sum(H.p, H.r, prop.multiProcessorCount, batch_hint);
         // batched plans (batch_hint > 1) always take the sum tail when it fits: a K2 grid of
@@ -902,7 +762,6 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
             }
         }
     }
-    }  // static schedule
     d->mu0 = std::all_of(H.phase.begin(), H.phase.end(), [](const cplx& z) { return z == cplx(1.0, 0.0); });
 
     // omega_p^t = e^{-2 pi i t / p}, exactly reduced
@@ -981,7 +840,7 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     // sum tail also keeps them within the slots a transform leaves free (capacity - P2):
     // measured 40 reducers 46.4 us, 48 reducers 53.9 us per transform at C2b.  Caller overrides
     // (tail_ctas) are capped the same way.
-    if (!d->dyn && d->k1_capacity > 1) {
+    if (d->k1_capacity > 1) {
         const uint64_t cap = d->sum_tail && d->k1_capacity > d->P2 ? d->k1_capacity - d->P2 : d->k1_capacity - 1;
         d->reducers = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(d->reducers, cap));
     }
@@ -1025,8 +884,7 @@ pft_status pft_launches_per_execute(pft_dplan_t d, int* launches) {
     PFT_API_BEGIN
     dp(d);
     PFT_REQUIRE(launches != nullptr, "launches is null");
-    const pft_dplan_s* x = dp(d);
-    *launches = x->dyn ? ((x->sum_tail && !x->sum_kernel) ? 1 : 2) : (x->fused(1) || x->sum_tail || x->k2_tail) ? 1 : 2;
+    *launches = (dp(d)->fused(1) || dp(d)->sum_tail || dp(d)->k2_tail) ? 1 : 2;
     PFT_API_END
 }
 
@@ -1035,13 +893,6 @@ pft_status pft_dplan_tail_kind(pft_dplan_t d, int* kind) {
     const pft_dplan_s* x = dp(d);
     PFT_REQUIRE(kind != nullptr, "kind is null");
     *kind = x->sum_tail ? 1 : x->k2_tail ? 2 : x->fused(1) ? 3 : 0;
-    PFT_API_END
-}
-
-pft_status pft_dplan_schedule(pft_dplan_t d, int* schedule) {
-    PFT_API_BEGIN
-    PFT_REQUIRE(schedule != nullptr, "schedule is null");
-    *schedule = dp(d)->dyn ? PFT_K1_SCHEDULE_DYNAMIC : PFT_K1_SCHEDULE_STATIC;
     PFT_API_END
 }
 
@@ -1180,7 +1031,6 @@ pft_status pft_execute_partial(pft_dplan_t dh, const pft_c128* d_in_local, int w
     PFT_API_BEGIN
     pft_dplan_s* d = dp(dh);
     PFT_REQUIRE(d_in_local && d_partial, "execute_partial: null buffer");
-    PFT_REQUIRE(!d->dyn, "execute_partial: needs a static-schedule device plan (PFT_K1_SCHEDULE_STATIC)");
     const ShardLayout v = shard_layout(d->host.q, world, rank);
     if (row_stride == 0) row_stride = v.row_len;
     PFT_REQUIRE(row_stride >= v.row_len, "execute_partial: row_stride < local row length");
@@ -1197,7 +1047,6 @@ pft_status pft_finalize(pft_dplan_t dh, const pft_c128* d_partial, size_t batch,
     pft_dplan_s* d = dp(dh);
     if (batch == 0) return PFT_OK;
     PFT_REQUIRE(d_partial && d_out, "finalize: null buffer");
-    PFT_REQUIRE(!d->dyn, "finalize: needs a static-schedule device plan (PFT_K1_SCHEDULE_STATIC)");
     DeviceGuard guard(d->device);
     const auto P = d->k2_params(reinterpret_cast<const double2*>(d_partial), d->slab_elems(),
                                 reinterpret_cast<double2*>(d_out), d->own_status());

@@ -92,67 +92,6 @@ cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t
     return cudaErrorInvalidValue;
 }
 
-int k1d_max_active_per_sm(int r, size_t smem, bool mu0) {
-    switch (r) {
-#define X(n) case n: return k1d_active_r<n>(smem, mu0);
-        PFT_R_CASES(X)
-#undef X
-    }
-    return 0;
-}
-
-cudaError_t launch_k1d(const CUtensorMap& map, const K1Params& P, int r, uint32_t grid, bool mu0, cudaStream_t st) {
-    const size_t smem = k1d_smem_bytes(r, P.P1, P.stages, P.fft_group);
-    switch (r) {
-#define X(n) case n: return launch_k1d_r<n>(map, P, dim3(grid), smem, st, mu0);
-        PFT_R_CASES(X)
-#undef X
-    }
-    return cudaErrorInvalidValue;
-}
-
-// Residue-row sum of the dynamic K1's sum tail: one warp per CTA owns 32 outputs (s = 32 x + lane)
-// and sums the P2 rows in ascending c with 8 loads in flight: deterministic.  Launched right after
-// K1 with programmatic dependent launch: it releases the next launch at once and waits for K1's
-// rows.  One warp, no shared memory, few registers: its CTAs fit beside two dynamic-K1 CTAs, so
-// they never hold an SM slot the next transform's K1 needs.
-constexpr int kSumThreads = 32;
-__global__ void __launch_bounds__(kSumThreads) k_sum_rows(const K2Params Q, uint32_t P2, const double2* rows0,
-                                                         uint64_t y_stride) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const uint32_t b = blockIdx.y;
-    const uint64_t so = (uint64_t)blockIdx.x * 32 + threadIdx.x;
-    if (so >= Q.W) return;
-    const double2* __restrict__ rows = rows0 + (size_t)b * y_stride + so;
-    double2 acc = make_double2(0.0, 0.0);
-    for (uint32_t c0 = 0; c0 < P2; c0 += 8) {
-        double2 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = c0 + u < P2 ? __ldcg(rows + (size_t)(c0 + u) * Q.W) : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (c0 + u < P2) acc = cadd(acc, v[u]);
-    }
-    const double2 o = cmul(acc, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
-    Q.out[(size_t)b * Q.W + so] = o;
-    if (!isfinite(o.x) || !isfinite(o.y)) atomicOr(Q.status, 1);
-}
-
-cudaError_t launch_sum_rows(const K2Params& Q, uint32_t P2, const double2* rows, uint64_t y_stride, uint32_t batch,
-                            cudaStream_t st) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)((Q.W + 31) / 32), batch);
-    cfg.blockDim = dim3(kSumThreads);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_sum_rows, Q, P2, rows, y_stride);
-}
-
 cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st) {
     const uint32_t gx = P.mode == K2_L2 ? (P.k2_ctas ? P.k2_ctas : 148u)
                                          : P.P1;

@@ -110,8 +110,7 @@ class ShardedTransform:
     def dplan(self):
         if self._dplan is None:
             from . import DevicePlan
-            # the split steps (execute_partial / finalize) run the static K1 + K2 pair
-            self._dplan = DevicePlan(self.plan, device=self.device, p2=self._p2, schedule="static")
+            self._dplan = DevicePlan(self.plan, device=self.device, p2=self._p2)
         return self._dplan
 
     def partial(self, d_local: int, d_slab: int, stream: int = 0) -> None:

@@ -140,7 +140,7 @@ def test_sharded_partials_sum_to_unsharded(pft, oracle, N, M, mu, p, world):
     unsharded transform.  Ranks run one after another on this GPU (no inter-kernel waits)."""
     import torch
     plan = pft.build_plan(N, M, mu, p, 1e-12)
-    d = plan.device_plan(schedule="static")
+    d = plan.device_plan()
     a = pft.generate_signal(pft.KIND_UNIFORM, 5, N)
     slab = torch.zeros(plan.p * plan.r, dtype=torch.complex128, device="cuda")
     part = torch.empty_like(slab)
@@ -170,7 +170,7 @@ def test_batched_workspace_and_tail_forms(pft, oracle, form):
           "k2-tail": dict(second_pass="k2-fft", k2_at="tail"),
           "k2-tail-1": dict(second_pass="k2-fft", k2_at="tail", tail_ctas=1),
           "sum": dict(second_pass="sum"), "sum-all-reduce": dict(second_pass="sum", tail_ctas=1 << 20)}[form]
-    d = pft.DevicePlan(plan, schedule="static", **kw)
+    d = pft.DevicePlan(plan, **kw)
     assert d.launches_per_execute() == (2 if form == "k2" else 1)
     fuse = form
     a = pft.generate_signal(pft.KIND_UNIFORM, 9, N * batch)
@@ -213,16 +213,15 @@ def test_autotuned_divisor_plan_parity(pft, oracle):
     assert rel_l2(got, oracle.execute(plan, a)) <= GATE
 
 
-@pytest.mark.parametrize("schedule", ["static", "dynamic"])
 @pytest.mark.parametrize("N,M,mu,p", [(2 ** 16, 256, 0, 256), (2 ** 16, 256, 0, 512), (2 ** 14, 100, -7, 128),
                                      (4096, 64, 5, 64), (4096, 64, -3, 128)])  # P2 = 1: direct output
-def test_batched_small_signals_sum_tail(pft, oracle, N, M, mu, p, schedule):
+def test_batched_small_signals_sum_tail(pft, oracle, N, M, mu, p):
     """C3-style batches (BASELINE configs[2]): a large batch hint gives P2 = 2-4 CTAs per
     signal and the sum tail with W > p (the bins wrap mod p); every signal matches the oracle."""
     import torch
     batch = 5
     plan = pft.build_plan(N, M, mu, p, 1e-12)
-    d = pft.DevicePlan(plan, batch_hint=4096, schedule=schedule)
+    d = pft.DevicePlan(plan, batch_hint=4096)
     assert d.launches_per_execute() == 1 and d.P2 <= 8
     a = pft.generate_signal(pft.KIND_UNIFORM, 33, N * batch)
     x = torch.from_numpy(a).cuda()
@@ -247,7 +246,7 @@ def test_sum_tail_and_k2_forms_agree(pft, oracle, N, M, mu, p):
     ref = oracle.execute(plan, a)
     res = []
     for mode, launches in (("sum", 1), ("k2-fft", 2)):
-        d = pft.DevicePlan(plan, second_pass=mode, k2_at="grid", schedule="static")
+        d = pft.DevicePlan(plan, second_pass=mode, k2_at="grid")
         assert d.launches_per_execute() == launches
         out = torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda")
         d.execute_ptr(x.data_ptr(), out.data_ptr())
@@ -257,9 +256,8 @@ def test_sum_tail_and_k2_forms_agree(pft, oracle, N, M, mu, p):
     assert rel_l2(res[0], res[1]) <= 1e-13
 
 
-@pytest.mark.parametrize("schedule", ["static", "auto"])
 @pytest.mark.parametrize("mode", ["k2-fft", "k2-dot", "k2-direct", "k2-l2", "sum"])
-def test_every_second_pass_form(pft, oracle, mode, schedule):
+def test_every_second_pass_form(pft, oracle, mode):
     """Each second-pass form forced on the same plan (K2 FFT, dot, direct, L2; sum tail) matches
     the oracle: the auto selection only picks among them by speed."""
     import torch
@@ -267,7 +265,7 @@ def test_every_second_pass_form(pft, oracle, mode, schedule):
     plan = pft.build_plan(N, M, mu, p, 1e-12)
     a = pft.generate_signal(pft.KIND_UNIFORM, 12, N)
     x = torch.from_numpy(a).cuda()
-    d = pft.DevicePlan(plan, second_pass=mode, schedule=schedule)
+    d = pft.DevicePlan(plan, second_pass=mode)
     out = torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda")
     for _ in range(2):
         d.execute_ptr(x.data_ptr(), out.data_ptr())
@@ -315,12 +313,11 @@ EDGE = [
 ]
 
 
-@pytest.mark.parametrize("schedule", ["static", "auto"])
 @pytest.mark.parametrize("N,M,mu,p", EDGE)
-def test_degenerate_shapes(pft, oracle, N, M, mu, p, schedule):
+def test_degenerate_shapes(pft, oracle, N, M, mu, p):
     plan = pft.build_plan(N, M, mu, p, 1e-12)
     a = uniform(pft, 17, N)
-    gpu = plan.device_plan(schedule=schedule).execute_host(a)
+    gpu = pft.execute(plan, a).values
     ref = oracle.execute(plan, a)
     assert rel_l2(gpu, ref) <= GATE, plan.json()
 
@@ -339,10 +336,9 @@ def _m_for_terms(pft, r: int, p: int):
     return None
 
 
-@pytest.mark.parametrize("schedule", ["static", "auto"])
 @pytest.mark.parametrize("mu", [0, 1234])
 @pytest.mark.parametrize("r", list(range(2, 26)))
-def test_every_contraction_path(pft, oracle, r, mu, schedule):
+def test_every_contraction_path(pft, oracle, r, mu):
     """Every r instantiation of K1 against the oracle, with and without phase factors: the
     unsplit vector contraction, the two-lane j split (k1_js) and the FP64 tensor-core
     (DMMA) contraction (k1_tc, r = 16..18) all meet the gate."""
@@ -356,5 +352,5 @@ def test_every_contraction_path(pft, oracle, r, mu, schedule):
     plan = pft.build_plan(N, M, mu, p, 1e-12)
     assert plan.r == r
     a = uniform(pft, 100 + r, N)
-    got = plan.device_plan(schedule=schedule).execute_host(a)
+    got = pft.execute(plan, a).values
     assert rel_l2(got, oracle.execute(plan, a)) <= GATE

@@ -26,4 +26,4 @@ out = torch.empty((2 * M + 1) * B, dtype=torch.complex128, device="cuda")
 for _ in range(reps):
     d.execute_ptr(x.data_ptr(), out.data_ptr(), batch=B, in_stride=N, d_ws=ws.data_ptr())
 torch.cuda.synchronize()
-print(cfg, opts, d.P1, d.P2, d.schedule, d.tail_kind(), "status", d.status(d_ws=ws.data_ptr()))
+print(cfg, opts, d.P1, d.P2, d.tail_kind(), "status", d.status(d_ws=ws.data_ptr()))

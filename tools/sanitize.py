@@ -19,18 +19,15 @@ import paper_2008_12559_b200 as pft  # noqa: E402
 
 FORMS = [
     # (label, N, M, mu, p, batch, DevicePlan options)
-    ("static sum tail, many classes", 2 ** 18, 200, 33, 2 ** 11, 1, dict(schedule="static", second_pass="sum")),
-    ("static sum tail, fast reduction (tensor cores)", 2 ** 14, 64, 0, 2 ** 8, 3, dict(schedule="static", batch_hint=64)),
-    ("static sum tail, one class per signal", 4096, 64, 5, 64, 3, dict(schedule="static", batch_hint=64)),
-    ("static K2 grid (FFT form)", 2 ** 18, 2 ** 11, -7, 2 ** 12, 1, dict(schedule="static", second_pass="k2-fft", k2_at="grid")),
-    ("static K2 dot form", 2 ** 18, 2 ** 9, 7, 2 ** 12, 1, dict(schedule="static", second_pass="k2-dot")),
-    ("static K2 direct form", 2 ** 18, 2 ** 9, 7, 2 ** 12, 1, dict(schedule="static", second_pass="k2-direct")),
-    ("static K2 L2 form", 2 ** 18, 2 ** 6, 7, 2 ** 12, 1, dict(schedule="static", second_pass="k2-l2")),
-    ("static K2 tail (last arrivals)", 2 ** 18, 2 ** 9, -5, 2 ** 12, 1, dict(schedule="static", second_pass="k2-fft", k2_at="tail")),
-    ("static fused K2 (grid barrier)", 2 ** 16, 128, 77, 2 ** 12, 2, dict(schedule="static", second_pass="k2-fft", k2_at="fused")),
-    ("dynamic sum tail + row-sum kernel", 2 ** 18, 200, 33, 2 ** 11, 1, dict(schedule="dynamic", second_pass="sum")),
-    ("dynamic sum tail, fast reduction", 2 ** 14, 64, 0, 2 ** 8, 3, dict(schedule="dynamic", batch_hint=64)),
-    ("dynamic K2 grid", 2 ** 18, 2 ** 11, -7, 2 ** 12, 1, dict(schedule="dynamic", second_pass="k2-fft")),
+    ("sum tail, many classes", 2 ** 18, 200, 33, 2 ** 11, 1, dict(second_pass="sum")),
+    ("sum tail, fast reduction (tensor cores)", 2 ** 14, 64, 0, 2 ** 8, 3, dict(batch_hint=64)),
+    ("sum tail, one class per signal", 4096, 64, 5, 64, 3, dict(batch_hint=64)),
+    ("K2 grid (FFT form)", 2 ** 18, 2 ** 11, -7, 2 ** 12, 1, dict(second_pass="k2-fft", k2_at="grid")),
+    ("K2 dot form", 2 ** 18, 2 ** 9, 7, 2 ** 12, 1, dict(second_pass="k2-dot")),
+    ("K2 direct form", 2 ** 18, 2 ** 9, 7, 2 ** 12, 1, dict(second_pass="k2-direct")),
+    ("K2 L2 form", 2 ** 18, 2 ** 6, 7, 2 ** 12, 1, dict(second_pass="k2-l2")),
+    ("K2 tail (last arrivals)", 2 ** 18, 2 ** 9, -5, 2 ** 12, 1, dict(second_pass="k2-fft", k2_at="tail")),
+    ("fused K2 (grid barrier)", 2 ** 16, 128, 77, 2 ** 12, 2, dict(second_pass="k2-fft", k2_at="fused")),
 ]
 
 
@@ -59,13 +56,13 @@ def run_2d() -> float:
     plan = pft.build_plan_2d(256, 256, 8, 8, 3, -5)
     a = np.random.default_rng(3).random((256, 256)).astype(np.complex128)
     got = pft.execute_2d(plan, a).values
-    ref = oracle.execute_2d(plan, a)
+    ref = oracle.execute_2d(plan.plan1, plan.plan2, a)
     return float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
 
 
 def run_sharded() -> float:
     plan = pft.build_plan(2 ** 18, 2 ** 9, 11, 2 ** 12, 1e-12)
-    d = pft.DevicePlan(plan, schedule="static")
+    d = pft.DevicePlan(plan)
     a = pft.generate_signal(pft.KIND_UNIFORM, 5, plan.N)
     slab = torch.zeros(plan.p * plan.r, dtype=torch.complex128, device="cuda")
     part = torch.empty_like(slab)
