@@ -349,6 +349,26 @@ pft_status pft_anomaly(pft_dplan_t d, const double* x, uint64_t k, uint64_t* idx
 /* (N, M, mu) of a device plan. */
 pft_status pft_dplan_shape(pft_dplan_t d, uint64_t* N, uint64_t* M, int64_t* mu);
 
+/* ------------------------------------------------------------------ verification (SPEC.md oracle module)
+ * naive_dft on the GPU: out[s] = sum_n a[n] e^{-2 pi i (first_m + s) n / N}, s in [count), every angle
+ * reduced exactly in integers ((m n) mod N) before one sincospi per term.
+ * O(N count); used by the CLI's --verify, the anomaly pipeline's "fft" source and bench's naive
+ * column -- desk-scale ground truth on the device, not a CPU path. */
+pft_status pft_naive_dft_device(const pft_c128* d_in, uint64_t N, int64_t first_m, uint64_t count, pft_c128* d_out,
+                                void* stream);
+pft_status pft_naive_dft_host(const pft_c128* h_in, uint64_t N, int64_t first_m, uint64_t count, pft_c128* h_out);
+/* compare(actual, estimate, l1_input, epsilon, two_d_bound) -> ErrorReport: relative_l2 =
+ * ||estimate - actual|| / ||actual|| (0 if both are zero, +inf if only actual is), max_abs, bound =
+ * l1_input * eps (1-D, Theorem 2) or l1_input * (eps^2 + 2 eps) (2-D, Theorem 4). */
+typedef struct pft_error_report {
+    double relative_l2, max_abs, l1_input, bound;
+    int bound_satisfied;
+} pft_error_report;
+pft_status pft_compare(const pft_c128* actual, const pft_c128* estimate, uint64_t n, double l1_input, double epsilon,
+                       int two_d_bound, pft_error_report* report);
+/* sum |a_i| (types.hpp:92-96) */
+pft_status pft_l1_norm(const pft_c128* a, uint64_t n, double* l1);
+
 pft_status pft_device_count(int* n);
 
 #ifdef __cplusplus

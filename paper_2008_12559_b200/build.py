@@ -24,6 +24,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "build"
 LIB = PKG / "libpft_b200.so"
+CLI = PKG / "pft"  # the command-line surface (SPEC.md cli module), linked against LIB
 TABLE = PKG / "data" / "scope_table_v1.pftt"
 INCLUDE = ROOT / "include"
 
@@ -109,6 +110,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         _run([NVCC, "-shared", *ARCH, "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp", "-ldl"], verbose)
         os.replace(tmp, LIB)
         stamp_file.write_text(stamp)
+    # the CLI (host code compiled by nvcc: it times with CUDA events), rpath'd to the library
+    cli_src = CSRC / "cli" / "pft_cli.cu"
+    cli_stamp = BUILD / "cli.stamp"
+    cli_key = _deps_hash(cli_src) + LIB.stat().st_mtime_ns.__str__()
+    if cli_src.exists() and (force or not CLI.exists() or not cli_stamp.exists() or cli_stamp.read_text() != cli_key):
+        tmp = CLI.with_suffix(".tmp")
+        _run([NVCC, "-std=c++20", "-O2", *ARCH, "-I", INCLUDE, cli_src, "-o", tmp, "-L", PKG, "-lpft_b200",
+              "-Xlinker", "-rpath,$ORIGIN", "-ldl"], verbose)
+        os.replace(tmp, CLI)
+        cli_stamp.write_text(cli_key)
     # drop stale objects
     live = {o.name for o in objs}
     for o in BUILD.glob("*.o"):

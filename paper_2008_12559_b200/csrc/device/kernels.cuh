@@ -205,6 +205,8 @@ cudaError_t configure_k2(int r, uint32_t P2);
 cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t batch, bool mu0, cudaStream_t st);
 cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st);
 cudaError_t launch_k0(const GenParams& G, cudaStream_t st);
+cudaError_t launch_naive_dft(const double2* a, uint64_t N, int64_t first, uint64_t count, double2* out,
+                             cudaStream_t st);
 cudaError_t launch_transpose(const double2* in, double2* out, uint64_t rows, uint64_t cols, cudaStream_t st);
 
 }  // namespace pftdev

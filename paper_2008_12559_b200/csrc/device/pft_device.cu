@@ -1120,6 +1120,44 @@ pft_status pft_execute_host(pft_dplan_t dh, const pft_c128* h_in, size_t batch, 
     PFT_API_END
 }
 
+pft_status pft_naive_dft_device(const pft_c128* d_in, uint64_t N, int64_t first_m, uint64_t count, pft_c128* d_out,
+                                void* stream) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(N >= 1 && d_in && (d_out || count == 0), "naive_dft: bad arguments");
+    if (count == 0) return PFT_OK;
+    if (usable_device_count() == 0) fail(PFT_ERR_NO_DEVICE, "no CUDA device visible (this library has no CPU fallback)");
+    cuda_check(pftdev::launch_naive_dft(reinterpret_cast<const double2*>(d_in), N, first_m, count,
+                                        reinterpret_cast<double2*>(d_out), static_cast<cudaStream_t>(stream)),
+               "naive DFT launch");
+    PFT_API_END
+}
+
+pft_status pft_naive_dft_host(const pft_c128* h_in, uint64_t N, int64_t first_m, uint64_t count, pft_c128* h_out) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(N >= 1 && h_in && (h_out || count == 0), "naive_dft_host: bad arguments");
+    if (count == 0) return PFT_OK;
+    if (usable_device_count() == 0) fail(PFT_ERR_NO_DEVICE, "no CUDA device visible (this library has no CPU fallback)");
+    struct Bufs {
+        void *in = nullptr, *out = nullptr;
+        cudaStream_t st = nullptr;
+        ~Bufs() {
+            if (st) cudaStreamDestroy(st);
+            cudaFree(in);
+            cudaFree(out);
+        }
+    } b;
+    cuda_check(cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaMalloc(&b.in, N * sizeof(pft_c128)), "cudaMalloc(input)");
+    cuda_check(cudaMalloc(&b.out, count * sizeof(pft_c128)), "cudaMalloc(output)");
+    cuda_check(cudaMemcpyAsync(b.in, h_in, N * sizeof(pft_c128), cudaMemcpyHostToDevice, b.st), "H2D input");
+    cuda_check(pftdev::launch_naive_dft(static_cast<const double2*>(b.in), N, first_m, count,
+                                        static_cast<double2*>(b.out), b.st),
+               "naive DFT launch");
+    cuda_check(cudaMemcpyAsync(h_out, b.out, count * sizeof(pft_c128), cudaMemcpyDeviceToHost, b.st), "D2H output");
+    cuda_check(cudaStreamSynchronize(b.st), "stream synchronize");
+    PFT_API_END
+}
+
 pft_status pft_generate_device(const pft_signal_desc* desc, pft_c128* d_out, uint64_t count, void* stream) {
     PFT_API_BEGIN
     PFT_REQUIRE(desc && (d_out || count == 0), "generate_device: bad arguments");

@@ -129,6 +129,58 @@ cudaError_t launch_transpose(const double2* in, double2* out, uint64_t rows, uin
     return cudaGetLastError();
 }
 
+// Exact-angle direct DFT (naive_dft; Eq. (1)): out[s] = sum_n a[n] e^{-2 pi i m n / N}
+// for m = first + s, with (m n) mod N carried exactly in integers (k_{n+T} = k_n + (m T mod N) mod N)
+// and one sincospi per term on the exactly reduced angle (no angle recurrence).
+// One CTA per bin; lane-strided partial sums then a fixed shuffle / shared-memory tree:
+// deterministic.  O(N (2M+1)) work: the CLI's --verify, the anomaly pipeline's "fft" source and
+// the bench's naive column run it at desk scale.
+constexpr int kNaiveThreads = 256;
+__global__ void __launch_bounds__(kNaiveThreads) k_naive_dft(const double2* __restrict__ a, uint64_t N,
+                                                            int64_t first, double2* __restrict__ out) {
+    __shared__ double2 part[kNaiveThreads / 32];
+    const int64_t m = first + (int64_t)blockIdx.x;
+    const uint64_t mm = (uint64_t)(((m % (int64_t)N) + (int64_t)N) % (int64_t)N);  // m mod N
+    const uint64_t t = threadIdx.x;
+    uint64_t k = (uint64_t)(((unsigned __int128)mm * t) % N);                       // (m t) mod N
+    const uint64_t step = (uint64_t)(((unsigned __int128)mm * kNaiveThreads) % N);  // (m T) mod N
+    const double invN2 = 2.0 / (double)N;
+    double2 acc = make_double2(0.0, 0.0);
+    for (uint64_t n = t; n < N; n += kNaiveThreads) {
+        double sn, cs;
+        sincospi(-(double)k * invN2, &sn, &cs);  // e^{-2 pi i k / N}
+        const double2 x = __ldg(a + n);
+        acc.x = fma(x.x, cs, fma(-x.y, sn, acc.x));
+        acc.y = fma(x.x, sn, fma(x.y, cs, acc.y));
+        k += step;
+        if (k >= N) k -= N;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    }
+    if ((t & 31) == 0) part[t >> 5] = acc;
+    __syncthreads();
+    if (t == 0) {
+        double2 tot = part[0];
+        for (int w = 1; w < kNaiveThreads / 32; ++w) tot = cadd(tot, part[w]);
+        out[blockIdx.x] = tot;
+    }
+}
+
+cudaError_t launch_naive_dft(const double2* a, uint64_t N, int64_t first, uint64_t count, double2* out,
+                             cudaStream_t st) {
+    for (uint64_t done = 0; done < count;) {  // grid.x <= 2^31 - 1 bins per launch
+        const uint64_t n = count - done < (1ull << 30) ? count - done : (1ull << 30);
+        k_naive_dft<<<(unsigned)n, kNaiveThreads, 0, st>>>(a, N, first + (int64_t)done, out + done);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        done += n;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_k0(const GenParams& G, cudaStream_t st) {
     const int threads = 256;
     uint64_t blocks = (G.count + threads - 1) / threads;

@@ -1,6 +1,7 @@
 // capi_host.cpp -- extern "C" entry points for the host-side modules (minimax, table,
 // planner, synthetic inputs).  Exceptions never cross the boundary: each entry point
 // maps pft::detail::Error to its pft_status and records the message for pft_last_error.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -345,6 +346,35 @@ pft_status pft_generate_host(const pft_signal_desc* d, pft_c128* out, uint64_t c
         }
         out[i] = {v.real(), v.imag()};
     }
+    PFT_API_END
+}
+
+pft_status pft_l1_norm(const pft_c128* a, uint64_t n, double* l1) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(l1 != nullptr && (a != nullptr || n == 0), "l1_norm: bad arguments");
+    double s = 0.0;
+    for (uint64_t i = 0; i < n; ++i) s += std::hypot(a[i].re, a[i].im);  // ascending i
+    *l1 = s;
+    PFT_API_END
+}
+
+// SPEC.md:361-369 (compare -> ErrorReport), with its zero-denominator convention (:364, :376).
+pft_status pft_compare(const pft_c128* actual, const pft_c128* estimate, uint64_t n, double l1_input, double epsilon,
+                       int two_d_bound, pft_error_report* report) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(report != nullptr && ((actual && estimate) || n == 0), "compare: bad arguments");
+    double num = 0.0, den = 0.0, mx = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const double dr = estimate[i].re - actual[i].re, di = estimate[i].im - actual[i].im;
+        num += dr * dr + di * di;
+        den += actual[i].re * actual[i].re + actual[i].im * actual[i].im;
+        mx = std::max(mx, std::hypot(dr, di));
+    }
+    report->relative_l2 = den > 0.0 ? std::sqrt(num / den) : (num > 0.0 ? INFINITY : 0.0);
+    report->max_abs = mx;
+    report->l1_input = l1_input;
+    report->bound = l1_input * (two_d_bound ? epsilon * epsilon + 2.0 * epsilon : epsilon);
+    report->bound_satisfied = mx <= report->bound ? 1 : 0;
     PFT_API_END
 }
 
