@@ -145,6 +145,20 @@ def omp_threads(n: int) -> None:
         pass
 
 
+def host_cpu() -> dict:
+    """CPU model, logical CPUs and the OpenMP team size of the CPU legs."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(),
+            "omp_num_threads": int(os.environ.get("OMP_NUM_THREADS", "0")) or os.cpu_count()}
+
+
 def cpu_oracle_rate(pft_mod, plan, a, budget_s: float):
     """Transforms/s of the CPU oracle (all host threads) on the same plan and input."""
     import oracle
@@ -197,7 +211,8 @@ def run_reference(args):
                                                          if args.config in BATCH else "")},
         "input_gbs": value * 16 * N / 1e9,
         "cpu_baseline": {"value": value, "unit": "transforms/s", "cores": cores, "kind": "port",
-                         "sample": f"{steps} full transforms (oracle/oracle.cpp, OpenMP {cores} threads)"},
+                         "sample": f"{steps} full transforms (oracle/oracle.cpp, OpenMP {cores} threads)",
+                         **host_cpu()},
         "e2e": {"value": value, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -316,8 +331,14 @@ def run_ours(args):
     lat_graph = capture(lambda i: d.execute_ptr(bufs[i % nbuf].data_ptr(), out.data_ptr(), batch=B, in_stride=N,
                                                 d_ws=ws[0].data_ptr(), stream=sp, overlap=overlap), n_lat)
     latency_us = timed(lat_graph) / n_lat * 1e3
-    # isolated latency: ONE execute on an idle device (synchronised before, CUDA events around
-    # it, no overlap with any other transform), input rotated so it is not L2-resident; median
+    # isolated latency: executes WITHOUT the overlap flag, so each starts only after the previous
+    # one completed (no two transforms share the device) -- K executes captured in a graph, device
+    # time per execute (launch gaps of the graph included, host API overhead not)
+    iso_graph = capture(lambda i: d.execute_ptr(bufs[(i + 1) % nbuf].data_ptr(), out.data_ptr(), batch=B, in_stride=N,
+                                                d_ws=ws[0].data_ptr(), stream=sp), n_lat)
+    latency_iso_us = timed(iso_graph) / n_lat * 1e3
+    # and one call on an idle device from the host: synchronise, CUDA events around one
+    # pft_execute (host API overhead included); median
     iso = []
     for i in range(max(5, min(args.steps, 30))):
         torch.cuda.synchronize(dev)
@@ -330,7 +351,7 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         iso.append(a0.elapsed_time(a1) * 1e3)
     iso.sort()
-    latency_iso_us = iso[len(iso) // 2]
+    latency_call_us = iso[len(iso) // 2]
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -412,7 +433,7 @@ def run_ours(args):
                 rate, n, el = cpu_oracle_rate(pft, plan, a_host, args.cpu_seconds)
                 cpu = {"value": rate, "unit": "transforms/s", "cores": os.cpu_count(), "kind": "port",
                        "sample": f"{n} full {args.config} transforms (one signal each) in {el:.1f} s "
-                                 f"(oracle/oracle.cpp, OpenMP {os.cpu_count()} threads)"}
+                                 f"(oracle/oracle.cpp, OpenMP {os.cpu_count()} threads)", **host_cpu()}
                 omp_threads(1)  # report the 1-thread rate as well
                 r1, n1, el1 = cpu_oracle_rate(pft, plan, a_host, min(args.cpu_seconds, 5.0))
                 omp_threads(os.cpu_count())
@@ -441,6 +462,7 @@ def run_ours(args):
                                      "single stream; execute i+1's K1 starts streaming while execute "
                                      "i finishes, via programmatic dependent launch"},
             "latency_us_isolated": latency_iso_us,
+            "latency_us_single_call": latency_call_us,
             "latency_us_chained": latency_us,
             "parity_rel_l2": parity["rel_l2_vs_oracle"] if parity else None,
             "parity": parity,

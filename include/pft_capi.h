@@ -173,8 +173,14 @@ typedef struct pft_dplan_opts {
     int k2_at;           /* PFT_K2_AT_*                                                        */
     int tail_ctas;       /* sum-tail reducers / K2-tail workers per signal (0 = plan); always
                             capped below the co-resident K1 capacity (forward progress)       */
-    int k2_grid_ctas;    /* grid width of the PFT_PASS2_K2_L2 form (0 = SM count)              */
-    int reserved[2];     /* must be 0                                                          */
+    int k2_grid_ctas;    /* K2 grid width: the PFT_PASS2_K2_L2 form (0 = SM count); the
+                            PFT_PASS2_K2_FFT form on its own grid: > 0 = a grid of that many
+                            CTAs looping over m1 (0 = the plan's choice)                      */
+    int k1_split;        /* 0: an isolated execute (no PFT_EXEC_OVERLAP_PREVIOUS) whose K1 grid
+                            fills at most half of the SM slots runs two CTAs (a thread-block
+                            cluster) per residue class, each streaming half of the columns and
+                            summing their C slabs over distributed shared memory; 1: never    */
+    int reserved;        /* must be 0                                                          */
     uint64_t batch_hint; /* typical batch per execute (0/1 = single signal): sizes the K1 grid */
 } pft_dplan_opts;
 

@@ -539,10 +539,13 @@ class DevicePlan:
     second_pass: "auto" | "sum" (sum tail in K1) | "k2-fft" | "k2-dot" | "k2-direct" | "k2-l2"
     k2_at: where the k2-fft form runs: "auto" | "grid" (own launch) | "tail" (K1's last
     arrivals) | "fused" (K1 behind a grid barrier).  tail_ctas: sum-tail reducers / K2-tail
-    workers per signal (0 = plan).  batch_hint: typical batch per execute."""
+    workers per signal (0 = plan).  batch_hint: typical batch per execute.  split: isolated
+    executes may run two K1 CTAs (a cluster) per residue class (PFT_EXEC_OVERLAP_PREVIOUS
+    executes never do)."""
 
     def __init__(self, plan: PftPlan, device: int = 0, p2: int = 0, k1_stages: int = 0, second_pass: str = "auto",
-                 k2_at: str = "auto", tail_ctas: int = 0, k2_grid_ctas: int = 0, batch_hint: int = 1):
+                 k2_at: str = "auto", tail_ctas: int = 0, k2_grid_ctas: int = 0, batch_hint: int = 1,
+                 split: bool = True):
         self.plan = plan
         opts = _capi.DPlanOpts()
         opts.device = device
@@ -552,6 +555,7 @@ class DevicePlan:
         opts.k2_at = K2_AT[k2_at]
         opts.tail_ctas = tail_ctas
         opts.k2_grid_ctas = k2_grid_ctas
+        opts.k1_split = 0 if split else 1
         opts.batch_hint = batch_hint
         h = C.c_void_p()
         _check(lib().pft_dplan_create(plan.handle, C.byref(opts), C.byref(h)))

@@ -26,7 +26,8 @@ class PlanInfo(C.Structure):
 
 class DPlanOpts(C.Structure):
     _fields_ = [("device", C.c_int), ("p2", C.c_uint64), ("k1_stages", C.c_int), ("second_pass", C.c_int),
-                ("k2_at", C.c_int), ("tail_ctas", C.c_int), ("k2_grid_ctas", C.c_int), ("reserved", C.c_int * 2),
+                ("k2_at", C.c_int), ("tail_ctas", C.c_int), ("k2_grid_ctas", C.c_int), ("k1_split", C.c_int),
+                ("reserved", C.c_int),
                 ("batch_hint", C.c_uint64)]
 
 

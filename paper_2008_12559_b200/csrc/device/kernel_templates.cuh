@@ -22,6 +22,7 @@
 //
 // Summation orders are fixed (lane-strided partial sums + xor-butterfly), so results
 // are deterministic run to run.
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -32,6 +33,7 @@
 #include "tma.cuh"
 
 namespace pftdev {
+namespace cg = cooperative_groups;
 
 // Grid-wide barrier for K1's fused K2 tail (all CTAs are co-resident: cooperative launch).
 // Self-resetting: the last arriver zeroes the count and bumps the generation, so the state
@@ -627,16 +629,21 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     __syncthreads();  // barriers initialised: the producer starts streaming immediately
     // sum tail: this thread's entry of the tail's twiddle tables, fetched now so its latency
     // hides behind the stream (entry t < P1: omega_p^{t c}; P1 <= t < P1 + P2: omega_P2^{t - P1})
+    // split > 1 (an isolated transform): a cluster of `split` CTAs per residue class, CTA `rank`
+    // streaming its share of the column chunks; the shares' C slabs are summed over DSMEM below
+    const uint32_t split = P.split > 1 ? P.split : 1;
+    const uint32_t rank = blockIdx.x % split;
+    const uint32_t c = blockIdx.x / split;  // residue class k = c (mod P2)
+    const uint32_t b = blockIdx.y;          // signal
     double2 tail_tw = make_double2(0.0, 0.0);
     if (P.sum_tail && (uint32_t)tid < P.P1 + P.P2) {
         const uint32_t t = tid;
-        tail_tw = __ldg(P.omega + (t < P.P1 ? (size_t)t * blockIdx.x : (size_t)(t - P.P1) * P.P1));
+        tail_tw = __ldg(P.omega + (t < P.P1 ? (size_t)t * c : (size_t)(t - P.P1) * P.P1));
     }
-
-    const uint32_t c = blockIdx.x;  // residue class k = c (mod P2)
-    const uint32_t b = blockIdx.y;  // signal
     const uint32_t npairs = P.gp_end > P.gp0 ? P.gp_end - P.gp0 : 0;
-    const uint32_t nch = (npairs + K1_CP - 1) / K1_CP;
+    const uint32_t nch_all = (npairs + K1_CP - 1) / K1_CP;
+    const uint32_t ch_lo = (uint32_t)((uint64_t)nch_all * rank / split), ch_hi = (uint32_t)((uint64_t)nch_all * (rank + 1) / split);
+    const uint32_t nch = ch_hi - ch_lo;  // this CTA's chunks [ch_lo, ch_hi) of every row
     const uint32_t nrb = (P.P1 + K1_BR - 1) / K1_BR;
     const uint32_t total = nch * nrb;
 
@@ -644,7 +651,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         // ---- producer: one elected lane streams front/mirror boxes + table slices
         if (lane == 0 && total > 0) {
             prefetch_tensormap(&tmap);
-            uint32_t s = 0, ph = 0, rb = 0, ch = 0;  // slot, its phase; row batch, chunk
+            uint32_t s = 0, ph = 0, rb = 0, ch = ch_lo;  // slot, its phase; row batch, chunk
             for (uint32_t it = 0; it < total; ++it) {
                 if (it >= S) mbar_wait(&empty[s], ph ^ 1u);
                 unsigned char* st = ring + (size_t)s * STAGE;
@@ -670,8 +677,8 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                     s = 0;
                     ph ^= 1u;
                 }
-                if (++ch == nch) {
-                    ch = 0;
+                if (++ch == ch_hi) {
+                    ch = ch_lo;
                     ++rb;
                 }
             }
@@ -696,12 +703,12 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                 // unpaired columns l = 0 (all lanes) and l = q/2 (t4 = 1): loads issued now,
                 // consumed after the chunk loop
                 double2 x0 = make_double2(0.0, 0.0), xh = make_double2(0.0, 0.0);
-                if (k1 < P.P1) {
+                if (k1 < P.P1 && rank == 0) {
                     const double2* row = P.a + (size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride;
                     if (P.single0_col >= 0) x0 = __ldg(row + P.single0_col);
                     if (t4 == 1 && P.singleh_col >= 0) xh = __ldg(row + P.singleh_col);
                 }
-                for (uint32_t ch = 0; ch < nch; ++ch) {
+                for (uint32_t ch = ch_lo; ch < ch_hi; ++ch) {
                     mbar_wait(&full[s], ph);
                     __syncwarp();
                     const uint32_t valid = min((uint32_t)K1_CP, npairs - ch * K1_CP);
@@ -732,11 +739,11 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
             const uint32_t k1 = rb * K1_BR + rin;
             // unpaired columns (l = 0 on the lanes li < JS, l = q/2 on li = JS): issue the load
             // now, consume it after the chunk loop so its DRAM latency is hidden
-            const int scol = li < JS ? P.single0_col : (li == JS ? P.singleh_col : -1);
+            const int scol = rank != 0 ? -1 : li < JS ? P.single0_col : (li == JS ? P.singleh_col : -1);
             double2 xs = make_double2(0.0, 0.0);
             if (k1 < P.P1 && scol >= 0)
                 xs = __ldg(P.a + (size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride + scol);
-            for (uint32_t ch = 0; ch < nch; ++ch) {
+            for (uint32_t ch = ch_lo; ch < ch_hi; ++ch) {
                 mbar_wait(&full[s], ph);
                 // Reconverge before touching the stage: lane 0's `empty` arrive below leaves
                 // the warp diverged, and reading a stage from a diverged warp was observed to
@@ -765,6 +772,18 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     // get scheduled and run its prologue while this grid finishes its FFT tail.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     __syncthreads();
+    if (split > 1) {
+        // the cluster's shares of C_c: rank 0 adds rank 1's slab from distributed shared memory
+        // (fixed order: own + remote), then rank 1 leaves; rank 0 runs the FFT pass and the tail
+        cg::cluster_group cluster = cg::this_cluster();
+        cluster.sync();
+        if (rank == 0) {
+            const double2* remote = cluster.map_shared_rank(Cs, 1u);
+            for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) Cs[idx] = cadd(Cs[idx], remote[idx]);
+        }
+        cluster.sync();  // rank 1's shared memory stays alive until rank 0 has read it
+        if (rank != 0) return;
+    }
     // C = w_j acc_j: the vector path applies w_j at the row store; the tensor-core path folds
     // it into the first FFT stage's loads (or one pass when there is no FFT)
     if (k1_tc(R) && P.P1 <= 1) {
@@ -932,6 +951,61 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
         out[s] = v;
         if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
     }
+}
+
+// K2 FFT form on a narrow grid (K2Params.k2_ctas CTAs per signal) that loops over m1: few enough
+// CTAs to be resident beside the next transform's K1 (launched when every K2 CTA has started),
+// so K2's latency-bound work overlaps that K1's stream instead of holding its SM slots.  The
+// post powers ((m - mu)/p)^j are formed in registers by ascending repeated multiplication (as the
+// planner forms post_powers; x = (m - mu) * (1/p) is exact for power-of-two p, within an ulp
+// otherwise) instead of W * r dependent table loads.
+template <int R>
+__global__ void __launch_bounds__(K2_THREADS) k2_fft_loop(K2Params P) {
+    extern __shared__ __align__(16) double2 zs[];
+    double2* Z = zs;                              // [R][P2]
+    double2* scratch = zs + (size_t)R * P.P2;     // [R][P2]
+    double2* tw2 = scratch + (size_t)R * P.P2;    // omega_P2^t
+    double2* pre = tw2 + P.P2;                    // omega_p^{m1 c}
+    const uint32_t b = blockIdx.y;
+    if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    for (uint32_t c = threadIdx.x; c < P.P2; c += blockDim.x) tw2[c] = __ldg(P.omega + (size_t)c * P.P1);
+    const int64_t Mh = (int64_t)((P.W - 1) / 2);
+    bool waited = false;
+    double2* __restrict__ out = P.out + (size_t)b * P.W;
+    for (uint32_t m1 = blockIdx.x; m1 < P.P1; m1 += gridDim.x) {
+        const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
+        if (s0 >= P.W) continue;  // no output slot maps to this m1 (block-uniform)
+        for (uint32_t c = threadIdx.x; c < P.P2; c += blockDim.x) pre[c] = __ldg(P.omega + (size_t)m1 * c);  // m1 c < p
+        if (!waited) {  // K1's slab complete and visible
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            waited = true;
+        }
+        __syncthreads();
+        load_twiddled_slab<R>(P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R, P.P2, m1, pre, Z);
+        __syncthreads();
+        const double2* res = Z;
+        if (P.P2 > 1) res = fft_columns(Z, scratch, R, P.fft2, SmemTwiddles{tw2});
+        for (uint64_t s = s0 + (uint64_t)P.P1 * threadIdx.x; s < P.W; s += (uint64_t)P.P1 * blockDim.x) {
+            uint64_t mp = P.first_mod_p + s % P.p;
+            if (mp >= P.p) mp -= P.p;
+            const uint32_t m2 = (uint32_t)(mp / P.P1);
+            const double x = (double)((int64_t)s - Mh) * P.inv_p;
+            double2 acc = res[m2];
+            double tp = x;
+#pragma unroll
+            for (int j = 1; j < R; ++j) {  // ascending j
+                const double2 v = res[(size_t)j * P.P2 + m2];
+                acc.x = fma(v.x, tp, acc.x);
+                acc.y = fma(v.y, tp, acc.y);
+                if (j + 1 < R) tp *= x;
+            }
+            const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+            out[s] = v;
+            if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
+        }
+        __syncthreads();  // smem reuse by the next m1
+    }
+    if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // K2 (dot form, few outputs per m1): only the ~W/P1 bins this CTA owns are needed, so
@@ -1123,7 +1197,7 @@ cudaError_t launch_k1_r(const CUtensorMap& map, const K1Params& P, dim3 grid, si
     cfg.blockDim = dim3(K1_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     unsigned n = 0;
     if (P.pdl) {
         attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1133,6 +1207,13 @@ cudaError_t launch_k1_r(const CUtensorMap& map, const K1Params& P, dim3 grid, si
     if (P.fused) {  // the grid barrier needs every CTA resident
         attr[n].id = cudaLaunchAttributeCooperative;
         attr[n].val.cooperative = 1;
+        ++n;
+    }
+    if (P.split > 1) {  // clusters of `split` CTAs per residue class
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = P.split;
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
         ++n;
     }
     cfg.attrs = attr;
@@ -1180,6 +1261,7 @@ cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
         cfg.blockDim = dim3(K2L_THREADS);
         return cudaLaunchKernelEx(&cfg, k2_l2_post<R>, P);
     }
+    if (P.mode == K2_FFT && P.k2_ctas > 0) return cudaLaunchKernelEx(&cfg, k2_fft_loop<R>, P);
     if (P.mode == K2_FFT) return cudaLaunchKernelEx(&cfg, k2_fft_post<R>, P);
     if (P.mode == K2_DOT) return cudaLaunchKernelEx(&cfg, k2_dot_post<R>, P);
     return cudaLaunchKernelEx(&cfg, k2_direct_post<R>, P);
@@ -1188,6 +1270,8 @@ cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
 template <int R>
 cudaError_t configure_k2_r(size_t smem) {
     cudaError_t e = cudaFuncSetAttribute(k2_fft_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k2_fft_loop<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k2_dot_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }

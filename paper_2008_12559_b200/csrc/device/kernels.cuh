@@ -80,7 +80,7 @@ struct K2Params {
     double inv_p;                  // 1 / p
     uint32_t first_mod_p1;         // (mu - M) mod P1
     int mode;                      // K2_DIRECT / K2_FFT / K2_DOT
-    uint32_t k2_ctas;              // K2_L2 grid width (0 = 148)
+    uint32_t k2_ctas;              // K2_L2 grid width (0 = 148); K2_FFT: > 0 = looping grid of that width
     int release_next;              // trigger the next launch at K2 start (1) / end (2) (PDL chaining)
     FftRadices fft2;               // radices of P2
     double2* out;                  // [batch][W]
@@ -131,6 +131,7 @@ struct K1Params {
     FftRadices fft;             // radices of P1
     uint32_t stages;            // ring depth (K1_MIN_STAGES..K1_MAX_STAGES)
     int pdl;                    // launched with programmatic stream serialization
+    uint32_t split;             // CTAs (a cluster) per residue class sharing its column chunks (1 or 2)
     double2* Y;                 // signal b's [P1][P2][r] slab, or [P2][W] residue rows (sum_tail),
                                 // at Y + b * y_stride
     uint64_t y_stride;          // elements between consecutive signals' data

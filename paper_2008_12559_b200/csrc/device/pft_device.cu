@@ -289,6 +289,7 @@ struct pft_dplan_s {
     int k2_mode = pftdev::K2_DIRECT;
     uint32_t k2_ctas = 0;
     bool allow_fuse = false; // K2 fused into K1's tail (opt-in; measured slower at C2b/C4)
+    bool allow_split = true; // isolated executes: two CTAs (a cluster) per residue class
     bool sum_tail = false;   // unsharded execute: K1 sum tail, no K2 (few output bins)
     bool k2_tail = false;    // unsharded execute: K2's work by K1's last arrivals (many bins)
     uint32_t k2_group = 0;   // k2_tail: columns j per FFT group
@@ -394,6 +395,7 @@ struct pft_dplan_s {
         P.fft = fft;
         P.stages = k1_stages;
         P.pdl = pdl ? 1 : 0;
+        P.split = 1;
         P.Y = Y;
         P.y_stride = y_stride;
         return P;
@@ -493,6 +495,11 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
     auto P2 = d->k2_params(w.Y, w.y_stride, out, w.status);
     P1.arrivals = w.arrivals;
     P1.ctl_stride = w.ctl_stride;
+    // An isolated transform (no overlap with a neighbour) whose grid leaves half the CTA slots
+    // idle runs two CTAs (a cluster) per residue class, each streaming half of the column chunks:
+    // one transform then fills both slots of every SM (C2b: 128 -> 256 CTAs).
+    if (!pdl && d->allow_split && !d->fused(batch) && 2 * d->P2 * batch <= d->k1_capacity && d->host.q >= 4 * pftdev::K1_CP)
+        P1.split = 2;
     if (d->sum_tail) {
         P1.sum_tail = 1;
         P1.reducers = d->reducers;
@@ -669,7 +676,9 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     d->host.achieved_epsilon = H.achieved_epsilon;
     d->host.plan_id = H.plan_id;
     d->W = 2 * H.M + 1;
-    PFT_REQUIRE(!opts || (opts->reserved[0] == 0 && opts->reserved[1] == 0), "dplan_create: reserved options must be 0");
+    d->allow_split = !(opts && opts->k1_split == 1);
+    PFT_REQUIRE(!opts || opts->reserved == 0, "dplan_create: reserved options must be 0");
+    PFT_REQUIRE(!opts || (opts->k1_split >= 0 && opts->k1_split <= 1), "dplan_create: k1_split must be 0 or 1");
     const int pass2 = opts ? opts->second_pass : PFT_PASS2_AUTO;
     const int k2_at = opts ? opts->k2_at : PFT_K2_AT_AUTO;
     PFT_REQUIRE(pass2 >= PFT_PASS2_AUTO && pass2 <= PFT_PASS2_K2_L2, "dplan_create: unknown second_pass");

@@ -82,7 +82,7 @@ cudaError_t configure_k2(int r, uint32_t P2) {
 }
 
 cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t batch, bool mu0, cudaStream_t st) {
-    const dim3 grid(P.P2, batch);
+    const dim3 grid(P.P2 * (P.split > 1 ? P.split : 1), batch);
     const size_t smem = k1_smem_bytes(r, P.P1, P.stages);
     switch (r) {
 #define X(n) case n: return launch_k1_r<n>(map, P, grid, smem, st, mu0);
@@ -94,7 +94,8 @@ cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t
 
 cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st) {
     const uint32_t gx = P.mode == K2_L2 ? (P.k2_ctas ? P.k2_ctas : 148u)
-                                         : P.P1;
+                        : (P.mode == K2_FFT && P.k2_ctas > 0) ? (P.k2_ctas < P.P1 ? P.k2_ctas : P.P1)
+                                                               : P.P1;
     const dim3 grid(gx, batch);
     switch (r) {
 #define X(n) case n: return launch_k2_r<n>(P, grid, st);

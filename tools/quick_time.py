@@ -31,6 +31,8 @@ def parse_opts(text: str) -> dict:
     for kv in filter(None, (text or "").split(",")):
         k, v = kv.split("=")
         out[k] = int(v) if v.lstrip("-").isdigit() else v
+        if k == "split":
+            out[k] = bool(out[k])
     return out
 
 
@@ -67,16 +69,19 @@ def run(cfg: str, p: int, opts: dict, reps: int, check: bool) -> dict:
         e1.record(st)
     torch.cuda.synchronize()
     chained = e0.elapsed_time(e1) / reps * 1e3
-    iso = []
-    for i in range(15):
+    with torch.cuda.stream(st):  # serialized executes (no overlap flag): device time per execute
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2, stream=st):
+            for i in range(min(reps, 50)):
+                ex(i + 1, overlap=False)
+        g2.replay()
         torch.cuda.synchronize()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(st):
-            a0.record(st)
-            ex(i + 1, overlap=False)
-            a1.record(st)
-        torch.cuda.synchronize()
-        iso.append(a0.elapsed_time(a1) * 1e3)
+        a0.record(st)
+        g2.replay()
+        a1.record(st)
+    torch.cuda.synchronize()
+    iso = [a0.elapsed_time(a1) * 1e3 / min(reps, 50)]
     res = {"cfg": cfg, "p": p, "opts": opts, "P1": d.P1, "P2": d.P2, "tail": d.tail_kind(),
            "chained_us": chained, "isolated_us": float(np.median(iso)),
            "frac": 16 * N * B / (chained * 1e-6) / 1e9 / bench.measured_hbm_peak()[0]}
