@@ -159,6 +159,8 @@ typedef struct pft_dplan_s* pft_dplan_t;
 #define PFT_PASS2_K2_DOT 3     /* K2: direct dot over P2 from shared memory (few bins per m1)  */
 #define PFT_PASS2_K2_DIRECT 4  /* K2: direct sum over P2 from global memory (any P2)           */
 #define PFT_PASS2_K2_L2 5      /* K2: one warp per bin over the L2-resident slab, no smem       */
+#define PFT_PASS2_K2_BLUESTEIN 6 /* K2: chirp-z length-P2 DFT via two power-of-two FFTs of L >=
+                                    2 P2 - 1 (any P2 <= 2048, prime factors > 64 included)       */
 /* Where the K2 work of the PFT_PASS2_K2_FFT form runs. */
 #define PFT_K2_AT_AUTO 0
 #define PFT_K2_AT_GRID 1       /* a separate K2 launch after K1                                 */
@@ -330,6 +332,8 @@ pft_status pft_launches_per_execute(pft_dplan_t d, int* launches);
  * 0 separate K2 grid, 1 sum tail in K1 (few bins), 2 K2 work by K1's last arrivals (many
  * bins), 3 K2 in K1 behind a grid barrier (opt-in). */
 pft_status pft_dplan_tail_kind(pft_dplan_t d, int* kind);
+/* The second-pass form a device plan runs (PFT_PASS2_*, never _AUTO). */
+pft_status pft_dplan_second_pass(pft_dplan_t d, int* form);
 
 /* ------------------------------------------------------------------ data formats and callers
  * The formats either side of execute and the pipeline that calls it (

@@ -527,7 +527,8 @@ def device_count() -> int:
     return n.value
 
 
-PASS2 = {"auto": 0, "sum": 1, "k2-fft": 2, "k2-dot": 3, "k2-direct": 4, "k2-l2": 5}  # PFT_PASS2_*
+PASS2 = {"auto": 0, "sum": 1, "k2-fft": 2, "k2-dot": 3, "k2-direct": 4, "k2-l2": 5,
+         "k2-bluestein": 6}                                                          # PFT_PASS2_*
 K2_AT = {"auto": 0, "grid": 1, "tail": 2, "fused": 3}                                 # PFT_K2_AT_*
 EXEC_OVERLAP_PREVIOUS = 1                                                             # PFT_EXEC_*
 
@@ -599,6 +600,14 @@ class DevicePlan:
         _check(lib().pft_dplan_tail_kind(self._h, C.byref(n)))
         return self.TAIL_KINDS[n.value]
 
+    @property
+    def second_pass(self) -> str:
+        """The second-pass form this plan runs ("sum", "k2-fft", "k2-dot", "k2-direct", "k2-l2",
+        "k2-bluestein")."""
+        n = C.c_int()
+        _check(lib().pft_dplan_second_pass(self._h, C.byref(n)))
+        return {v: k for k, v in PASS2.items()}[n.value]
+
     def execute_ptr(self, d_in: int, d_out: int, batch: int = 1, in_stride: int = 0, d_ws: int = 0,
                     stream: int = 0, overlap: bool = False) -> None:
         """pft_execute_ex.  overlap=True (PFT_EXEC_OVERLAP_PREVIOUS): K1 may stream while the
@@ -632,6 +641,15 @@ class DevicePlan:
         out = np.zeros(batch * (2 * self.plan.M + 1), dtype=np.complex128)
         _check(lib().pft_execute_host(self._h, _ptr(a), batch, _ptr(out), None, None, None))
         return out
+
+
+def naive_dft(a, first_m: int, count: int) -> np.ndarray:
+    """Exact-angle direct DFT on the GPU at bins first_m .. first_m + count - 1:
+    the verification path of the CLI (not the transform)."""
+    a = np.ascontiguousarray(np.asarray(a), dtype=np.complex128).reshape(-1)
+    out = np.zeros(max(count, 1), dtype=np.complex128)
+    _check(lib().pft_naive_dft_host(_ptr(a), a.size, int(first_m), int(count), _ptr(out)))
+    return out[:count]
 
 
 def execute(plan: PftPlan, a, device: int = 0) -> PartialSpectrum:

@@ -107,6 +107,9 @@ SIGNATURES: dict[str, tuple] = {
     "pft_sparse_tones": (ST, [U64, I, I64, I64, P, P]),
     "pft_launches_per_execute": (ST, [P, C.POINTER(I)]),
     "pft_dplan_tail_kind": (ST, [P, C.POINTER(I)]),
+    "pft_dplan_second_pass": (ST, [P, C.POINTER(I)]),
+    "pft_naive_dft_device": (ST, [P, U64, I64, U64, P, P]),
+    "pft_naive_dft_host": (ST, [P, U64, I64, U64, P]),
     "pft_device_count": (ST, [C.POINTER(I)]),
     "pft_signal_read": (ST, [C.c_char_p, I, P, U64, C.POINTER(U64), C.POINTER(I)]),
     "pft_signal_write": (ST, [C.c_char_p, I, P, U64, I]),

@@ -1008,6 +1008,98 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_loop(K2Params P) {
     if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// K2, Bluestein (chirp-z) form, for P2 with prime factors the in-smem Stockham radices do not
+// cover ("Bluestein for prime factors > 61").  With
+// h_c = e^{-pi i c^2/P2} and m2 c = (m2^2 + c^2 - (m2 - c)^2) / 2,
+//   X[m2] = sum_c x_c e^{-2 pi i m2 c / P2} = h_m2 * sum_c (x_c h_c) conj(h_{m2 - c}),
+// a linear convolution evaluated as a length-L cyclic one (L >= 2 P2 - 1, a power of two, <= 4096):
+// A = FFT_L(x h, zero-padded); A *= FFT_L(conj h wrapped)/L (host table chirp_hat); X = h * IFFT_L(A)
+// (IFFT as conj(FFT(conj(.)))).  One CTA per m1: columns j in groups of K2B_GROUP through the
+// two transforms in shared memory (2 columns per pass for L <= 2048, 1 for L = 4096: P2 <= 2048),
+// each output's Eq. (7) sum accumulated in registers in
+// ascending j as the columns complete (<= 4 outputs per thread).
+template <int R>
+__global__ void __launch_bounds__(K2_THREADS) k2_bluestein_post(K2Params P) {
+    extern __shared__ __align__(16) double2 zs[];
+    constexpr int NOUT = 4;
+    const int G = (int)P.bl_group;
+    const uint32_t L = P.L;
+    double2* A = zs;                        // [G][L]
+    double2* B = zs + (size_t)G * L;        // [G][L] Stockham scratch
+    const uint32_t m1 = blockIdx.x, b = blockIdx.y;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
+    if (s0 >= P.W) return;  // block-uniform
+    const int64_t Mh = (int64_t)((P.W - 1) / 2);
+    // this thread's outputs s = s0 + P1 (tid + i nt) and their m2
+    double2 acc[NOUT];
+    uint32_t m2s[NOUT];
+    double xs[NOUT], pws[NOUT];
+#pragma unroll
+    for (int i = 0; i < NOUT; ++i) {
+        acc[i] = make_double2(0.0, 0.0);
+        const uint64_t s = s0 + (uint64_t)P.P1 * (tid + (uint64_t)i * nt);
+        m2s[i] = 0xffffffffu;
+        if (s < P.W) {
+            uint64_t mp = P.first_mod_p + s % P.p;
+            if (mp >= P.p) mp -= P.p;
+            m2s[i] = (uint32_t)(mp / P.P1);
+            xs[i] = (double)((int64_t)s - Mh) * P.inv_p;  // (m - mu)/p
+            pws[i] = 1.0;
+        }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's slab complete and visible
+    const double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R;
+    const Twiddles twL{P.omega_L, 1u};
+    for (int j0 = 0; j0 < R; j0 += G) {
+        const int g = R - j0 < G ? R - j0 : G;
+        // x_c h_c (x_c = omega_p^{m1 c} Y[c][j]), zero-padded to L
+        for (uint32_t idx = tid; idx < (uint32_t)g * L; idx += nt) {
+            const uint32_t jj = idx / L, c = idx - jj * L;
+            double2 v = make_double2(0.0, 0.0);
+            if (c < P.P2) {
+                v = __ldcg(Y + (size_t)c * R + j0 + jj);
+                if (m1 != 0 && c != 0) v = cmul(v, __ldg(P.omega + (size_t)m1 * c));  // m1 c < p
+                v = cmul(v, __ldg(P.chirp + c));
+            }
+            A[idx] = v;
+        }
+        __syncthreads();
+        double2* r1 = fft_columns(A, B, g, P.fft2, twL);
+        double2* o1 = r1 == A ? B : A;
+        // times the kernel's transform, conjugated for the inverse transform
+        for (uint32_t idx = tid; idx < (uint32_t)g * L; idx += nt) {
+            const double2 v = cmul(r1[idx], __ldg(P.chirp_hat + (idx % L)));
+            o1[idx] = make_double2(v.x, -v.y);
+        }
+        __syncthreads();
+        double2* r2 = fft_columns(o1, r1, g, P.fft2, twL);
+        // X[m2] = h_m2 conj(r2[m2]) (chirp_hat carries the 1/L); Eq. (7) terms of these columns
+        for (int jj = 0; jj < g; ++jj) {
+#pragma unroll
+            for (int i = 0; i < NOUT; ++i) {
+                if (m2s[i] == 0xffffffffu) continue;
+                const double2 t = r2[(size_t)jj * L + m2s[i]];
+                const double2 X = cmul(make_double2(t.x, -t.y), __ldg(P.chirp + m2s[i]));
+                acc[i].x = fma(X.x, pws[i], acc[i].x);  // ascending j
+                acc[i].y = fma(X.y, pws[i], acc[i].y);
+                pws[i] *= xs[i];
+            }
+        }
+        __syncthreads();  // A / B reuse by the next group
+    }
+    double2* __restrict__ out = P.out + (size_t)b * P.W;
+#pragma unroll
+    for (int i = 0; i < NOUT; ++i) {
+        if (m2s[i] == 0xffffffffu) continue;
+        const uint64_t s = s0 + (uint64_t)P.P1 * (tid + (uint64_t)i * nt);
+        const double2 v = cmul(acc[i], __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+        out[s] = v;
+        if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
+    }
+}
+
 // K2 (dot form, few outputs per m1): only the ~W/P1 bins this CTA owns are needed, so
 // instead of the full length-P2 FFT each warp evaluates
 //   out[s] = e^{-pi i m/p} sum_c omega_P2^{m2 c} (sum_j Z[j][c] ((m - mu)/p)^j)
@@ -1261,6 +1353,10 @@ cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
         cfg.blockDim = dim3(K2L_THREADS);
         return cudaLaunchKernelEx(&cfg, k2_l2_post<R>, P);
     }
+    if (P.mode == K2_BLUESTEIN) {
+        cfg.dynamicSmemBytes = k2_bluestein_smem_bytes(P.L);
+        return cudaLaunchKernelEx(&cfg, k2_bluestein_post<R>, P);
+    }
     if (P.mode == K2_FFT && P.k2_ctas > 0) return cudaLaunchKernelEx(&cfg, k2_fft_loop<R>, P);
     if (P.mode == K2_FFT) return cudaLaunchKernelEx(&cfg, k2_fft_post<R>, P);
     if (P.mode == K2_DOT) return cudaLaunchKernelEx(&cfg, k2_dot_post<R>, P);
@@ -1272,6 +1368,8 @@ cudaError_t configure_k2_r(size_t smem) {
     cudaError_t e = cudaFuncSetAttribute(k2_fft_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k2_fft_loop<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k2_bluestein_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k2_dot_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }

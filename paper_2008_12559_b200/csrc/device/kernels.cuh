@@ -64,7 +64,12 @@ static_assert(K1_STAGE_BYTES % 128 == 0, "TMA destinations stay 128-byte aligned
 
 constexpr int K2_THREADS = 256;
 constexpr int K2L_THREADS = 128;
-enum K2Mode { K2_DIRECT = 0, K2_FFT = 1, K2_DOT = 2, K2_L2 = 3 };
+enum K2Mode { K2_DIRECT = 0, K2_FFT = 1, K2_DOT = 2, K2_L2 = 3, K2_BLUESTEIN = 4 };
+// Bluestein (chirp-z) K2: the length-P2 DFT of any P2 (a prime factor > 64 included) as a
+// convolution with a power-of-two length L >= 2 P2 - 1, columns in groups of K2B_GROUP.
+constexpr uint32_t K2B_MAX_L = 4096;
+inline uint32_t k2_bluestein_group(uint32_t L) { return L <= 2048 ? 2u : 1u; }  // columns per pass
+inline size_t k2_bluestein_smem_bytes(uint32_t L) { return sizeof(double2) * 2 * (size_t)k2_bluestein_group(L) * L; }
 
 
 struct K2Params {
@@ -82,7 +87,12 @@ struct K2Params {
     int mode;                      // K2_DIRECT / K2_FFT / K2_DOT
     uint32_t k2_ctas;              // K2_L2 grid width (0 = 148); K2_FFT: > 0 = looping grid of that width
     int release_next;              // trigger the next launch at K2 start (1) / end (2) (PDL chaining)
-    FftRadices fft2;               // radices of P2
+    FftRadices fft2;               // radices of P2 (K2_FFT) or of L (K2_BLUESTEIN)
+    const double2* chirp;          // K2_BLUESTEIN: [P2] e^{-pi i c^2 / P2}
+    const double2* chirp_hat;      // K2_BLUESTEIN: [L] FFT_L of the conjugate chirp kernel / L
+    const double2* omega_L;        // K2_BLUESTEIN: [L] e^{-2 pi i t / L}
+    uint32_t L;                    // K2_BLUESTEIN: convolution length (power of two)
+    uint32_t bl_group;             // K2_BLUESTEIN: columns per transform pass (smem: 2 x group x L)
     double2* out;                  // [batch][W]
     int* status;                   // non-finite flag word of the workspace (bit 0)
 };

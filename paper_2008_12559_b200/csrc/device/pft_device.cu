@@ -304,6 +304,10 @@ struct pft_dplan_s {
     double2* d_w = nullptr;
     double2 phase0{1.0, 0.0}, phaseh{1.0, 0.0};
     double2* d_omega = nullptr;
+    // Bluestein K2 (K2_BLUESTEIN): chirp h_c, FFT_L of the conjugate chirp kernel / L, omega_L
+    uint32_t bl_L = 0;
+    void* bl_tables = nullptr;
+    double2 *d_chirp = nullptr, *d_chirp_hat = nullptr, *d_omega_L = nullptr;
     double* d_post_powers = nullptr;
     double2* d_post_twiddles = nullptr;
     void* d_ws = nullptr;  // the plan's own batch-1 workspace (executes with d_ws == NULL, finalize)
@@ -333,6 +337,7 @@ struct pft_dplan_s {
             delete s;
         }
         if (tables) cudaFree(tables);
+        if (bl_tables) cudaFree(bl_tables);
         if (d_ws) cudaFree(d_ws);
         cudaSetDevice(prev);
     }
@@ -420,6 +425,11 @@ struct pft_dplan_s {
         P.k2_ctas = k2_ctas;
         P.release_next = 1;  // a following K1 only streams early when its execute asked for it
         P.fft2 = fft2;
+        P.chirp = d_chirp;
+        P.chirp_hat = d_chirp_hat;
+        P.omega_L = d_omega_L;
+        P.L = bl_L;
+        P.bl_group = bl_L ? pftdev::k2_bluestein_group(bl_L) : 1;
         P.out = out;
         P.status = status;
         return P;
@@ -681,7 +691,7 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     PFT_REQUIRE(!opts || (opts->k1_split >= 0 && opts->k1_split <= 1), "dplan_create: k1_split must be 0 or 1");
     const int pass2 = opts ? opts->second_pass : PFT_PASS2_AUTO;
     const int k2_at = opts ? opts->k2_at : PFT_K2_AT_AUTO;
-    PFT_REQUIRE(pass2 >= PFT_PASS2_AUTO && pass2 <= PFT_PASS2_K2_L2, "dplan_create: unknown second_pass");
+    PFT_REQUIRE(pass2 >= PFT_PASS2_AUTO && pass2 <= PFT_PASS2_K2_BLUESTEIN, "dplan_create: unknown second_pass");
     PFT_REQUIRE(k2_at >= PFT_K2_AT_AUTO && k2_at <= PFT_K2_AT_FUSED, "dplan_create: unknown k2_at");
     PFT_REQUIRE(!opts || (opts->tail_ctas >= 0 && opts->k2_grid_ctas >= 0), "dplan_create: negative CTA count");
     const int tail_ctas = opts ? opts->tail_ctas : 0;
@@ -716,18 +726,29 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         // latency-bound at C2b/C4's 2049 / 2001 bins) -- unless the sum tail below applies
         // (measured C2b 49 vs 54 us, C4 35 vs 45 us per transform).
         const bool l2_ok = d->P2 <= 1024 && double(d->W) * d->P2 <= 64.0 * 1024 * 1024;
+        uint32_t bl_L = 1;
+        while (bl_L < 2 * d->P2 - 1) bl_L <<= 1;
+        const bool bl_ok = d->P2 > 1 && bl_L <= pftdev::K2B_MAX_L && d->W <= 4ull * pftdev::K2_THREADS * d->P1;
         if (pass2 == PFT_PASS2_K2_FFT && fft_ok) d->k2_mode = pftdev::K2_FFT;
         else if (pass2 == PFT_PASS2_K2_DOT && dot_ok) d->k2_mode = pftdev::K2_DOT;
         else if (pass2 == PFT_PASS2_K2_DIRECT) d->k2_mode = pftdev::K2_DIRECT;
         else if (pass2 == PFT_PASS2_K2_L2) d->k2_mode = pftdev::K2_L2;
         else if (pass2 == PFT_PASS2_SUM_TAIL) d->k2_mode = pftdev::K2_FFT;  // with the sum tail below
         else if (l2_ok && d->W <= 2 * d->P1) d->k2_mode = pftdev::K2_L2;  // few bins per m1 (C1)
+        else if (pass2 == PFT_PASS2_K2_BLUESTEIN && bl_ok) d->k2_mode = pftdev::K2_BLUESTEIN;
         else if (fft_ok) d->k2_mode = pftdev::K2_FFT;
+        // P2 with a prime factor > 64 (no Stockham radix schedule) and many bins per m1: chirp-z
+        // (two length-L FFTs per column) beats the dot / direct forms' O(bins x P2) per column
+        else if (bl_ok && d->W >= 32 * d->P1) d->k2_mode = pftdev::K2_BLUESTEIN;
         else if (dot_ok) d->k2_mode = pftdev::K2_DOT;
         else d->k2_mode = pftdev::K2_DIRECT;
         if (d->k2_mode == pftdev::K2_FFT) {
             if (d->P2 > 1) factor_radices((uint32_t)d->P2, d->fft2);
             else d->fft2.n = 1;
+        }
+        if (d->k2_mode == pftdev::K2_BLUESTEIN) {
+            d->bl_L = bl_L;
+            factor_radices(bl_L, d->fft2);
         }
         // K2 CTAs (each loops over m1): few enough to all be resident beside K1 (opts override)
         d->k2_ctas = opts && opts->k2_grid_ctas > 0 ? (uint32_t)opts->k2_grid_ctas : 0;
@@ -834,6 +855,39 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
                "upload post_powers");
     cuda_check(cudaMemcpy(d->d_post_twiddles, H.post_twiddles.data(), d->W * sizeof(double2), cudaMemcpyHostToDevice),
                "upload post_twiddles");
+    if (d->k2_mode == pftdev::K2_BLUESTEIN) {
+        // h_c = e^{-pi i c^2 / P2} (exact: c^2 mod 2 P2); kernel b_k = conj(h_k) for |k| < P2 wrapped
+        // into length L; its FFT_L / L in long double; omega_L.
+        const uint64_t P2 = d->P2, L = d->bl_L;
+        std::vector<cplx> chirp(P2), hat(L), omL(L);
+        for (uint64_t c = 0; c < P2; ++c) chirp[c] = cispi_frac(-(__int128)((c * c) % (2 * P2)), (__int128)P2);
+        std::vector<std::complex<long double>> bk(L, 0.0L);
+        for (uint64_t k = 0; k < P2; ++k) {
+            const cplx v = std::conj(chirp[k]);
+            bk[k] = {v.real(), v.imag()};
+            if (k) bk[L - k] = bk[k];
+        }
+        const long double tau = 6.283185307179586476925286766559005768L;
+#pragma omp parallel for schedule(static)
+        for (long long t = 0; t < (long long)L; ++t) {
+            std::complex<long double> acc = 0.0L;
+            for (uint64_t k = 0; k < L; ++k) {
+                if (bk[k] == std::complex<long double>(0.0L)) continue;
+                const uint64_t e = ((uint64_t)t * k) % L;
+                acc += bk[k] * std::polar(1.0L, -tau * (long double)e / (long double)L);
+            }
+            acc /= (long double)L;
+            hat[t] = cplx((double)acc.real(), (double)acc.imag());
+        }
+        for (uint64_t t = 0; t < L; ++t) omL[t] = cispi_frac(-2 * (__int128)t, (__int128)L);
+        cuda_check(cudaMalloc(&d->bl_tables, (P2 + 2 * L) * sizeof(double2)), "cudaMalloc(bluestein tables)");
+        d->d_chirp = static_cast<double2*>(d->bl_tables);
+        d->d_chirp_hat = d->d_chirp + P2;
+        d->d_omega_L = d->d_chirp_hat + L;
+        cuda_check(cudaMemcpy(d->d_chirp, chirp.data(), P2 * sizeof(double2), cudaMemcpyHostToDevice), "upload chirp");
+        cuda_check(cudaMemcpy(d->d_chirp_hat, hat.data(), L * sizeof(double2), cudaMemcpyHostToDevice), "upload chirp_hat");
+        cuda_check(cudaMemcpy(d->d_omega_L, omL.data(), L * sizeof(double2), cudaMemcpyHostToDevice), "upload omega_L");
+    }
     cuda_check(pftdev::configure_k1(H.r, (uint32_t)d->P1, d->mu0), "configure K1 (early)");
     cuda_check(cudaMalloc(&d->d_ws, d->workspace_bytes(1)), "cudaMalloc(workspace)");
     cuda_check(cudaMemset(d->d_ws, 0, d->workspace_bytes(1)), "cudaMemset(workspace)");
@@ -894,6 +948,22 @@ pft_status pft_launches_per_execute(pft_dplan_t d, int* launches) {
     dp(d);
     PFT_REQUIRE(launches != nullptr, "launches is null");
     *launches = (dp(d)->fused(1) || dp(d)->sum_tail || dp(d)->k2_tail) ? 1 : 2;
+    PFT_API_END
+}
+
+pft_status pft_dplan_second_pass(pft_dplan_t d, int* form) {
+    PFT_API_BEGIN
+    const pft_dplan_s* x = dp(d);
+    PFT_REQUIRE(form != nullptr, "form is null");
+    if (x->sum_tail) *form = PFT_PASS2_SUM_TAIL;
+    else
+        switch (x->k2_mode) {
+            case pftdev::K2_FFT: *form = PFT_PASS2_K2_FFT; break;
+            case pftdev::K2_DOT: *form = PFT_PASS2_K2_DOT; break;
+            case pftdev::K2_L2: *form = PFT_PASS2_K2_L2; break;
+            case pftdev::K2_BLUESTEIN: *form = PFT_PASS2_K2_BLUESTEIN; break;
+            default: *form = PFT_PASS2_K2_DIRECT; break;
+        }
     PFT_API_END
 }
 

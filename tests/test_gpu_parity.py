@@ -354,3 +354,34 @@ def test_every_contraction_path(pft, oracle, r, mu):
     a = uniform(pft, 100 + r, N)
     got = pft.execute(plan, a).values
     assert rel_l2(got, oracle.execute(plan, a)) <= GATE
+
+
+@pytest.mark.parametrize("N,M,mu,p,P2", [
+    (2 ** 10 * 1021, 2 ** 12, 77, 1021 * 2 ** 7, 1021),     # prime P2 = 1021: L = 2048, 2 columns per pass
+    (2 ** 12 * 67, 2 ** 12, -5, 67 * 2 ** 7, 67),           # smallest prime > 64: L = 256
+    (2 ** 9 * 2039, 2 ** 11, 3, 2039 * 2 ** 6, 2039),       # prime P2 = 2039: L = 4096, 1 column per pass
+    (2 ** 10 * 3 * 331, 1500, 0, 3 * 331 * 2 ** 6, 993),     # composite P2 with a prime factor 331 > 64
+])
+def test_bluestein_second_pass(pft, oracle, N, M, mu, p, P2):
+    """the length-P2 pass for P2 with a prime factor > 64 by
+    chirp-z (Bluestein) -- two power-of-two FFTs of L >= 2 P2 - 1 per column -- is chosen
+    automatically when the bins per m1 are many, matches the oracle, and agrees with the direct
+    and dot forms of the same pass."""
+    import torch
+    plan = pft.build_plan(N, M, mu, p, 1e-12)
+    a = pft.generate_signal(pft.KIND_UNIFORM, 31, N)
+    x = torch.from_numpy(a).cuda()
+    ref = oracle.execute(plan, a)
+    res = {}
+    for form in ("auto", "k2-bluestein", "k2-direct"):
+        d = pft.DevicePlan(plan, p2=P2, second_pass=form)
+        assert d.P2 == P2
+        if form == "auto":
+            assert d.second_pass == "k2-bluestein", d.second_pass
+        out = torch.empty(2 * M + 1, dtype=torch.complex128, device="cuda")
+        for _ in range(2):
+            d.execute_ptr(x.data_ptr(), out.data_ptr())
+        torch.cuda.synchronize()
+        res[form] = out.cpu().numpy()
+        assert rel_l2(res[form], ref) <= GATE, (form, rel_l2(res[form], ref))
+    assert rel_l2(res["k2-bluestein"], res["k2-direct"]) <= 1e-13
