@@ -111,9 +111,10 @@ bool sum_tail_pays(uint64_t N, uint64_t W, uint64_t P2, int r) {
 uint64_t choose_p2_sum(uint64_t p, int r, int n_sms, size_t batch) {
     if (batch > 1) {
         // batched signals supply the CTAs: give each CTA as many rows as fit (the smallest P2),
-        // keeping >= 2 CTAs per SM over the batch
+        // keeping >= 1 CTA per SM over the batch (the 2-D column pass, 129 signals of 4096 at
+        // p = 128: P2 = 2 7.2 us vs P2 = 4 11.3 us, profiles/r02/p2d)
         for (uint64_t d : divisors(p))
-            if (d * batch >= 2ull * (uint64_t)n_sms && sum_p1_ok(p / d, r, d)) return d;
+            if (d * batch >= (uint64_t)n_sms && sum_p1_ok(p / d, r, d)) return d;
     }
     // pass 0: P1 a power of two >= K1_BR (full 32-row boxes, radix-16/8 FFT: C4 p = 11520
     // measured 17.6 us with P1 = 128, P2 = 90 vs 20.2 us with P1 = 90, P2 = 128);
