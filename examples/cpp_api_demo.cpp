@@ -1,7 +1,8 @@
 // cpp_api_demo.cpp -- the reference's plan-then-execute interface, used from C++ exactly as
 // code written against proj/include/pft/types.hpp + SPEC.md would use it.
 //
-//   g++ -std=c++20 -I include examples/cpp_api_demo.cpp -L paper_2008_12559_b200 -lpft_b200
+//   g++ -std=c++20 -I include -I /usr/local/cuda/include examples/cpp_api_demo.cpp
+//       -L paper_2008_12559_b200 -lpft_b200 -L /usr/local/cuda/lib64 -lcudart
 //       -Wl,-rpath,$PWD/paper_2008_12559_b200 -pthread -o /tmp/pft_demo && /tmp/pft_demo [--require-gpu]
 //
 // Without a GPU the execute part reports pft::DeviceError and the demo still exits 0 (the
@@ -13,6 +14,8 @@
 #include <stdexcept>
 #include <thread>
 #include <vector>
+
+#include <cuda_runtime.h>
 
 #include "pft/pft.hpp"
 
@@ -87,6 +90,31 @@ int main(int argc, char** argv) {
         } catch (const std::invalid_argument&) {
         }
         if (!(impulse_error(pft::execute(p2, a), p2.N, 0) <= bound)) return 9;
+        // the sharded step through the C++ API on a 1-rank communicator: K1 | ncclReduce | K2
+        int have_nccl = 0;
+        pft_nccl_available(&have_nccl);
+        if (have_nccl) {
+            pft::NcclComm comm(1, 0, pft::NcclComm::unique_id(), 0);
+            size_t slab_bytes = 0;
+            pft_partial_bytes(p2.device_plan(), 1, &slab_bytes);
+            pft::cplx *d_in = nullptr, *d_slab = nullptr, *d_out = nullptr;
+            cudaMalloc(&d_in, p2.N * sizeof(pft::cplx));
+            cudaMalloc(&d_slab, slab_bytes);
+            cudaMalloc(&d_out, (2 * p2.M + 1) * sizeof(pft::cplx));
+            cudaMemcpy(d_in, a.data(), p2.N * sizeof(pft::cplx), cudaMemcpyHostToDevice);
+            pft::execute_sharded(p2, d_in, p2.q, comm.get(), 0, d_slab, d_out);
+            std::vector<pft::cplx> got(2 * p2.M + 1);
+            cudaMemcpy(got.data(), d_out, got.size() * sizeof(pft::cplx), cudaMemcpyDeviceToHost);
+            cudaFree(d_in);
+            cudaFree(d_slab);
+            cudaFree(d_out);
+            pft::PartialSpectrum sh;
+            sh.range = p2.range();
+            sh.values = got;
+            const double e = impulse_error(sh, p2.N, 0);
+            std::printf("execute_sharded (1 rank): max error %.3e\n", e);
+            if (!(e <= bound)) return 10;
+        }
         return 0;
     } catch (const pft::DeviceError& e) {
         std::printf("execute: %s\n", e.what());  // no GPU here: fails loudly, no CPU fallback

@@ -281,4 +281,50 @@ inline void execute_device(const PftPlan& plan, const cplx* d_in, cplx* d_out, v
                                      detail_api::c(d_out), workspace, stream, flags));
 }
 
+// ---------------------------------------------------------------- sharded transform
+
+// A NCCL communicator made by the library (pft_nccl_comm_init); any ncclComm_t the application
+// created with its own NCCL can be passed to execute_sharded instead.
+class NcclComm {
+public:
+    static std::vector<unsigned char> unique_id() {  // on one rank; share it with the others
+        std::vector<unsigned char> id(PFT_NCCL_UNIQUE_ID_BYTES);
+        detail_api::check(pft_nccl_get_unique_id(id.data()));
+        return id;
+    }
+    NcclComm(int world, int rank, const std::vector<unsigned char>& id, int device) {
+        if (id.size() != PFT_NCCL_UNIQUE_ID_BYTES) throw std::invalid_argument("NCCL unique id must be 128 bytes");
+        detail_api::check(pft_nccl_comm_init(world, rank, id.data(), device, &comm_));
+    }
+    NcclComm(const NcclComm&) = delete;
+    NcclComm& operator=(const NcclComm&) = delete;
+    ~NcclComm() { pft_nccl_comm_destroy(comm_); }
+    struct ncclComm* get() const { return comm_; }
+
+private:
+    struct ncclComm* comm_ = nullptr;
+};
+
+// Device-aware p for the transform sharded over `world` GPUs (the collective included).
+inline CostEstimate select_divisor_sharded(std::size_t N, std::size_t M, const ScopeTable& t, double epsilon,
+                                           int world, int n_sms = 148) {
+    uint64_t p = 0;
+    int r = 0;
+    double us = 0.0;
+    detail_api::check(pft_select_divisor_sharded(t.handle(), N, M, epsilon, n_sms, world, &p, &r, &us));
+    return CostEstimate{static_cast<std::size_t>(p), static_cast<std::size_t>(r), us};
+}
+
+// One rank's step of the contraction-axis sharded transform: K1 on this rank's slice
+// (pft_shard_layout row layout, row_stride elements per row), ncclReduce of the p x r partial
+// slab onto `root` over NVLink, K2 on the root into d_out (2M+1 values; unused elsewhere).
+// d_slab: pft_partial_bytes(plan, 1) bytes of device memory on every rank.  Asynchronous on
+// `stream`, graph-capturable.  The plan's device upload must be the communicator's device.
+inline void execute_sharded(const PftPlan& plan, const cplx* d_in_local, std::uint64_t row_stride,
+                            struct ncclComm* comm, int root, cplx* d_slab, cplx* d_out, void* stream = nullptr,
+                            int device = 0) {
+    detail_api::check(pft_execute_sharded(plan.device_plan(device), detail_api::c(d_in_local), row_stride, comm, root,
+                                          detail_api::c(d_slab), detail_api::c(d_out), stream));
+}
+
 }  // namespace pft

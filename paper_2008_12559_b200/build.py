@@ -83,8 +83,14 @@ def _deps_hash(src: Path) -> str:
     return h.hexdigest()[:16]
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
+    """checked=True: the bounds-checked flavour (-DPFT_CHECKED: every computed workspace / output /
+    input index is checked and traps) as libpft_b200_checked.so, for the GPU check runs
+    (PFT_LIB=... python tools/sanitize.py / pytest); the product library is unchanged."""
+    global BUILD, LIB
+    if checked:
+        BUILD, LIB = PKG / "build" / "checked", PKG / "libpft_b200_checked.so"
+    BUILD.mkdir(parents=True, exist_ok=True)
     _write_table_blob()
     objs: list[Path] = []
     jobs: list[list] = []
@@ -97,7 +103,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     for src in sorted((CSRC / "device").glob("*.cu")):
         obj = BUILD / f"dev_{src.stem}_{_deps_hash(src)}.o"
         if force or not obj.exists():
-            jobs.append([NVCC, *NVCC_FLAGS, *incs, "-c", src, "-o", obj])
+            jobs.append([NVCC, *NVCC_FLAGS, *(["-DPFT_CHECKED"] if checked else []), *incs, "-c", src, "-o", obj])
         objs.append(obj)
     # translation units compile concurrently (the kernel instantiations dominate)
     with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
@@ -113,8 +119,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     # the CLI (host code compiled by nvcc: it times with CUDA events), rpath'd to the library
     cli_src = CSRC / "cli" / "pft_cli.cu"
     cli_stamp = BUILD / "cli.stamp"
-    cli_key = _deps_hash(cli_src) + LIB.stat().st_mtime_ns.__str__()
-    if cli_src.exists() and (force or not CLI.exists() or not cli_stamp.exists() or cli_stamp.read_text() != cli_key):
+    cli_key = _deps_hash(cli_src) + LIB.stat().st_mtime_ns.__str__() if cli_src.exists() else ""
+    if not checked and cli_src.exists() and (force or not CLI.exists() or not cli_stamp.exists() or
+                                              cli_stamp.read_text() != cli_key):
         tmp = CLI.with_suffix(".tmp")
         _run([NVCC, "-std=c++20", "-O2", *ARCH, "-I", INCLUDE, cli_src, "-o", tmp, "-L", PKG, "-lpft_b200",
               "-Xlinker", "-rpath,$ORIGIN", "-ldl"], verbose)
@@ -125,15 +132,19 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     for o in BUILD.glob("*.o"):
         if o.name not in live:
             o.unlink()
-    return LIB
+    lib = LIB
+    if checked:
+        BUILD, LIB = PKG / "build", PKG / "libpft_b200.so"
+    return lib
 
 
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--checked", action="store_true", help="bounds-checked flavour (libpft_b200_checked.so)")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, checked=a.checked))
 
 
 if __name__ == "__main__":

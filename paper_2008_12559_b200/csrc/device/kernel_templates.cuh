@@ -325,10 +325,12 @@ __device__ __forceinline__ void k1_sum_tail_fast(const K1Params& P, const double
         const uint64_t so = (uint64_t)tid + (uint64_t)i * nt;
         if (so < Q.W) {
             keep[i] = k1_row_value<R>(P, res, twc, tw2, c, so, Mh, p1_pow2, p2_pow2, lg_p1);
+            PFT_BOUND((size_t)b * P.y_stride + (size_t)c * Q.W + so, P.y_elems);
             rowc[so] = keep[i];
         }
     }
     unsigned* ctl = P.arrivals + (size_t)b * P.ctl_stride;  // {tickets, ...}
+    PFT_BOUND((size_t)b * P.ctl_stride, P.ctl_words);
     unsigned* s_last = reinterpret_cast<unsigned*>(tw2 + P.P2);
     __syncthreads();  // every row store precedes thread 0's fence and ticket
     if (tid == 0) {
@@ -346,6 +348,7 @@ __device__ __forceinline__ void k1_sum_tail_fast(const K1Params& P, const double
         const uint64_t so = (uint64_t)tid + (uint64_t)i * nt;
         if (so < Q.W) {
             double2 v[FAST_P2];
+            PFT_BOUND((size_t)b * P.y_stride + (size_t)(P.P2 - 1) * Q.W + so, P.y_elems);
 #pragma unroll
             for (int r = 0; r < FAST_P2; ++r)
                 v[r] = (uint32_t)r >= P.P2 ? make_double2(0.0, 0.0)
@@ -356,6 +359,7 @@ __device__ __forceinline__ void k1_sum_tail_fast(const K1Params& P, const double
             for (int r = 1; r < FAST_P2; ++r)
                 if ((uint32_t)r < P.P2) tot = cadd(tot, v[r]);  // fixed order c = 0, 1, ...
             const double2 o = cmul(tot, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
+            PFT_BOUND((size_t)b * Q.W + so, Q.out_elems);
             Q.out[(size_t)b * Q.W + so] = o;
             if (!isfinite(o.x) || !isfinite(o.y)) atomicOr(Q.status, 1);
         }
@@ -403,15 +407,18 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
         const double2 v = k1_row_value<R>(P, res, twc, tw2, c, so, Mh, p1_pow2, p2_pow2, lg_p1);
         if (direct) {
             const double2 o = cmul(v, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
+            PFT_BOUND((size_t)b * Q.W + so, Q.out_elems);
             Q.out[(size_t)b * Q.W + so] = o;
             if (!isfinite(o.x) || !isfinite(o.y)) atomicOr(Q.status, 1);
         } else {
+            PFT_BOUND((size_t)b * P.y_stride + (size_t)c * Q.W + so, P.y_elems);
             rowc[so] = v;
         }
     }
     if (direct) return;
     // publish the row, then take a ticket: the last `reducers` arrivals of signal b reduce
     unsigned* ctl = P.arrivals + (size_t)b * P.ctl_stride;  // {tickets, done, ready[P2]}
+    PFT_BOUND((size_t)b * P.ctl_stride + P.P2 + 1, P.ctl_words);
     unsigned* ready = ctl + 2;
     double2* part = tw2 + P.P2;                           // [nw][64] reducer partials
     unsigned* s_ticket = reinterpret_cast<unsigned*>(part + (size_t)nw * 64);
@@ -447,6 +454,8 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
             for (int u = 0; u < 8; ++u) {
                 const uint32_t r = r0 + u * nw;
                 const bool in = r < P.P2;
+                if (in && oka) PFT_BOUND((size_t)b * P.y_stride + (size_t)r * Q.W + sa, P.y_elems);
+                if (in && okb) PFT_BOUND((size_t)b * P.y_stride + (size_t)r * Q.W + sb, P.y_elems);
                 va[u] = (in && oka) ? __ldcg(rows + (size_t)r * Q.W + sa) : make_double2(0.0, 0.0);
                 vb[u] = (in && okb) ? __ldcg(rows + (size_t)r * Q.W + sb) : make_double2(0.0, 0.0);
             }
@@ -465,6 +474,7 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
                 double2 tot = part[warp * 32 + lane];
                 for (int w = 1; w < nw; ++w) tot = cadd(tot, part[w * 64 + warp * 32 + lane]);
                 const double2 v = cmul(tot, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
+                PFT_BOUND((size_t)b * Q.W + so, Q.out_elems);
                 Q.out[(size_t)b * Q.W + so] = v;
                 if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(Q.status, 1);
             }
@@ -505,6 +515,7 @@ __device__ __forceinline__ void k1_k2_tail(const K1Params& P, uint32_t c, uint32
     double2* pre = tw2 + P.P2;                    // omega_p^{m1 c}
     unsigned* s_t = reinterpret_cast<unsigned*>(pre + P.P2);
     unsigned* ctl = P.arrivals + (size_t)b * P.ctl_stride;   // {tickets, done}
+    PFT_BOUND((size_t)b * P.ctl_stride + 1, P.ctl_words);
     __syncthreads();  // the CTA's slab stores precede thread 0's fence and ticket
     if (tid == 0) {
         __threadfence();
@@ -556,6 +567,7 @@ __device__ __forceinline__ void k1_k2_tail(const K1Params& P, uint32_t c, uint32
                 for (int u = 0; u < U; ++u) {
                     const uint32_t idx = base + u * nt;
                     const uint32_t cc = idx / g, jj = idx - cc * g;
+                    if (idx < n) PFT_BOUND((size_t)b * P.y_stride + (size_t)m1 * P.P2 * R + (size_t)cc * R + j0 + jj, P.y_elems);
                     v[u] = idx < n ? __ldcg(Ym + (size_t)cc * R + j0 + jj) : make_double2(0.0, 0.0);
                 }
 #pragma unroll
@@ -590,6 +602,7 @@ __device__ __forceinline__ void k1_k2_tail(const K1Params& P, uint32_t c, uint32
                     acc = cmul(acc, first ? ptw0 : __ldg(Q.post_twiddles + s));  // e^{-pi i m / p}
                     if (!isfinite(acc.x) || !isfinite(acc.y)) atomicOr(Q.status, 1);
                 }
+                PFT_BOUND((size_t)b * Q.W + s, Q.out_elems);
                 out[s] = acc;
             }
             __syncthreads();  // Z / scratch reuse by the next group or m1
@@ -705,6 +718,8 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                 double2 x0 = make_double2(0.0, 0.0), xh = make_double2(0.0, 0.0);
                 if (k1 < P.P1 && rank == 0) {
                     const double2* row = P.a + (size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride;
+                    PFT_BOUND((size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride +
+                                  (size_t)max(P.single0_col, P.singleh_col), P.in_elems);
                     if (P.single0_col >= 0) x0 = __ldg(row + P.single0_col);
                     if (t4 == 1 && P.singleh_col >= 0) xh = __ldg(row + P.singleh_col);
                 }
@@ -741,8 +756,10 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
             // now, consume it after the chunk loop so its DRAM latency is hidden
             const int scol = rank != 0 ? -1 : li < JS ? P.single0_col : (li == JS ? P.singleh_col : -1);
             double2 xs = make_double2(0.0, 0.0);
-            if (k1 < P.P1 && scol >= 0)
+            if (k1 < P.P1 && scol >= 0) {
+                PFT_BOUND((size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride + scol, P.in_elems);
                 xs = __ldg(P.a + (size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride + scol);
+            }
             for (uint32_t ch = ch_lo; ch < ch_hi; ++ch) {
                 mbar_wait(&full[s], ph);
                 // Reconverge before touching the stage: lane 0's `empty` arrive below leaves
@@ -809,6 +826,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride;
     for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) {
         const uint32_t m1 = idx / R, j = idx - m1 * R;
+        PFT_BOUND((size_t)b * P.y_stride + ((size_t)m1 * P.P2 + c) * R + j, P.y_elems);
         Y[((size_t)m1 * P.P2 + c) * R + j] = res[(size_t)j * P.P1 + m1];
     }
     // the K2 tail lives in its own instantiations (K2T, k1_k2_tail_instantiated(R)): its code in
@@ -874,6 +892,7 @@ __device__ __forceinline__ void k2_fft_block(const K2Params& P, uint32_t m1, uin
     }
     __syncthreads();
     const double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R;
+    PFT_BOUND((size_t)b * P.y_stride + ((size_t)m1 + 1) * P.P2 * R - 1, P.y_elems);
     load_twiddled_slab<R>(Y, P.P2, m1, pre, Z);
     __syncthreads();
     const double2* res = Z;
@@ -892,6 +911,7 @@ __device__ __forceinline__ void k2_fft_block(const K2Params& P, uint32_t m1, uin
             acc.y = fma(v.y, pw, acc.y);
         }
         const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+        PFT_BOUND((size_t)b * P.W + s, P.out_elems);
         out[s] = v;
         if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
     }
@@ -929,6 +949,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     const double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R;
+    PFT_BOUND((size_t)b * P.y_stride + ((size_t)m1 + 1) * P.P2 * R - 1, P.y_elems);
     load_twiddled_slab<R>(Y, P.P2, m1, pre, Z);
     __syncthreads();
     const double2* res = Z;
@@ -948,6 +969,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
             acc.y = fma(v.y, pw, acc.y);
         }
         const double2 v = cmul(acc, first ? ptw0 : __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+        PFT_BOUND((size_t)b * P.W + s, P.out_elems);
         out[s] = v;
         if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
     }
@@ -1000,6 +1022,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_loop(K2Params P) {
                 if (j + 1 < R) tp *= x;
             }
             const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+            PFT_BOUND((size_t)b * P.W + s, P.out_elems);
             out[s] = v;
             if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
         }
@@ -1051,6 +1074,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_bluestein_post(K2Params P) {
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's slab complete and visible
     const double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R;
+    PFT_BOUND((size_t)b * P.y_stride + ((size_t)m1 + 1) * P.P2 * R - 1, P.y_elems);
     const Twiddles twL{P.omega_L, 1u};
     for (int j0 = 0; j0 < R; j0 += G) {
         const int g = R - j0 < G ? R - j0 : G;
@@ -1095,6 +1119,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_bluestein_post(K2Params P) {
         if (m2s[i] == 0xffffffffu) continue;
         const uint64_t s = s0 + (uint64_t)P.P1 * (tid + (uint64_t)i * nt);
         const double2 v = cmul(acc[i], __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+        PFT_BOUND((size_t)b * P.W + s, P.out_elems);
         out[s] = v;
         if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
     }
@@ -1131,6 +1156,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_dot_post(K2Params P) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     const double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R;
+    PFT_BOUND((size_t)b * P.y_stride + ((size_t)m1 + 1) * P.P2 * R - 1, P.y_elems);
     load_twiddled_slab<R>(Y, P.P2, m1, pre, Z);
     __syncthreads();
     const bool p2_pow2 = (P.P2 & (P.P2 - 1)) == 0;
@@ -1161,6 +1187,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_dot_post(K2Params P) {
         }
         if (lane == 0) {
             const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+            PFT_BOUND((size_t)b * P.W + s, P.out_elems);
             out[s] = v;
             if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
         }
@@ -1213,6 +1240,7 @@ __global__ void __launch_bounds__(K2L_THREADS) k2_l2_post(K2Params P) {
         }
         if (lane == 0) {
             const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+            PFT_BOUND((size_t)b * P.W + s, P.out_elems);
             out[s] = v;
             if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
         }
@@ -1231,6 +1259,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_direct_post(K2Params P) {
     constexpr int NW = K2_THREADS / 32;
     const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
     const double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R;
+    PFT_BOUND((size_t)b * P.y_stride + ((size_t)m1 + 1) * P.P2 * R - 1, P.y_elems);
     double2* __restrict__ out = P.out + (size_t)b * P.W;
     if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1261,6 +1290,7 @@ __global__ void __launch_bounds__(K2_THREADS) k2_direct_post(K2Params P) {
         }
         if (lane == 0) {
             const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+            PFT_BOUND((size_t)b * P.W + s, P.out_elems);
             out[s] = v;
             if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
         }

@@ -8,6 +8,21 @@
 
 namespace pftdev {
 
+// Checked builds (build.py --checked, -DPFT_CHECKED): every workspace / output / input access the
+// kernels compute an index for is bounds-checked against the extents the host passes, and a
+// violation traps the kernel (the launch then fails with a CUDA error).  Product builds compile
+// the checks away.  (compute-sanitizer is closed on this GPU pool: profiles/r02/sanitizer_attempt.txt.)
+#ifdef PFT_CHECKED
+#define PFT_BOUND(idx, n)                                                      \
+    do {                                                                       \
+        if (!(static_cast<uint64_t>(idx) < static_cast<uint64_t>(n))) __trap(); \
+    } while (0)
+#else
+#define PFT_BOUND(idx, n) \
+    do {                  \
+    } while (0)
+#endif
+
 // K1: 8 consumer warps + 1 TMA producer warp.  A stage holds, for 16 rows of A, a chunk of
 // 32 column pairs (l, q-l): the "front" box (columns l ascending) and the "mirror" box
 // (columns q-l), 16 x 32 complex128 each, plus the 32-entry pair table slice
@@ -95,6 +110,8 @@ struct K2Params {
     uint32_t bl_group;             // K2_BLUESTEIN: columns per transform pass (smem: 2 x group x L)
     double2* out;                  // [batch][W]
     int* status;                   // non-finite flag word of the workspace (bit 0)
+    uint64_t y_elems;              // checked builds: elements addressable from Y
+    uint64_t out_elems;            // checked builds: elements of out
 };
 
 // Pair-table entry (host-built): phase_l = e^{-2 pi i mu (l - q/2)/N}, t_l = 1 - 2l/q and
@@ -150,6 +167,9 @@ struct K1Params {
     unsigned* arrivals;         // signal b's control words at arrivals + b * ctl_stride (zeroed once):
                                 // sum tail {tickets, done, ready[P2]}, K2 tail {tickets, done}
     uint64_t ctl_stride;        // words between consecutive signals' control words
+    uint64_t in_elems;          // checked builds: elements addressable from a
+    uint64_t y_elems;           // checked builds: elements addressable from Y
+    uint64_t ctl_words;         // checked builds: words addressable from arrivals
     int k2_tail;                // K2 work done by the last `reducers` CTAs of a signal to write
                                 // their slab (last-arrival, no grid-wide wait; see k1_k2_tail)
     uint32_t k2_group;          // k2_tail: columns j per FFT group (the group's Z + scratch fit the ring)

@@ -506,6 +506,12 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
     auto P2 = d->k2_params(w.Y, w.y_stride, out, w.status);
     P1.arrivals = w.arrivals;
     P1.ctl_stride = w.ctl_stride;
+    // extents for checked builds (PFT_BOUND): what this call may address
+    P1.in_elems = (uint64_t)(batch - 1) * in_stride + d->host.N;
+    P1.y_elems = (uint64_t)(batch - 1) * w.y_stride + d->data_elems();
+    P1.ctl_words = (uint64_t)(batch - 1) * w.ctl_stride + d->counters_per_signal();
+    P2.y_elems = P1.y_elems;
+    P2.out_elems = (uint64_t)batch * d->W;
     // An isolated transform (no overlap with a neighbour) whose grid leaves half the CTA slots
     // idle runs two CTAs (a cluster) per residue class, each streaming half of the column chunks:
     // one transform then fills both slots of every SM (C2b: 128 -> 256 CTAs).
@@ -1116,8 +1122,10 @@ pft_status pft_execute_partial(pft_dplan_t dh, const pft_c128* d_in_local, int w
     PFT_REQUIRE(row_stride >= v.row_len, "execute_partial: row_stride < local row length");
     DeviceGuard guard(d->device);
     const CUtensorMap map = make_input_map(d, d_in_local, v.row_len, row_stride, 1, 0);
-    const auto P = d->k1_params(v, reinterpret_cast<const double2*>(d_in_local), row_stride, 0,
-                                reinterpret_cast<double2*>(d_partial), d->slab_elems(), false);
+    auto P = d->k1_params(v, reinterpret_cast<const double2*>(d_in_local), row_stride, 0,
+                          reinterpret_cast<double2*>(d_partial), d->slab_elems(), false);
+    P.in_elems = d->host.p * row_stride;
+    P.y_elems = d->slab_elems();
     cuda_check(pftdev::launch_k1(map, P, d->host.r, 1, d->mu0, static_cast<cudaStream_t>(stream)), "K1 launch");
     PFT_API_END
 }
@@ -1128,8 +1136,10 @@ pft_status pft_finalize(pft_dplan_t dh, const pft_c128* d_partial, size_t batch,
     if (batch == 0) return PFT_OK;
     PFT_REQUIRE(d_partial && d_out, "finalize: null buffer");
     DeviceGuard guard(d->device);
-    const auto P = d->k2_params(reinterpret_cast<const double2*>(d_partial), d->slab_elems(),
-                                reinterpret_cast<double2*>(d_out), d->own_status());
+    auto P = d->k2_params(reinterpret_cast<const double2*>(d_partial), d->slab_elems(),
+                          reinterpret_cast<double2*>(d_out), d->own_status());
+    P.y_elems = batch * d->slab_elems();
+    P.out_elems = batch * d->W;
     cuda_check(pftdev::launch_k2(P, d->host.r, (uint32_t)batch, static_cast<cudaStream_t>(stream)), "K2 launch");
     PFT_API_END
 }

@@ -109,9 +109,11 @@ int main() {
 
 def _demo(tmp_path):
     exe = tmp_path / "demo"
-    _compile(["g++", "-std=c++20", "-Wall", "-Werror", "-pthread", "-I", str(ROOT / "include"),
-              str(ROOT / "examples" / "cpp_api_demo.cpp"), "-L", str(LIB.parent), "-lpft_b200",
-              f"-Wl,-rpath,{LIB.parent}"], exe)
+    cuda = Path(shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc").resolve().parents[1]
+    _compile(["g++", "-std=c++20", "-Wall", "-Werror", "-pthread", "-I", str(ROOT / "include"), "-I",
+              str(cuda / "include"), str(ROOT / "examples" / "cpp_api_demo.cpp"), "-L", str(LIB.parent),
+              "-lpft_b200", "-L", str(cuda / "lib64"), "-lcudart", f"-Wl,-rpath,{LIB.parent}",
+              f"-Wl,-rpath,{cuda / 'lib64'}"], exe)
     return exe
 
 
@@ -133,3 +135,4 @@ def test_cpp_api_demo_executes_on_the_gpu(tmp_path, pft):
     res = subprocess.run([str(exe), "--require-gpu"], capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "4 threads x 3 executes on one plan" in res.stdout
+    assert "execute_sharded (1 rank)" in res.stdout
