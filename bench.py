@@ -243,9 +243,9 @@ def run_ours(args):
     B = B_total // world if B_total > 1 else 1
     scaling = "strong" if B_total > 1 else "weak"
 
-    # inputs: >= 2 buffers, together > 2x L2, rotated so no step re-reads a cached input (a
-    # batched input is one buffer far larger than L2)
-    nbuf = 1 if (B > 1 or 16 * N >= 16 * L2_BYTES) else max(2, -(-2 * L2_BYTES // (16 * N)))
+    # inputs: >= 4 buffers, together >= 8x L2 (126 MiB), rotated so no step re-reads an input still
+    # in L2 (a batched input is one buffer far larger than L2; C5 one 16 GiB signal)
+    nbuf = 1 if (B > 1 or 16 * N >= 16 * L2_BYTES) else max(4, -(-8 * L2_BYTES // (16 * N)))
     bufs = [torch.empty(N * B, dtype=torch.complex128, device=dev) for _ in range(nbuf)]
     for i, b in enumerate(bufs):
         make_input_device(pft, b, N * B, mu, M, SEEDS[args.config] + (0 if B > 1 else 100 * rank), kind,
@@ -450,7 +450,7 @@ def run_ours(args):
                        "parallelism": (f"signals sharded over {world} GPUs" if B_total > 1 else
                                        f"replicas x{world}") if world > 1 else "single GPU",
                        "l2": (f"one input of {16 * N * B / 2**30:.2f} GiB (> L2 126 MiB)" if nbuf == 1 else
-                              f"{nbuf} rotating inputs of {16 * N / 2**20:.0f} MiB (> L2 126 MiB)"),
+                              f"{nbuf} rotating inputs of {16 * N / 2**20:.1f} MiB ({nbuf * 16 * N / L2_BYTES:.1f}x L2)"),
                        "timing": "CUDA graph of K steps, CUDA events on the launch stream",
                        "streams": args.streams, "overlap_previous": overlap,
                        "tail": {"sum tail": "sum tail in K1 (one kernel per execute)",

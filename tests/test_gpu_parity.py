@@ -48,9 +48,9 @@ CASES = [
     (3 * 5 * 7 * 64, 20, 11, 3 * 5 * 64, 1e-12, "normal"),  # odd q = 7
     (2 ** 20, 2 ** 12, 2 ** 18, 2 ** 14, 1e-12, "uniform"),  # M/p = 1/4
     (2 ** 20, 300, 12345, 512, 1e-12, "uniform"),  # sum tail with W = 601 > p: bins wrap mod p
-    (6220800, 1000, -12345, 15360, 1e-12, "normal"),  # C4 at the autotuned p
+    (6220800, 1000, -12345, 15360, 1e-12, "normal"),  # C4, P2 = 120 (the bench plans: test_gpu_bench_plans.py)
     (6220800, 1000, -12345, 16200, 1e-12, "normal"),  # C4, non-power-of-two P2 = 135, P1 = 120
-    (2 ** 24, 2 ** 6, 2 ** 22, 2048, 1e-12, "uniform"),  # C2a at the autotuned p (P1 = 32)
+    (2 ** 24, 2 ** 6, 2 ** 22, 2048, 1e-12, "uniform"),  # C2a, P1 = 32 (round-1 autotuned pick)
 ]
 
 

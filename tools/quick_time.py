@@ -40,7 +40,7 @@ def run(cfg: str, p: int, opts: dict, reps: int, check: bool) -> dict:
     N, M, mu, _, kind, _ = bench.CONFIGS[cfg]
     B = bench.BATCH.get(cfg, 1)
     W = 2 * M + 1
-    nbuf = 1 if (B > 1 or 16 * N >= 16 * bench.L2_BYTES) else max(2, -(-2 * bench.L2_BYTES // (16 * N)))
+    nbuf = 1 if (B > 1 or 16 * N >= 16 * bench.L2_BYTES) else max(4, -(-8 * bench.L2_BYTES // (16 * N)))
     bufs = [torch.empty(N * B, dtype=torch.complex128, device="cuda") for _ in range(nbuf)]
     for i, b in enumerate(bufs):
         bench.make_input_device(pft, b, N * B, mu, M, bench.SEEDS[cfg], kind, offset=(0 if B > 1 else i * N), N=N)
