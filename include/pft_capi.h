@@ -275,7 +275,8 @@ pft_status pft_select_divisor_sharded(pft_table_t t, uint64_t N, uint64_t M, dou
 pft_status pft_dplan_device(pft_dplan_t d, int* device);
 
 /* Status word of a workspace (bit 0 = non-finite output, i.e. non-finite input, since the last
- * reset).  Synchronises `stream`.  pft_status_query reads the plan's own workspace (executes
+ * reset; bit 1 = a device-side wait of the K2 worker / ring forms ran into its bound -- an
+ * internal error, the outputs of that execute are invalid).  Synchronises `stream`.  pft_status_query reads the plan's own workspace (executes
  * with d_ws == NULL, and pft_finalize). */
 pft_status pft_workspace_status(pft_dplan_t d, void* d_ws, void* stream, int* flags, int reset);
 pft_status pft_status_query(pft_dplan_t d, void* stream, int* flags, int reset);
@@ -330,7 +331,8 @@ pft_status pft_sparse_tones(uint64_t seed, int n, int64_t lo, int64_t hi, int64_
 pft_status pft_launches_per_execute(pft_dplan_t d, int* launches);
 /* How an unsharded execute finishes after the contraction + first FFT pass (K1):
  * 0 separate K2 grid, 1 sum tail in K1 (few bins), 2 K2 work by K1's last arrivals (many
- * bins), 3 K2 in K1 behind a grid barrier (opt-in). */
+ * bins), 3 K2 in K1 behind a grid barrier (opt-in), 4 K2 worker CTAs riding in K1's grid when
+ * the execute overlaps its predecessor (PFT_EXEC_OVERLAP_PREVIOUS), a separate K2 grid otherwise. */
 pft_status pft_dplan_tail_kind(pft_dplan_t d, int* kind);
 /* The second-pass form a device plan runs (PFT_PASS2_*, never _AUTO). */
 pft_status pft_dplan_second_pass(pft_dplan_t d, int* form);

@@ -591,7 +591,7 @@ class DevicePlan:
         _check(lib().pft_launches_per_execute(self._h, C.byref(n)))
         return n.value
 
-    TAIL_KINDS = ("K2 grid", "sum tail", "K2 tail", "fused K2")
+    TAIL_KINDS = ("K2 grid", "sum tail", "K2 tail", "fused K2", "K2 workers in K1 (chained) / K2 grid")
 
     def tail_kind(self) -> str:
         """How execute finishes after K1: "K2 grid", "sum tail", "K2 tail" (K2's work by K1's

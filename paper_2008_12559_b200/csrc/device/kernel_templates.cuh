@@ -616,7 +616,242 @@ __device__ __forceinline__ void k1_k2_tail(const K1Params& P, uint32_t c, uint32
     }
 }
 
-template <int R, bool MU0, bool K2T = false>
+// One Stockham stage of the ring K2 on the slab's own layout: element (c, j) at c * R + j, the
+// R columns of a point travelling together.  Work item idx = jj * R + j (j fastest): its RAD
+// loads src[idx + r * nb * R] are contiguous across a warp; the stores are contiguous in runs of
+// Ns * R elements (the first stage's, Ns = 1, in runs of R).  Same butterflies, twiddles and
+// order as stockham_stage_fixed, so a column's result is bitwise the one the K2 grid computes.
+// pre: four-step twiddles omega_p^{m1 c} folded into the first stage's loads (null = none).
+template <int RAD, int R>
+__device__ __forceinline__ void k2_ring_stage(const double2* __restrict__ src, double2* __restrict__ dst, int n, int Ns,
+                                              int lg_ns, const double2* __restrict__ tw, const double2* __restrict__ pre,
+                                              int t0, int nt) {
+    const int nb = n / RAD;
+    const uint32_t tstride = (uint32_t)(n / (Ns * RAD));
+    for (int idx = t0; idx < nb * R; idx += nt) {
+        const int jj = idx / R, j = idx - jj * R;
+        const int k = jj & (Ns - 1);
+        const int base = ((jj >> lg_ns) << lg_ns) * RAD + k;
+        double2 v[RAD];
+#pragma unroll
+        for (int r = 0; r < RAD; ++r) v[r] = src[idx + r * nb * R];
+        if (pre) {
+#pragma unroll
+            for (int r = 0; r < RAD; ++r) {
+                const int c = jj + r * nb;
+                if (c != 0) v[r] = cmul(v[r], pre[c]);
+            }
+        }
+        if (k != 0) {
+#pragma unroll
+            for (int r = 1; r < RAD; ++r) v[r] = cmul(v[r], tw[(uint32_t)(k * r) * tstride]);
+        }
+        if constexpr (RAD == 2) dft2(v[0], v[1]);
+        if constexpr (RAD == 4) dft4(v[0], v[1], v[2], v[3]);
+        if constexpr (RAD == 8) dft8(v);
+        if constexpr (RAD == 16) dft16(v);
+#pragma unroll
+        for (int r = 0; r < RAD; ++r) dst[(base + r * Ns) * R + j] = v[r];
+    }
+}
+
+// K2 worker CTAs inside K1's grid (chained executes of one long transform with many bins: C2c).
+// The grid carries `workers` extra CTAs after the P2 streaming CTAs.  They are dispatched last, so
+// they land in the SM slots the streamers leave free (C2c: 256 streamers + 40 workers = the 296
+// slots), release the next launch at once, and wait for the slab counter to reach P2 (each
+// streamer bumps it after its slab store).  Then worker w runs K2 for m1 = w, w + workers, ...
+// as a bulk-copy ring: the slab is stored in two column groups per m1 ([m1][group][c][j'],
+// K1Params.slab_split) so a group (P2 x ceil(R/2) complex128) is one contiguous cp.async.bulk,
+// issued by the CTA's ninth warp (K1's producer/consumer pattern: full/empty mbarriers) into one of
+// two load buffers while the eight consumer warps work on the other; the length-P2 stages (radix
+// 8/4/2: the CTA keeps K1's register budget) ping-pong between the load buffer and a scratch
+// buffer on the group's own (c, j') layout, and a bin's Eq. (7) sum continues in registers from the first group into the
+// second (one ascending-j fma chain).  With one kernel per execute the next transform's K1 is a
+// direct programmatic dependent of this one: its streamers take the streamers' slots as they exit
+// and stream while these workers finish -- a separate K2 kernel between two K1s cost the chain
+// ~7 us even when empty (profiles/r02/ab_ring_k2.jsonl).  The next K1 writes the slab only after
+// its griddepcontrol.wait, i.e. after every worker here has exited.
+template <int R>
+__device__ __forceinline__ void k1_k2_worker(const K1Params& P, uint32_t w, uint32_t b, unsigned char* smem) {
+    const K2Params& Q = P.k2;
+    constexpr int G0 = (R + 1) / 2, G1 = R - G0, NG = G1 > 0 ? 2 : 1;
+    constexpr int NOUT = 2;   // bins per consumer thread and m1 (host: ceil(W / P1) <= NOUT * NT)
+    constexpr int NT = 32 * K1_CONSUMER_WARPS;  // consumer threads (warps 0..7); warp 8 loads
+    constexpr uint32_t kSpinLimit = 1u << 22;   // bounded waits: a lost signal becomes status bit 2, not a hang
+    const int tid = threadIdx.x;
+    const uint32_t n = P.P2, cap = n * (uint32_t)G0;
+    double2* bufs = reinterpret_cast<double2*>(smem);     // [3][cap]: load buffers 0 and 1, FFT scratch 2
+    double2* tw2 = bufs + 3 * (size_t)cap;                // omega_P2^t
+    double2* pre = tw2 + n;                               // omega_p^{m1 c}
+    uint64_t* full = reinterpret_cast<uint64_t*>(pre + n);  // [2] slab group landed
+    uint64_t* empty = full + 2;                              // [2] load buffer consumed
+    unsigned* ctl = P.arrivals + (size_t)b * P.ctl_stride;  // {slabs stored, workers done}
+    PFT_BOUND((size_t)b * P.ctl_stride + 1, P.ctl_words);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint32_t NW = P.workers;
+    const uint32_t nk = w < P.P1 ? (P.P1 - w + NW - 1) / NW : 0;
+    const uint32_t nq = nk * NG;  // (m1, group) steps, in order
+    if (tid == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        fence_barrier_init();
+    }
+    if (tid < NT) {
+        for (uint32_t c = tid; c < n; c += NT) tw2[c] = __ldg(P.omega + (size_t)c * P.P1);
+        if (nk > 0)
+            for (uint32_t c = tid; c < n; c += NT) pre[c] = __ldg(P.omega + (size_t)w * c);
+    }
+    // the previous grid (the workers of the previous transform re-arm this signal's counters as
+    // they finish, and read the slab this transform's streamers rewrite) must be complete first
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __syncthreads();  // barriers and tables ready; the two roles part here
+    if (tid >= NT) {
+        // ---- loader warp: one lane waits for the slab, then keeps two groups in flight
+        if (tid == NT && nq > 0) {
+            uint32_t spins = 0;
+            while (ld_acquire_u32(ctl) < P.P2) {
+                __nanosleep(256);
+                if (++spins > kSpinLimit) {
+                    atomicOr(Q.status, 2);
+                    break;
+                }
+            }
+            __threadfence();
+            asm volatile("fence.proxy.async;" ::: "memory");  // the streamers' slab stores before the bulk reads
+            const double2* __restrict__ Yb = P.Y + (size_t)b * P.y_stride;
+            for (uint32_t q = 0; q < nq; ++q) {
+                const uint32_t lb = q & 1u;
+                if (q >= 2) {  // the consumers have finished with this buffer's previous group
+                    const uint32_t par = ((q >> 1) - 1u) & 1u;
+                    spins = 0;
+                    while (!mbar_try_wait(&empty[lb], par))
+                        if (++spins > kSpinLimit) {
+                            atomicOr(Q.status, 2);
+                            break;
+                        }
+                }
+                const uint32_t m1 = w + (q / NG) * NW, g = q % NG;
+                const uint32_t bytes = n * (uint32_t)(g ? G1 : G0) * (uint32_t)sizeof(double2);
+                const size_t off = (size_t)m1 * n * R + (g ? (size_t)n * G0 : 0);
+                PFT_BOUND((size_t)b * P.y_stride + off + bytes / sizeof(double2) - 1, P.y_elems);
+                mbar_arrive_expect_tx(&full[lb], bytes);
+                bulk_load(bufs + (size_t)lb * cap, Yb + off, bytes, &full[lb]);
+            }
+        }
+    } else if (nq > 0) {
+        // ---- consumers (named barrier 1 over the NT consumer threads)
+        auto team_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); };
+        const int lg_n = 31 - __clz((int)n);  // radix schedule of the power-of-two P2: 8s, then one 4 or 2
+        const int64_t Mh = (int64_t)((Q.W - 1) / 2);
+        double2* __restrict__ out = Q.out + (size_t)b * Q.W;
+        double2 acc[NOUT];
+        double tp[NOUT];
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) {
+            acc[o] = make_double2(0.0, 0.0);
+            tp[o] = 0.0;
+        }
+        constexpr int PRE_PER = 2;  // host: P2 <= 512 = PRE_PER * NT
+        double2 pre_next[PRE_PER];
+        for (uint32_t q = 0; q < nq; ++q) {
+            const uint32_t m1 = w + (q / NG) * NW, g = q % NG, lb = q & 1u;
+            const uint64_t s0 = (uint64_t)((m1 + P.P1 - Q.first_mod_p1) % P.P1);
+            if (g == NG - 1 && q + 1 < nq) {  // the next m1's four-step twiddles, stored after the stages
+#pragma unroll
+                for (int i = 0; i < PRE_PER; ++i) {
+                    const uint32_t c = tid + i * NT;
+                    if (c < n) pre_next[i] = __ldg(P.omega + (size_t)(m1 + NW) * c);  // (m1 + NW) c < p
+                }
+            }
+            {
+                uint32_t spins = 0;
+                while (!mbar_try_wait(&full[lb], (q >> 1) & 1u))
+                    if (++spins > kSpinLimit) {
+                        atomicOr(Q.status, 2);
+                        break;
+                    }
+            }
+            double2* src = bufs + (size_t)lb * cap;
+            double2* dst = bufs + 2 * (size_t)cap;
+            int Ns = 1, lg_ns = 0;
+            while (lg_ns < lg_n) {
+                const int lgr = lg_n - lg_ns >= 3 ? 3 : lg_n - lg_ns, RAD = 1 << lgr;
+                const double2* pr = (lg_ns == 0 && m1 != 0) ? pre : nullptr;
+                if (g == 0) {
+                    if (RAD == 8) k2_ring_stage<8, G0>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, NT);
+                    else if (RAD == 4) k2_ring_stage<4, G0>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, NT);
+                    else k2_ring_stage<2, G0>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, NT);
+                } else if constexpr (G1 > 0) {
+                    if (RAD == 8) k2_ring_stage<8, G1>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, NT);
+                    else if (RAD == 4) k2_ring_stage<4, G1>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, NT);
+                    else k2_ring_stage<2, G1>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, NT);
+                }
+                lg_ns += lgr;
+                Ns *= RAD;
+                team_sync();
+                double2* t = src;
+                src = dst;
+                dst = t;
+            }
+            if (g == NG - 1 && q + 1 < nq) {  // pre[] was last read in this m1's last first stage
+#pragma unroll
+                for (int i = 0; i < PRE_PER; ++i) {
+                    const uint32_t c = tid + i * NT;
+                    if (c < n) pre[c] = pre_next[i];
+                }
+            }
+            const int gw = g ? G1 : G0, j0 = g ? G0 : 0;
+#pragma unroll
+            for (int o = 0; o < NOUT; ++o) {
+                const uint64_t s = s0 + (uint64_t)P.P1 * (tid + o * NT);
+                if (s >= Q.W) continue;
+                uint64_t mp = Q.first_mod_p + s % Q.p;
+                if (mp >= Q.p) mp -= Q.p;
+                const uint32_t m2 = (uint32_t)(mp / P.P1);
+                const double x = (double)((int64_t)s - Mh) * Q.inv_p;
+                const double2* rv = src + (size_t)m2 * gw;
+                double2 a = acc[o];
+                double t = tp[o];
+#pragma unroll
+                for (int jj = 0; jj < G0; ++jj) {  // ascending j, this group's columns
+                    if (jj >= gw) break;
+                    const double2 v = rv[jj];
+                    if (j0 + jj == 0) {
+                        a = v;
+                        t = x;
+                    } else {
+                        a.x = fma(v.x, t, a.x);
+                        a.y = fma(v.y, t, a.y);
+                        if (j0 + jj + 1 < R) t *= x;
+                    }
+                }
+                acc[o] = a;
+                tp[o] = t;
+                if (g == NG - 1) {
+                    const double2 v = cmul(a, __ldg(Q.post_twiddles + s));  // e^{-pi i m / p}
+                    PFT_BOUND((size_t)b * Q.W + s, Q.out_elems);
+                    out[s] = v;
+                    if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(Q.status, 1);
+                }
+            }
+            // this step's reads and writes of the load buffer precede its asynchronous refill
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            team_sync();  // also: the scratch and pre[] are free for the next step
+            if (tid == 0) mbar_arrive(&empty[lb]);
+        }
+    }
+    __syncthreads();
+    // the last worker to finish re-arms the signal's counters
+    if (tid == 0 && atomicAdd(ctl + 1, 1u) == NW - 1) {
+        ctl[0] = 0;
+        ctl[1] = 0;
+        __threadfence();
+    }
+}
+
+template <int R, bool MU0, int TK = 0>
 __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_constant__ CUtensorMap tmap,
                                                                   const K1Params P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -632,6 +867,14 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     uint64_t* empty = full + S;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if constexpr (TK == 2) {  // K2 worker CTAs ride at the end of the grid (see k1_k2_worker)
+        const uint32_t streamers = P.P2 * (P.split > 1 ? P.split : 1);
+        if (P.workers && blockIdx.x >= streamers) {
+            unsigned char* wbase = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+            k1_k2_worker<R>(P, blockIdx.x - streamers, blockIdx.y, wbase);
+            return;
+        }
+    }
     if (tid == 0) {
         for (uint32_t s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -824,6 +1067,26 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     }
     // Y[b][m1][c][j]: the slab for one m1 is contiguous over (c, j) for K2.
     double2* __restrict__ Y = P.Y + (size_t)b * P.y_stride;
+    if constexpr (TK == 2) {
+        if (P.workers) {
+            // two column groups per m1, each contiguous over (c, j') for the workers' bulk copies
+            constexpr uint32_t G0 = (R + 1) / 2, G1 = R - G0;
+            for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) {
+                const uint32_t m1 = idx / R, j = idx - m1 * R;
+                const size_t at = (size_t)m1 * P.P2 * R +
+                                  (j < G0 ? (size_t)c * G0 + j : (size_t)P.P2 * G0 + (size_t)c * G1 + (j - G0));
+                PFT_BOUND((size_t)b * P.y_stride + at, P.y_elems);
+                Y[at] = res[(size_t)j * P.P1 + m1];
+            }
+            __syncthreads();  // the CTA's slab stores precede thread 0's fence and count
+            if (tid == 0) {
+                __threadfence();
+                PFT_BOUND((size_t)b * P.ctl_stride, P.ctl_words);
+                atomicAdd(P.arrivals + (size_t)b * P.ctl_stride, 1u);
+            }
+            return;
+        }
+    }
     for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) {
         const uint32_t m1 = idx / R, j = idx - m1 * R;
         PFT_BOUND((size_t)b * P.y_stride + ((size_t)m1 * P.P2 + c) * R + j, P.y_elems);
@@ -831,7 +1094,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     }
     // the K2 tail lives in its own instantiations (K2T, k1_k2_tail_instantiated(R)): its code in
     // every K1 cost C2b 2% (same-box A/B: 43.0 vs 42.2 us) though C2b never takes it
-    if constexpr (K2T) {
+    if constexpr (TK == 1) {
         if (P.k2_tail) {
             k1_k2_tail<R>(P, c, b, reinterpret_cast<double2*>(ring));
             return;
@@ -1029,6 +1292,150 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_loop(K2Params P) {
         __syncthreads();  // smem reuse by the next m1
     }
     if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// K2 FFT form as a ring on a narrow grid (chained executes of single long transforms: C2c).
+// K1's grid leaves a few SMs without a CTA (C2c: 256 CTAs at two per SM on 128 of the 148 SMs);
+// this kernel's k2_ctas CTAs (one per such SM: three slab buffers, up to the whole shared memory)
+// hold those SMs while the NEXT transform's K1 -- launched as soon as every CTA here has started --
+// streams on the others, so the second pass no longer idles HBM between two streams.  Each CTA
+// loops over m1 = blockIdx.x, + gridDim.x, ...: the m1 slab Y[m1][c][j] (contiguous P2 * R
+// complex128) arrives by one cp.async.bulk per slab, two slabs ahead of the FFT (mbarrier
+// complete_tx), the length-P2 Stockham stages run on the slab's own (c, j) layout between two of
+// the three buffers, and Eq. (7) reads the result where it lies.  Power-of-two P2 with radices
+// 2/4/8/16 only; the post powers are formed in registers as in k2_fft_loop.
+template <int R>
+__global__ void __launch_bounds__(K2_THREADS, 1) k2_ring(K2Params P) {
+    extern __shared__ __align__(128) unsigned char k2r_raw[];
+    const uint32_t n = P.P2, slab = n * (uint32_t)R;
+    double2* bufs = reinterpret_cast<double2*>(k2r_raw);  // [3][slab]
+    double2* tw2 = bufs + 3 * (size_t)slab;               // omega_P2^t
+    double2* pre = tw2 + n;                               // omega_p^{m1 c}
+    uint64_t* full = reinterpret_cast<uint64_t*>(pre + n);  // one mbarrier per buffer
+    const int tid = threadIdx.x;
+    const uint32_t b = blockIdx.y, G = gridDim.x;
+    if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (tid == 0) {
+        for (int s = 0; s < 3; ++s) mbar_init(&full[s], 1);
+        fence_barrier_init();
+    }
+    for (uint32_t c = tid; c < n; c += blockDim.x) tw2[c] = __ldg(P.omega + (size_t)c * P.P1);
+    const uint32_t m1_first = blockIdx.x;
+    const uint32_t nk = m1_first < P.P1 ? (P.P1 - m1_first + G - 1) / G : 0;
+    constexpr int PRE_PER = 4;  // P2 <= PRE_PER * K2_THREADS
+    double2 pre_next[PRE_PER];
+#pragma unroll
+    for (int i = 0; i < PRE_PER; ++i) {
+        const uint32_t c = tid + i * K2_THREADS;
+        pre_next[i] = (nk > 0 && c < n) ? __ldg(P.omega + (size_t)m1_first * c) : make_double2(1.0, 0.0);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's slab complete and visible
+    __syncthreads();
+    const double2* __restrict__ Yb = P.Y + (size_t)b * P.y_stride;
+    const uint32_t bytes = slab * (uint32_t)sizeof(double2);
+    // buffer roles: ia = this m1's slab, ib = the next one's (in flight), ic = free (FFT scratch)
+    uint32_t ia = 0, ib = 1, ic = 2, phase = 0;  // phase bit s = parity the next wait on buffer s uses
+    if (tid == 0) {
+        for (uint32_t k = 0; k < 2 && k < nk; ++k) {
+            PFT_BOUND((size_t)b * P.y_stride + ((size_t)(m1_first + k * G) + 1) * slab - 1, P.y_elems);
+            mbar_arrive_expect_tx(&full[k], bytes);
+            bulk_load(bufs + (size_t)k * slab, Yb + (size_t)(m1_first + k * G) * slab, bytes, &full[k]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < PRE_PER; ++i) {
+        const uint32_t c = tid + i * K2_THREADS;
+        if (c < n) pre[c] = pre_next[i];
+    }
+    __syncthreads();
+    const int64_t Mh = (int64_t)((P.W - 1) / 2);
+    double2* __restrict__ out = P.out + (size_t)b * P.W;
+    for (uint32_t k = 0; k < nk; ++k) {
+        const uint32_t m1 = m1_first + k * G;
+        if (k + 1 < nk) {
+#pragma unroll
+            for (int i = 0; i < PRE_PER; ++i) {
+                const uint32_t c = tid + i * K2_THREADS;
+                if (c < n) pre_next[i] = __ldg(P.omega + (size_t)(m1 + G) * c);  // (m1 + G) c < p
+            }
+        }
+        // this thread's first output slot of m1 and its post twiddle (latency hidden by the FFT)
+        const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
+        const uint64_t s_first = s0 + (uint64_t)P.P1 * tid;
+        double2 ptw0 = make_double2(0.0, 0.0);
+        if (s_first < P.W) ptw0 = __ldg(P.post_twiddles + s_first);
+        {  // bounded: a lost completion becomes status bit 2, not a hang
+            uint32_t spins = 0;
+            while (!mbar_try_wait(&full[ia], (phase >> ia) & 1u))
+                if (++spins > (1u << 22)) {
+                    atomicOr(P.status, 2);
+                    break;
+                }
+        }
+        phase ^= 1u << ia;
+        double2* src = bufs + (size_t)ia * slab;
+        double2* dst = bufs + (size_t)ic * slab;
+        uint32_t isrc = ia, idst = ic;
+        int Ns = 1, lg_ns = 0;
+        for (int st = 0; st < P.fft2.count; ++st) {
+            const int RAD = P.fft2.radix[st];
+            const double2* pr = (st == 0 && m1 != 0) ? pre : nullptr;
+            switch (RAD) {
+                case 2: k2_ring_stage<2, R>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, K2_THREADS); lg_ns += 1; break;
+                case 4: k2_ring_stage<4, R>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, K2_THREADS); lg_ns += 2; break;
+                case 8: k2_ring_stage<8, R>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, K2_THREADS); lg_ns += 3; break;
+                default: k2_ring_stage<16, R>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, K2_THREADS); lg_ns += 4; break;
+            }
+            Ns *= RAD;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before a buffer's async refill
+            __syncthreads();
+            double2* t = src;
+            src = dst;
+            dst = t;
+            const uint32_t ti = isrc;
+            isrc = idst;
+            idst = ti;
+        }
+        // the result is in buffer isrc; idst is free: the slab two m1 ahead lands there
+        if (tid == 0 && k + 2 < nk) {
+            PFT_BOUND((size_t)b * P.y_stride + ((size_t)(m1 + 2 * G) + 1) * slab - 1, P.y_elems);
+            mbar_arrive_expect_tx(&full[idst], bytes);
+            bulk_load(bufs + (size_t)idst * slab, Yb + (size_t)(m1 + 2 * G) * slab, bytes, &full[idst]);
+        }
+        if (k + 1 < nk) {  // pre[] was last read in the first stage
+#pragma unroll
+            for (int i = 0; i < PRE_PER; ++i) {
+                const uint32_t c = tid + i * K2_THREADS;
+                if (c < n) pre[c] = pre_next[i];
+            }
+        }
+        const double2* res = src;
+        for (uint64_t s = s_first; s < P.W; s += (uint64_t)P.P1 * K2_THREADS) {
+            uint64_t mp = P.first_mod_p + s % P.p;
+            if (mp >= P.p) mp -= P.p;
+            const uint32_t m2 = (uint32_t)(mp / P.P1);
+            const double x = (double)((int64_t)s - Mh) * P.inv_p;
+            const double2* rv = res + (size_t)m2 * R;
+            double2 acc = rv[0];
+            double tp = x;
+#pragma unroll
+            for (int j = 1; j < R; ++j) {  // ascending j
+                const double2 v = rv[j];
+                acc.x = fma(v.x, tp, acc.x);
+                acc.y = fma(v.y, tp, acc.y);
+                if (j + 1 < R) tp *= x;
+            }
+            const double2 v = cmul(acc, s == s_first ? ptw0 : __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
+            PFT_BOUND((size_t)b * P.W + s, P.out_elems);
+            out[s] = v;
+            if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
+        }
+        __syncthreads();  // the result buffer becomes the next m1's scratch
+        const uint32_t na = ib, nb_ = idst, nc = isrc;
+        ia = na;
+        ib = nb_;
+        ic = nc;
+    }
 }
 
 // K2, Bluestein (chirp-z) form, for P2 with prime factors the in-smem Stockham radices do not
@@ -1342,11 +1749,18 @@ cudaError_t launch_k1_r(const CUtensorMap& map, const K1Params& P, dim3 grid, si
     cfg.numAttrs = n;
     if constexpr (k1_k2_tail_instantiated(R)) {
         if (P.k2_tail) {
-            if (mu0) return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, true, true>, map, P);
-            return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, false, true>, map, P);
+            if (mu0) return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, true, 1>, map, P);
+            return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, false, 1>, map, P);
         }
     }
     if (P.k2_tail) return cudaErrorInvalidValue;  // no K2-tail instantiation for this r
+    if constexpr (k1_k2_workers_instantiated(R)) {
+        if (P.workers) {
+            if (mu0) return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, true, 2>, map, P);
+            return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, false, 2>, map, P);
+        }
+    }
+    if (P.workers) return cudaErrorInvalidValue;  // no worker instantiation for this r
     if (mu0) return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, true>, map, P);
     return cudaLaunchKernelEx(&cfg, k1_contract_fft<R, false>, map, P);
 }
@@ -1358,8 +1772,13 @@ cudaError_t configure_k1_r(size_t smem, bool mu0) {
                         : cudaFuncSetAttribute(k1_contract_fft<R, false>, a, (int)smem);
     if constexpr (k1_k2_tail_instantiated(R)) {
         if (e == cudaSuccess)
-            e = mu0 ? cudaFuncSetAttribute(k1_contract_fft<R, true, true>, a, (int)smem)
-                    : cudaFuncSetAttribute(k1_contract_fft<R, false, true>, a, (int)smem);
+            e = mu0 ? cudaFuncSetAttribute(k1_contract_fft<R, true, 1>, a, (int)smem)
+                    : cudaFuncSetAttribute(k1_contract_fft<R, false, 1>, a, (int)smem);
+    }
+    if constexpr (k1_k2_workers_instantiated(R)) {
+        if (e == cudaSuccess)
+            e = mu0 ? cudaFuncSetAttribute(k1_contract_fft<R, true, 2>, a, (int)smem)
+                    : cudaFuncSetAttribute(k1_contract_fft<R, false, 2>, a, (int)smem);
     }
     return e;
 }
@@ -1387,6 +1806,10 @@ cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
         cfg.dynamicSmemBytes = k2_bluestein_smem_bytes(P.L);
         return cudaLaunchKernelEx(&cfg, k2_bluestein_post<R>, P);
     }
+    if (P.mode == K2_FFT && P.ring) {
+        cfg.dynamicSmemBytes = k2_ring_smem_bytes(R, P.P2);
+        return cudaLaunchKernelEx(&cfg, k2_ring<R>, P);
+    }
     if (P.mode == K2_FFT && P.k2_ctas > 0) return cudaLaunchKernelEx(&cfg, k2_fft_loop<R>, P);
     if (P.mode == K2_FFT) return cudaLaunchKernelEx(&cfg, k2_fft_post<R>, P);
     if (P.mode == K2_DOT) return cudaLaunchKernelEx(&cfg, k2_dot_post<R>, P);
@@ -1398,6 +1821,8 @@ cudaError_t configure_k2_r(size_t smem) {
     cudaError_t e = cudaFuncSetAttribute(k2_fft_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k2_fft_loop<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k2_ring<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k2_bluestein_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -102,6 +102,7 @@ struct K2Params {
     int mode;                      // K2_DIRECT / K2_FFT / K2_DOT
     uint32_t k2_ctas;              // K2_L2 grid width (0 = 148); K2_FFT: > 0 = looping grid of that width
     int release_next;              // trigger the next launch at K2 start (1) / end (2) (PDL chaining)
+    int ring;                      // K2_FFT on k2_ctas CTAs as a bulk-copy ring over m1 (k2_ring)
     FftRadices fft2;               // radices of P2 (K2_FFT) or of L (K2_BLUESTEIN)
     const double2* chirp;          // K2_BLUESTEIN: [P2] e^{-pi i c^2 / P2}
     const double2* chirp_hat;      // K2_BLUESTEIN: [L] FFT_L of the conjugate chirp kernel / L
@@ -173,6 +174,8 @@ struct K1Params {
     int k2_tail;                // K2 work done by the last `reducers` CTAs of a signal to write
                                 // their slab (last-arrival, no grid-wide wait; see k1_k2_tail)
     uint32_t k2_group;          // k2_tail: columns j per FFT group (the group's Z + scratch fit the ring)
+    uint32_t workers;           // K2 worker CTAs per signal riding after the P2 streamers (k1_k2_worker);
+                                // the slab then has the two-column-group layout [m1][group][c][j']
     int fused;                  // run K2 in K1's tail behind a grid barrier (cooperative launch)
     unsigned* bar;              // grid-barrier state {count, generation} (workspace header, zeroed once)
     K2Params k2;                // K2 parameters for the fused tail
@@ -205,6 +208,10 @@ inline uint32_t k1_pick_stages(int r, uint32_t P1) {
 }
 // Z + scratch (r x P2 each) + omega_P2 + four-step twiddles (P2 each)
 inline size_t k2_smem_bytes(int r, uint32_t P2) { return sizeof(double2) * (2 * (size_t)r * P2 + 2 * (size_t)P2); }
+// ring K2 (k2_ring): three slab buffers (r x P2 each) + omega_P2 + four-step twiddles + 3 mbarriers
+inline size_t k2_ring_smem_bytes(int r, uint32_t P2) {
+    return sizeof(double2) * (3 * (size_t)r * P2 + 2 * (size_t)P2) + 3 * sizeof(uint64_t) + 8;
+}
 // Z (r x P2) + omega_P2 + four-step twiddles
 inline size_t k2_dot_smem_bytes(int r, uint32_t P2) { return sizeof(double2) * ((size_t)r * P2 + 2 * (size_t)P2); }
 
@@ -227,6 +234,13 @@ inline size_t k1_sum_scratch_bytes(uint32_t P1, uint32_t P2) {
 // r values with a K2-tail K1 instantiation: the long single transforms it pays for (C5: r = 6
 // at p = 2^18-2^19; SPEC's pick for N = 2^30 has r = 4).  Other r run the K2 grid.
 __host__ __device__ constexpr bool k1_k2_tail_instantiated(int r) { return r >= 4 && r <= 7; }
+// r values with a K2-worker K1 instantiation (many-bin single transforms: C2c has r = 14)
+__host__ __device__ constexpr bool k1_k2_workers_instantiated(int r) { return r >= 8 && r <= 18; }
+// K2 workers: three buffers of one column group (P2 x ceil(r/2)) + omega_P2 + four-step twiddles +
+// 3 mbarriers (+ alignment slack); must fit K1's shared memory
+inline size_t k1_k2_worker_bytes(int r, uint32_t P2) {
+    return sizeof(double2) * (3 * (size_t)((r + 1) / 2) * P2 + 2 * (size_t)P2) + 4 * sizeof(uint64_t) + 128;
+}
 // K1's last-arrival K2 tail: Z + scratch for `group` columns, omega_P2 + four-step twiddles,
 // ticket word
 inline size_t k1_k2_tail_bytes(uint32_t group, uint32_t P2) {

@@ -289,6 +289,9 @@ struct pft_dplan_s {
     uint32_t k1_stages = pftdev::K1_MIN_STAGES;
     int k2_mode = pftdev::K2_DIRECT;
     uint32_t k2_ctas = 0;
+    uint32_t k2_workers = 0; // chained single executes: K2 worker CTAs riding in K1's grid (k1_k2_worker); 0 = off
+    uint32_t ring_ctas = 0;  // chained single executes: K2 as a bulk-copy ring on this many CTAs (k2_ring); 0 = off
+    bool ring_always = false;  // caller-chosen ring width: isolated executes take the ring too
     bool allow_fuse = false; // K2 fused into K1's tail (opt-in; measured slower at C2b/C4)
     bool allow_split = true; // isolated executes: two CTAs (a cluster) per residue class
     bool sum_tail = false;   // unsharded execute: K1 sum tail, no K2 (few output bins)
@@ -344,7 +347,7 @@ struct pft_dplan_s {
     }
 
     size_t slab_elems() const { return (size_t)host.p * host.r; }
-    size_t counters_per_signal() const { return sum_tail ? P2 + 2 : k2_tail ? 2 : 0; }
+    size_t counters_per_signal() const { return sum_tail ? P2 + 2 : (k2_tail || k2_workers) ? 2 : 0; }
     size_t data_elems() const { return sum_tail ? std::max<size_t>(slab_elems(), (size_t)P2 * W) : slab_elems(); }
     // workspace layout (kernels.cuh): header, then per signal {control words, data}
     size_t ctl_bytes() const { return pftdev::ws_align(4 * counters_per_signal()); }
@@ -538,6 +541,16 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
         P1.k2 = P2;
         cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 (fused) launch");
         return;
+    }
+    if (d->k2_workers && batch == 1 && pdl) {  // one kernel: streamers + K2 workers in the slots they leave free
+        P1.workers = d->k2_workers;
+        P1.k2 = P2;
+        cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 (K2 workers) launch");
+        return;
+    }
+    if (d->ring_ctas && batch == 1 && (pdl || d->ring_always)) {  // K2 under the next transform's stream
+        P2.ring = 1;
+        P2.k2_ctas = d->ring_ctas;
     }
     cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
     cuda_check(pftdev::launch_k2(P2, d->host.r, (uint32_t)batch, st), "K2 launch");
@@ -896,8 +909,6 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         cuda_check(cudaMemcpy(d->d_omega_L, omL.data(), L * sizeof(double2), cudaMemcpyHostToDevice), "upload omega_L");
     }
     cuda_check(pftdev::configure_k1(H.r, (uint32_t)d->P1, d->mu0), "configure K1 (early)");
-    cuda_check(cudaMalloc(&d->d_ws, d->workspace_bytes(1)), "cudaMalloc(workspace)");
-    cuda_check(cudaMemset(d->d_ws, 0, d->workspace_bytes(1)), "cudaMemset(workspace)");
     cuda_check(pftdev::configure_k1(H.r, (uint32_t)d->P1, d->mu0), "configure K1");
     cuda_check(pftdev::configure_k2(H.r, (uint32_t)d->P2), "configure K2");
     d->k1_capacity = (uint64_t)pftdev::k1_max_active_per_sm(H.r, (uint32_t)d->P1, d->k1_stages, d->mu0) *
@@ -914,6 +925,36 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         const uint64_t cap = d->sum_tail && d->k1_capacity > d->P2 ? d->k1_capacity - d->P2 : d->k1_capacity - 1;
         d->reducers = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(d->reducers, cap));
     }
+    // Second pass of chained single executes whose K2 is its own grid (many bins: C2c).  A K2 kernel
+    // between two K1s keeps the next K1 from starting until this K1 has completed (measured: an
+    // empty K2 still costs the chain ~7 us), so the K2 work rides inside K1's grid instead:
+    // K2 worker CTAs (k1_k2_worker) in the slots the P2 streamers leave free, taken when their m1
+    // rounds (~8 us per m1 beside a streaming K1, measured at C2c) fit within the stream.
+    // tail_ctas overrides the count; k2_at = GRID or a caller-chosen k2_grid_ctas turns them off.
+    // k2_grid_ctas > 0 on such a plan selects the ring K2 kernel (k2_ring) on that many CTAs.
+    {
+        const bool pow2 = d->P2 >= 4 && (d->P2 & (d->P2 - 1)) == 0;
+        const bool eligible = !d->sum_tail && !d->k2_tail && !d->allow_fuse && d->k2_mode == pftdev::K2_FFT && pow2 &&
+                              batch_hint <= 1;
+        const uint64_t free_slots = d->k1_capacity > d->P2 ? d->k1_capacity - d->P2 : 0;
+        if (eligible && d->k2_ctas == 0 && k2_at != PFT_K2_AT_GRID && pftdev::k1_k2_workers_instantiated(H.r) &&
+            pftdev::k1_k2_worker_bytes(H.r, (uint32_t)d->P2) <= pftdev::k1_smem_bytes(H.r, (uint32_t)d->P1, d->k1_stages) &&
+            (d->W + d->P1 - 1) / d->P1 <= 2ull * 32 * pftdev::K1_CONSUMER_WARPS && d->P2 <= 512 && free_slots >= 8) {
+            uint64_t nw = std::min<uint64_t>(free_slots, d->P1);
+            if (tail_ctas > 0) nw = std::min<uint64_t>(nw, (uint64_t)tail_ctas);
+            const double rounds = (double)((d->P1 + nw - 1) / nw);
+            const double stream_us = 16.0 * (double)H.N / 6.5e6;
+            if (k2_at == PFT_K2_AT_TAIL || rounds * 8.0 <= stream_us) d->k2_workers = (uint32_t)nw;
+        }
+        if (!d->k2_workers && eligible && d->k2_ctas > 0 && d->P2 <= 4ull * pftdev::K2_THREADS &&
+            pftdev::k2_ring_smem_bytes(H.r, (uint32_t)d->P2) <= (size_t)227 * 1024) {
+            d->ring_ctas = d->k2_ctas;
+            d->ring_always = true;
+        }
+    }
+    // the plan's own batch-1 workspace (after every choice that sizes the control words)
+    cuda_check(cudaMalloc(&d->d_ws, d->workspace_bytes(1)), "cudaMalloc(workspace)");
+    cuda_check(cudaMemset(d->d_ws, 0, d->workspace_bytes(1)), "cudaMemset(workspace)");
     *out = d.release();
     PFT_API_END
 }
@@ -978,7 +1019,7 @@ pft_status pft_dplan_tail_kind(pft_dplan_t d, int* kind) {
     PFT_API_BEGIN
     const pft_dplan_s* x = dp(d);
     PFT_REQUIRE(kind != nullptr, "kind is null");
-    *kind = x->sum_tail ? 1 : x->k2_tail ? 2 : x->fused(1) ? 3 : 0;
+    *kind = x->sum_tail ? 1 : x->k2_tail ? 2 : x->fused(1) ? 3 : x->k2_workers ? 4 : 0;
     PFT_API_END
 }
 

@@ -53,12 +53,38 @@ def test_c2c_full_size_plan(pft, oracle):
     N, mu, a = sparse_c2(pft, 2 ** 14)
     plan = pft.build_plan(N, 2 ** 14, mu, 2 ** 15, 1e-12)
     d = pft.DevicePlan(plan)
-    assert plan.r == 14 and d.tail_kind() in ("K2 grid", "K2 tail")
+    assert plan.r == 14 and (d.P1, d.P2) == (128, 256) and d.tail_kind().startswith("K2 workers")
     x = torch.from_numpy(a).cuda()
     out = torch.empty(plan.M * 2 + 1, dtype=torch.complex128, device="cuda")
-    d.execute_ptr(x.data_ptr(), out.data_ptr())
+    d.execute_ptr(x.data_ptr(), out.data_ptr())  # isolated: K1 + K2 grid
     torch.cuda.synchronize()
-    assert rel_l2(out.cpu().numpy(), oracle.execute(plan, a)) <= GATE
+    ref = oracle.execute(plan, a)
+    assert rel_l2(out.cpu().numpy(), ref) <= GATE
+    # the benchmarked form: a chain with PFT_EXEC_OVERLAP_PREVIOUS (K2 workers inside K1's grid),
+    # distinct inputs and outputs in one CUDA graph, then an isolated execute on the same workspace
+    K = 4
+    xs = [a] + [pft.generate_signal(pft.KIND_UNIFORM, 900 + i, N) for i in range(1, K)]
+    dx = [x] + [torch.from_numpy(v).cuda() for v in xs[1:]]
+    outs = [torch.full((plan.M * 2 + 1,), np.nan, dtype=torch.complex128, device="cuda") for _ in range(K)]
+    ws = torch.zeros(-(-d.workspace_bytes(1) // 16), dtype=torch.complex128, device="cuda")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for i in range(K):
+                d.execute_ptr(dx[i].data_ptr(), outs[i].data_ptr(), d_ws=ws.data_ptr(), stream=st.cuda_stream,
+                              overlap=True)
+        for _ in range(3):
+            g.replay()
+        out.fill_(np.nan)
+        d.execute_ptr(dx[1].data_ptr(), out.data_ptr(), d_ws=ws.data_ptr(), stream=st.cuda_stream)
+        g.replay()
+    torch.cuda.synchronize()
+    refs = [ref] + [oracle.execute(plan, v) for v in xs[1:]]
+    for i in range(K):
+        assert rel_l2(outs[i].cpu().numpy(), refs[i]) <= GATE, i
+    assert rel_l2(out.cpu().numpy(), refs[1]) <= GATE
+    assert d.status(d_ws=ws.data_ptr()) == 0
 
 
 def test_c4_autotuned_plan(pft, oracle):
@@ -123,6 +149,14 @@ def test_c5_full_size_plan(pft, oracle):
     (2 ** 22, 2 ** 8, 2 ** 20, 2 ** 12, {}),                                        # sum tail (C2b-like)
     (2 ** 22, 2 ** 12, 2 ** 20, 2 ** 14, dict(second_pass="k2-fft", k2_at="grid")),  # K1 + K2 grid (C2c-like)
     (2 ** 22, 2 ** 9, -5, 2 ** 15, dict(second_pass="k2-fft", k2_at="tail")),       # K2 tail (C5-like)
+    # K2 worker CTAs inside K1's grid (the chained C2c form): default count, few workers (many m1
+    # rounds each), more than the free slots (capped), an odd r (column groups 6 + 5), mu = 0
+    (2 ** 22, 2 ** 12, 2 ** 20, 2 ** 14, dict(second_pass="k2-fft", k2_at="tail")),
+    (2 ** 22, 2 ** 12, 2 ** 20, 2 ** 14, dict(second_pass="k2-fft", k2_at="tail", tail_ctas=3)),
+    (2 ** 22, 2 ** 12, 2 ** 20, 2 ** 14, dict(second_pass="k2-fft", k2_at="tail", tail_ctas=200)),
+    (2 ** 22, 3000, 0, 2 ** 14, dict(second_pass="k2-fft", k2_at="tail", p2=128)),
+    # the ring K2 kernel on a narrow grid (opt-in, k2_grid_ctas)
+    (2 ** 22, 2 ** 12, 2 ** 20, 2 ** 14, dict(second_pass="k2-fft", k2_grid_ctas=12)),
 ])
 def test_overlap_chain_distinct_inputs_in_one_graph(pft, oracle, N, M, mu, p, kw):
     """K executes of distinct inputs into distinct outputs with PFT_EXEC_OVERLAP_PREVIOUS,
@@ -132,6 +166,8 @@ def test_overlap_chain_distinct_inputs_in_one_graph(pft, oracle, N, M, mu, p, kw
     K = 6
     plan = pft.build_plan(N, M, mu, p, 1e-12)
     d = pft.DevicePlan(plan, **kw)
+    if kw.get("k2_at") == "tail" and 8 <= plan.r <= 18:
+        assert d.tail_kind().startswith("K2 workers"), (plan.r, d.P1, d.P2, d.tail_kind())
     xs = [pft.generate_signal(pft.KIND_UNIFORM, 500 + i, N) for i in range(K)]
     dx = [torch.from_numpy(x).cuda() for x in xs]
     outs = [torch.full((2 * M + 1,), np.nan, dtype=torch.complex128, device="cuda") for _ in range(K)]

@@ -69,6 +69,7 @@ def run(cfg: str, p: int, opts: dict, reps: int, check: bool) -> dict:
         e1.record(st)
     torch.cuda.synchronize()
     chained = e0.elapsed_time(e1) / reps * 1e3
+    out_chained = out[:W * min(B, 4)].clone()  # the chain's last execute (input bufs[(reps - 1) % nbuf])
     with torch.cuda.stream(st):  # serialized executes (no overlap flag): device time per execute
         g2 = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g2, stream=st):
@@ -92,6 +93,10 @@ def run(cfg: str, p: int, opts: dict, reps: int, check: bool) -> dict:
         torch.cuda.synchronize()
         nb = min(B, 4)
         got = out[:W * nb].cpu().numpy().reshape(nb, W)
+        src_c = bufs[(reps - 1) % nbuf]
+        got_c = out_chained.cpu().numpy().reshape(min(B, 4), W)
+        res["rel_l2_chained"] = max(float(np.linalg.norm(got_c[b] - (r := oracle.execute(plan, src_c[b * N:(b + 1) * N].cpu().numpy())))
+                                          / np.linalg.norm(r)) for b in range(min(B, 4)))
         res["rel_l2"] = max(float(np.linalg.norm(got[b] - (r := oracle.execute(plan, src[b * N:(b + 1) * N].cpu().numpy())))
                                   / np.linalg.norm(r)) for b in range(nb))
     res["status"] = d.status(d_ws=ws.data_ptr())
