@@ -263,6 +263,8 @@ def run_ours(args):
                        k2_at=args.k2_at, tail_ctas=args.tail_ctas, k2_grid_ctas=args.k2_grid_ctas)
     overlap = not args.no_pdl  # independent inputs: PFT_EXEC_OVERLAP_PREVIOUS is the caller's promise
     launches = d.launches_per_execute()
+    if overlap and B == 1 and d.tail_kind().startswith("K2 workers"):
+        launches = 1  # chained single executes: the K2 work rides in K1's grid (one kernel per execute)
 
     stream = torch.cuda.Stream(device=dev)
     sp = stream.cuda_stream
@@ -378,7 +380,10 @@ def run_ours(args):
         import numpy as np
         import oracle
         src = bufs[(args.steps - 1) % nbuf]
-        d.execute_ptr(src.data_ptr(), out.data_ptr(), batch=B, in_stride=N, d_ws=ws[0].data_ptr(), stream=sp)
+        # in the timed chain's form: two chained executes (the overlap flag as timed), the last on src
+        for x in (bufs[(args.steps - 2) % nbuf], src):
+            d.execute_ptr(x.data_ptr(), out.data_ptr(), batch=B, in_stride=N, d_ws=ws[0].data_ptr(), stream=sp,
+                          overlap=overlap)
         torch.cuda.synchronize(dev)
         nb = min(B, 64)
         got = out[:W * nb].cpu().numpy().reshape(nb, W)
@@ -389,7 +394,8 @@ def run_ours(args):
             worst = max(worst, float(np.linalg.norm(got[b] - ref) / np.linalg.norm(ref)))
         parity = {"rel_l2_vs_oracle": worst, "gate": 1e-11, "pass": worst <= 1e-11,
                   "signals_checked": nb, "oracle_seconds": time.perf_counter() - t0,
-                  "what": "last timed input, same plan (p, r, P1, P2, tail), CPU oracle oracle/oracle.cpp"}
+                  "what": "last timed input, same plan (p, r, P1, P2, tail) and execute form as the timed "
+                          "chain, CPU oracle oracle/oracle.cpp"}
         if worst > 1e-11:
             log(f"PARITY FAILURE: rel_l2 {worst:.3e} > 1e-11")
 
@@ -455,7 +461,10 @@ def run_ours(args):
                        "streams": args.streams, "overlap_previous": overlap,
                        "tail": {"sum tail": "sum tail in K1 (one kernel per execute)",
                                 "K2 tail": "K2 work by K1's last-arriving CTAs (one kernel per execute)",
-                                "fused K2": "K2 in K1 behind a grid barrier (one kernel per execute)"}.get(
+                                "fused K2": "K2 in K1 behind a grid barrier (one kernel per execute)",
+                                "K2 workers in K1 (chained) / K2 grid":
+                                    ("K2 worker CTAs inside K1's grid (one kernel per execute)" if overlap else
+                                     "K1 + K2 grid (2 kernels per execute)")}.get(
                                     d.tail_kind(), f"K2 ({launches} kernels per execute)"),
                        "pipelining": "independent transforms alternate over 2 streams with separate "
                                      "workspaces" if args.streams == 2 else

@@ -661,7 +661,7 @@ __device__ __forceinline__ void k2_ring_stage(const double2* __restrict__ src, d
 // slots), release the next launch at once, and wait for the slab counter to reach P2 (each
 // streamer bumps it after its slab store).  Then worker w runs K2 for m1 = w, w + workers, ...
 // as a bulk-copy ring: the slab is stored in two column groups per m1 ([m1][group][c][j'],
-// K1Params.slab_split) so a group (P2 x ceil(R/2) complex128) is one contiguous cp.async.bulk,
+// already multiplied by the four-step twiddles omega_p^{m1 c}) so a group (P2 x ceil(R/2) complex128) is one contiguous cp.async.bulk,
 // issued by the CTA's ninth warp (K1's producer/consumer pattern: full/empty mbarriers) into one of
 // two load buffers while the eight consumer warps work on the other; the length-P2 stages (radix
 // 8/4/2: the CTA keeps K1's register budget) ping-pong between the load buffer and a scratch
@@ -682,8 +682,7 @@ __device__ __forceinline__ void k1_k2_worker(const K1Params& P, uint32_t w, uint
     const uint32_t n = P.P2, cap = n * (uint32_t)G0;
     double2* bufs = reinterpret_cast<double2*>(smem);     // [3][cap]: load buffers 0 and 1, FFT scratch 2
     double2* tw2 = bufs + 3 * (size_t)cap;                // omega_P2^t
-    double2* pre = tw2 + n;                               // omega_p^{m1 c}
-    uint64_t* full = reinterpret_cast<uint64_t*>(pre + n);  // [2] slab group landed
+    uint64_t* full = reinterpret_cast<uint64_t*>(tw2 + n);  // [2] slab group landed
     uint64_t* empty = full + 2;                              // [2] load buffer consumed
     unsigned* ctl = P.arrivals + (size_t)b * P.ctl_stride;  // {slabs stored, workers done}
     PFT_BOUND((size_t)b * P.ctl_stride + 1, P.ctl_words);
@@ -698,11 +697,8 @@ __device__ __forceinline__ void k1_k2_worker(const K1Params& P, uint32_t w, uint
         }
         fence_barrier_init();
     }
-    if (tid < NT) {
+    if (tid < NT && nk > 0)
         for (uint32_t c = tid; c < n; c += NT) tw2[c] = __ldg(P.omega + (size_t)c * P.P1);
-        if (nk > 0)
-            for (uint32_t c = tid; c < n; c += NT) pre[c] = __ldg(P.omega + (size_t)w * c);
-    }
     // the previous grid (the workers of the previous transform re-arm this signal's counters as
     // they finish, and read the slab this transform's streamers rewrite) must be complete first
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -753,18 +749,9 @@ __device__ __forceinline__ void k1_k2_worker(const K1Params& P, uint32_t w, uint
             acc[o] = make_double2(0.0, 0.0);
             tp[o] = 0.0;
         }
-        constexpr int PRE_PER = 2;  // host: P2 <= 512 = PRE_PER * NT
-        double2 pre_next[PRE_PER];
         for (uint32_t q = 0; q < nq; ++q) {
             const uint32_t m1 = w + (q / NG) * NW, g = q % NG, lb = q & 1u;
             const uint64_t s0 = (uint64_t)((m1 + P.P1 - Q.first_mod_p1) % P.P1);
-            if (g == NG - 1 && q + 1 < nq) {  // the next m1's four-step twiddles, stored after the stages
-#pragma unroll
-                for (int i = 0; i < PRE_PER; ++i) {
-                    const uint32_t c = tid + i * NT;
-                    if (c < n) pre_next[i] = __ldg(P.omega + (size_t)(m1 + NW) * c);  // (m1 + NW) c < p
-                }
-            }
             {
                 uint32_t spins = 0;
                 while (!mbar_try_wait(&full[lb], (q >> 1) & 1u))
@@ -778,7 +765,7 @@ __device__ __forceinline__ void k1_k2_worker(const K1Params& P, uint32_t w, uint
             int Ns = 1, lg_ns = 0;
             while (lg_ns < lg_n) {
                 const int lgr = lg_n - lg_ns >= 3 ? 3 : lg_n - lg_ns, RAD = 1 << lgr;
-                const double2* pr = (lg_ns == 0 && m1 != 0) ? pre : nullptr;
+                const double2* pr = nullptr;  // the streamers stored the slab with its four-step twiddles
                 if (g == 0) {
                     if (RAD == 8) k2_ring_stage<8, G0>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, NT);
                     else if (RAD == 4) k2_ring_stage<4, G0>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, NT);
@@ -794,13 +781,6 @@ __device__ __forceinline__ void k1_k2_worker(const K1Params& P, uint32_t w, uint
                 double2* t = src;
                 src = dst;
                 dst = t;
-            }
-            if (g == NG - 1 && q + 1 < nq) {  // pre[] was last read in this m1's last first stage
-#pragma unroll
-                for (int i = 0; i < PRE_PER; ++i) {
-                    const uint32_t c = tid + i * NT;
-                    if (c < n) pre[c] = pre_next[i];
-                }
             }
             const int gw = g ? G1 : G0, j0 = g ? G0 : 0;
 #pragma unroll
@@ -838,7 +818,7 @@ __device__ __forceinline__ void k1_k2_worker(const K1Params& P, uint32_t w, uint
             }
             // this step's reads and writes of the load buffer precede its asynchronous refill
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            team_sync();  // also: the scratch and pre[] are free for the next step
+            team_sync();  // also: the scratch is free for the next step
             if (tid == 0) mbar_arrive(&empty[lb]);
         }
     }
@@ -892,6 +872,9 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     const uint32_t c = blockIdx.x / split;  // residue class k = c (mod P2)
     const uint32_t b = blockIdx.y;          // signal
     double2 tail_tw = make_double2(0.0, 0.0);
+    if constexpr (TK == 2) {  // K2 workers: the four-step twiddle omega_p^{m1 c} of this class, applied at the slab store
+        if (P.workers && (uint32_t)tid < P.P1) tail_tw = __ldg(P.omega + (size_t)tid * (blockIdx.x / (P.split > 1 ? P.split : 1)));
+    }
     if (P.sum_tail && (uint32_t)tid < P.P1 + P.P2) {
         const uint32_t t = tid;
         tail_tw = __ldg(P.omega + (t < P.P1 ? (size_t)t * c : (size_t)(t - P.P1) * P.P1));
@@ -1070,13 +1053,17 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     if constexpr (TK == 2) {
         if (P.workers) {
             // two column groups per m1, each contiguous over (c, j') for the workers' bulk copies
+            // and already carrying the four-step twiddle omega_p^{m1 c} (host: P1 <= K1_THREADS)
             constexpr uint32_t G0 = (R + 1) / 2, G1 = R - G0;
+            if ((uint32_t)tid < P.P1) tw1[tid] = tail_tw;  // the first pass no longer needs omega_P1
+            __syncthreads();
             for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) {
                 const uint32_t m1 = idx / R, j = idx - m1 * R;
                 const size_t at = (size_t)m1 * P.P2 * R +
                                   (j < G0 ? (size_t)c * G0 + j : (size_t)P.P2 * G0 + (size_t)c * G1 + (j - G0));
                 PFT_BOUND((size_t)b * P.y_stride + at, P.y_elems);
-                Y[at] = res[(size_t)j * P.P1 + m1];
+                const double2 v = res[(size_t)j * P.P1 + m1];
+                Y[at] = (m1 == 0 || c == 0) ? v : cmul(v, tw1[m1]);
             }
             __syncthreads();  // the CTA's slab stores precede thread 0's fence and count
             if (tid == 0) {

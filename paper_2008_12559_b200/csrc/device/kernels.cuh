@@ -236,10 +236,10 @@ inline size_t k1_sum_scratch_bytes(uint32_t P1, uint32_t P2) {
 __host__ __device__ constexpr bool k1_k2_tail_instantiated(int r) { return r >= 4 && r <= 7; }
 // r values with a K2-worker K1 instantiation (many-bin single transforms: C2c has r = 14)
 __host__ __device__ constexpr bool k1_k2_workers_instantiated(int r) { return r >= 8 && r <= 18; }
-// K2 workers: three buffers of one column group (P2 x ceil(r/2)) + omega_P2 + four-step twiddles +
-// 3 mbarriers (+ alignment slack); must fit K1's shared memory
+// K2 workers: three buffers of one column group (P2 x ceil(r/2)) + omega_P2 + 4 mbarriers
+// (+ alignment slack); must fit K1's shared memory
 inline size_t k1_k2_worker_bytes(int r, uint32_t P2) {
-    return sizeof(double2) * (3 * (size_t)((r + 1) / 2) * P2 + 2 * (size_t)P2) + 4 * sizeof(uint64_t) + 128;
+    return sizeof(double2) * (3 * (size_t)((r + 1) / 2) * P2 + (size_t)P2) + 4 * sizeof(uint64_t) + 128;
 }
 // K1's last-arrival K2 tail: Z + scratch for `group` columns, omega_P2 + four-step twiddles,
 // ticket word

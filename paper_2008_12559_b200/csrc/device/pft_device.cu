@@ -939,9 +939,16 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         const uint64_t free_slots = d->k1_capacity > d->P2 ? d->k1_capacity - d->P2 : 0;
         if (eligible && d->k2_ctas == 0 && k2_at != PFT_K2_AT_GRID && pftdev::k1_k2_workers_instantiated(H.r) &&
             pftdev::k1_k2_worker_bytes(H.r, (uint32_t)d->P2) <= pftdev::k1_smem_bytes(H.r, (uint32_t)d->P1, d->k1_stages) &&
-            (d->W + d->P1 - 1) / d->P1 <= 2ull * 32 * pftdev::K1_CONSUMER_WARPS && d->P2 <= 512 && free_slots >= 8) {
+            (d->W + d->P1 - 1) / d->P1 <= 2ull * 32 * pftdev::K1_CONSUMER_WARPS && d->P1 <= (uint64_t)pftdev::K1_THREADS &&
+            free_slots >= 8) {
+            // the fewest workers that keep the fewest m1 rounds: every slot not held by a worker
+            // lets a streamer of the next transform start early and stream through the gap in
+            // which this transform's streamers run their FFT pass and store the slab (C2c: 32
+            // workers 55.9 us, 40 workers 56.8 us, workers that exit at once 48.5 us)
             uint64_t nw = std::min<uint64_t>(free_slots, d->P1);
-            if (tail_ctas > 0) nw = std::min<uint64_t>(nw, (uint64_t)tail_ctas);
+            const uint64_t min_rounds = (d->P1 + nw - 1) / nw;
+            nw = (d->P1 + min_rounds - 1) / min_rounds;
+            if (tail_ctas > 0) nw = std::min<uint64_t>(std::min<uint64_t>(free_slots, d->P1), (uint64_t)tail_ctas);
             const double rounds = (double)((d->P1 + nw - 1) / nw);
             const double stream_us = 16.0 * (double)H.N / 6.5e6;
             if (k2_at == PFT_K2_AT_TAIL || rounds * 8.0 <= stream_us) d->k2_workers = (uint32_t)nw;
