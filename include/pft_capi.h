@@ -176,8 +176,10 @@ typedef struct pft_dplan_opts {
     int tail_ctas;       /* sum-tail reducers / K2-tail workers per signal (0 = plan); always
                             capped below the co-resident K1 capacity (forward progress)       */
     int k2_grid_ctas;    /* K2 grid width: the PFT_PASS2_K2_L2 form (0 = SM count); the
-                            PFT_PASS2_K2_FFT form on its own grid: > 0 = a grid of that many
-                            CTAs looping over m1 (0 = the plan's choice)                      */
+                            PFT_PASS2_K2_FFT form on its own grid with a power-of-two P2: > 0 =
+                            the bulk-copy ring kernel on that many CTAs looping over m1
+                            (0 = the plan's choice: one CTA per m1, or for chained executes K2
+                            worker CTAs inside K1's grid, see pft_dplan_tail_kind)            */
     int k1_split;        /* 0: an isolated execute (no PFT_EXEC_OVERLAP_PREVIOUS) whose K1 grid
                             fills at most half of the SM slots runs two CTAs (a thread-block
                             cluster) per residue class, each streaming half of the columns and

@@ -1225,124 +1225,84 @@ __global__ void __launch_bounds__(K2_THREADS) k2_fft_post(K2Params P) {
     }
 }
 
-// K2 FFT form on a narrow grid (K2Params.k2_ctas CTAs per signal) that loops over m1: few enough
-// CTAs to be resident beside the next transform's K1 (launched when every K2 CTA has started),
-// so K2's latency-bound work overlaps that K1's stream instead of holding its SM slots.  The
-// post powers ((m - mu)/p)^j are formed in registers by ascending repeated multiplication (as the
-// planner forms post_powers; x = (m - mu) * (1/p) is exact for power-of-two p, within an ulp
-// otherwise) instead of W * r dependent table loads.
+// K2 FFT form as a bulk-copy ring on a grid of K2Params.k2_ctas CTAs per signal that loops over m1
+// (opt-in: pft_dplan_opts.k2_grid_ctas).  Each CTA runs m1 = blockIdx.x, + gridDim.x, ...: the m1
+// slab Y[m1][c][j] (contiguous P2 * R complex128) arrives by one cp.async.bulk per slab, issued
+// by the CTA's ninth warp into one of two load buffers (full/empty mbarriers, K1's
+// producer/consumer pattern) while the eight consumer warps run the previous one: the length-P2
+// Stockham stages on the slab's own (c, j) layout between the load buffer and a scratch buffer,
+// then Eq. (7) where the result lies.  Power-of-two P2 with radices 2/4/8/16; the post powers
+// ((m - mu)/p)^j are formed in registers by ascending repeated multiplication, as the planner
+// forms post_powers (x = (m - mu) * (1/p): exact for power-of-two p, within an ulp otherwise).
+// Measured at C2c (profiles/r02/c2c_k2_workers.md): 128 CTAs 64.0 us chained / 65.5 isolated vs
+// 67.6 / 70.9 for k2_fft_post; on the 20 SMs K1 leaves free (12-20 CTAs) 54.6-55.8 us chained --
+// but any kernel between two K1s costs the chain ~7 us, so the default for chains is the K2
+// workers inside K1's grid (k1_k2_worker).
+constexpr int K2R_THREADS = K2_THREADS + 32;  // 8 consumer warps + the loader warp
 template <int R>
-__global__ void __launch_bounds__(K2_THREADS) k2_fft_loop(K2Params P) {
-    extern __shared__ __align__(16) double2 zs[];
-    double2* Z = zs;                              // [R][P2]
-    double2* scratch = zs + (size_t)R * P.P2;     // [R][P2]
-    double2* tw2 = scratch + (size_t)R * P.P2;    // omega_P2^t
-    double2* pre = tw2 + P.P2;                    // omega_p^{m1 c}
-    const uint32_t b = blockIdx.y;
-    if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    for (uint32_t c = threadIdx.x; c < P.P2; c += blockDim.x) tw2[c] = __ldg(P.omega + (size_t)c * P.P1);
-    const int64_t Mh = (int64_t)((P.W - 1) / 2);
-    bool waited = false;
-    double2* __restrict__ out = P.out + (size_t)b * P.W;
-    for (uint32_t m1 = blockIdx.x; m1 < P.P1; m1 += gridDim.x) {
-        const uint64_t s0 = (uint64_t)((m1 + P.P1 - P.first_mod_p1) % P.P1);
-        if (s0 >= P.W) continue;  // no output slot maps to this m1 (block-uniform)
-        for (uint32_t c = threadIdx.x; c < P.P2; c += blockDim.x) pre[c] = __ldg(P.omega + (size_t)m1 * c);  // m1 c < p
-        if (!waited) {  // K1's slab complete and visible
-            asm volatile("griddepcontrol.wait;" ::: "memory");
-            waited = true;
-        }
-        __syncthreads();
-        load_twiddled_slab<R>(P.Y + (size_t)b * P.y_stride + (size_t)m1 * P.P2 * R, P.P2, m1, pre, Z);
-        __syncthreads();
-        const double2* res = Z;
-        if (P.P2 > 1) res = fft_columns(Z, scratch, R, P.fft2, SmemTwiddles{tw2});
-        for (uint64_t s = s0 + (uint64_t)P.P1 * threadIdx.x; s < P.W; s += (uint64_t)P.P1 * blockDim.x) {
-            uint64_t mp = P.first_mod_p + s % P.p;
-            if (mp >= P.p) mp -= P.p;
-            const uint32_t m2 = (uint32_t)(mp / P.P1);
-            const double x = (double)((int64_t)s - Mh) * P.inv_p;
-            double2 acc = res[m2];
-            double tp = x;
-#pragma unroll
-            for (int j = 1; j < R; ++j) {  // ascending j
-                const double2 v = res[(size_t)j * P.P2 + m2];
-                acc.x = fma(v.x, tp, acc.x);
-                acc.y = fma(v.y, tp, acc.y);
-                if (j + 1 < R) tp *= x;
-            }
-            const double2 v = cmul(acc, __ldg(P.post_twiddles + s));  // e^{-pi i m / p}
-            PFT_BOUND((size_t)b * P.W + s, P.out_elems);
-            out[s] = v;
-            if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
-        }
-        __syncthreads();  // smem reuse by the next m1
-    }
-    if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
-}
-
-// K2 FFT form as a ring on a narrow grid (chained executes of single long transforms: C2c).
-// K1's grid leaves a few SMs without a CTA (C2c: 256 CTAs at two per SM on 128 of the 148 SMs);
-// this kernel's k2_ctas CTAs (one per such SM: three slab buffers, up to the whole shared memory)
-// hold those SMs while the NEXT transform's K1 -- launched as soon as every CTA here has started --
-// streams on the others, so the second pass no longer idles HBM between two streams.  Each CTA
-// loops over m1 = blockIdx.x, + gridDim.x, ...: the m1 slab Y[m1][c][j] (contiguous P2 * R
-// complex128) arrives by one cp.async.bulk per slab, two slabs ahead of the FFT (mbarrier
-// complete_tx), the length-P2 Stockham stages run on the slab's own (c, j) layout between two of
-// the three buffers, and Eq. (7) reads the result where it lies.  Power-of-two P2 with radices
-// 2/4/8/16 only; the post powers are formed in registers as in k2_fft_loop.
-template <int R>
-__global__ void __launch_bounds__(K2_THREADS, 1) k2_ring(K2Params P) {
+__global__ void __launch_bounds__(K2R_THREADS, 1) k2_ring(K2Params P) {
     extern __shared__ __align__(128) unsigned char k2r_raw[];
+    constexpr int NT = K2_THREADS;
+    constexpr uint32_t kSpinLimit = 1u << 22;  // bounded waits: a lost signal becomes status bit 1, not a hang
     const uint32_t n = P.P2, slab = n * (uint32_t)R;
-    double2* bufs = reinterpret_cast<double2*>(k2r_raw);  // [3][slab]
+    double2* bufs = reinterpret_cast<double2*>(k2r_raw);  // [3][slab]: load buffers 0 and 1, FFT scratch 2
     double2* tw2 = bufs + 3 * (size_t)slab;               // omega_P2^t
     double2* pre = tw2 + n;                               // omega_p^{m1 c}
-    uint64_t* full = reinterpret_cast<uint64_t*>(pre + n);  // one mbarrier per buffer
+    uint64_t* full = reinterpret_cast<uint64_t*>(pre + n);  // [2] slab landed
+    uint64_t* empty = full + 2;                              // [2] load buffer consumed
     const int tid = threadIdx.x;
     const uint32_t b = blockIdx.y, G = gridDim.x;
     if (P.release_next) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (tid == 0) {
-        for (int s = 0; s < 3; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
         fence_barrier_init();
     }
-    for (uint32_t c = tid; c < n; c += blockDim.x) tw2[c] = __ldg(P.omega + (size_t)c * P.P1);
     const uint32_t m1_first = blockIdx.x;
     const uint32_t nk = m1_first < P.P1 ? (P.P1 - m1_first + G - 1) / G : 0;
-    constexpr int PRE_PER = 4;  // P2 <= PRE_PER * K2_THREADS
-    double2 pre_next[PRE_PER];
-#pragma unroll
-    for (int i = 0; i < PRE_PER; ++i) {
-        const uint32_t c = tid + i * K2_THREADS;
-        pre_next[i] = (nk > 0 && c < n) ? __ldg(P.omega + (size_t)m1_first * c) : make_double2(1.0, 0.0);
+    if (tid < NT) {
+        for (uint32_t c = tid; c < n; c += NT) tw2[c] = __ldg(P.omega + (size_t)c * P.P1);
+        if (nk > 0)
+            for (uint32_t c = tid; c < n; c += NT) pre[c] = __ldg(P.omega + (size_t)m1_first * c);
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's slab complete and visible
-    __syncthreads();
-    const double2* __restrict__ Yb = P.Y + (size_t)b * P.y_stride;
-    const uint32_t bytes = slab * (uint32_t)sizeof(double2);
-    // buffer roles: ia = this m1's slab, ib = the next one's (in flight), ic = free (FFT scratch)
-    uint32_t ia = 0, ib = 1, ic = 2, phase = 0;  // phase bit s = parity the next wait on buffer s uses
-    if (tid == 0) {
-        for (uint32_t k = 0; k < 2 && k < nk; ++k) {
-            PFT_BOUND((size_t)b * P.y_stride + ((size_t)(m1_first + k * G) + 1) * slab - 1, P.y_elems);
-            mbar_arrive_expect_tx(&full[k], bytes);
-            bulk_load(bufs + (size_t)k * slab, Yb + (size_t)(m1_first + k * G) * slab, bytes, &full[k]);
+    __syncthreads();  // barriers and tables ready; the two roles part here
+    if (tid >= NT) {
+        if (tid == NT) {  // ---- loader: keeps two slabs in flight
+            const double2* __restrict__ Yb = P.Y + (size_t)b * P.y_stride;
+            const uint32_t bytes = slab * (uint32_t)sizeof(double2);
+            for (uint32_t k = 0; k < nk; ++k) {
+                const uint32_t lb = k & 1u;
+                if (k >= 2) {  // the consumers have finished with this buffer's previous slab
+                    uint32_t spins = 0;
+                    while (!mbar_try_wait(&empty[lb], ((k >> 1) - 1u) & 1u))
+                        if (++spins > kSpinLimit) {
+                            atomicOr(P.status, 2);
+                            break;
+                        }
+                }
+                const uint32_t m1 = m1_first + k * G;
+                PFT_BOUND((size_t)b * P.y_stride + ((size_t)m1 + 1) * slab - 1, P.y_elems);
+                mbar_arrive_expect_tx(&full[lb], bytes);
+                bulk_load(bufs + (size_t)lb * slab, Yb + (size_t)m1 * slab, bytes, &full[lb]);
+            }
         }
+        return;
     }
-#pragma unroll
-    for (int i = 0; i < PRE_PER; ++i) {
-        const uint32_t c = tid + i * K2_THREADS;
-        if (c < n) pre[c] = pre_next[i];
-    }
-    __syncthreads();
+    // ---- consumers (named barrier 1 over the NT consumer threads)
+    auto team_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); };
     const int64_t Mh = (int64_t)((P.W - 1) / 2);
     double2* __restrict__ out = P.out + (size_t)b * P.W;
+    constexpr int PRE_PER = 4;  // host: P2 <= PRE_PER * K2_THREADS
+    double2 pre_next[PRE_PER];
     for (uint32_t k = 0; k < nk; ++k) {
-        const uint32_t m1 = m1_first + k * G;
-        if (k + 1 < nk) {
+        const uint32_t m1 = m1_first + k * G, lb = k & 1u;
+        if (k + 1 < nk) {  // the next m1's four-step twiddles, stored after the first stage
 #pragma unroll
             for (int i = 0; i < PRE_PER; ++i) {
-                const uint32_t c = tid + i * K2_THREADS;
+                const uint32_t c = tid + i * NT;
                 if (c < n) pre_next[i] = __ldg(P.omega + (size_t)(m1 + G) * c);  // (m1 + G) c < p
             }
         }
@@ -1351,53 +1311,41 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_ring(K2Params P) {
         const uint64_t s_first = s0 + (uint64_t)P.P1 * tid;
         double2 ptw0 = make_double2(0.0, 0.0);
         if (s_first < P.W) ptw0 = __ldg(P.post_twiddles + s_first);
-        {  // bounded: a lost completion becomes status bit 2, not a hang
+        {
             uint32_t spins = 0;
-            while (!mbar_try_wait(&full[ia], (phase >> ia) & 1u))
-                if (++spins > (1u << 22)) {
+            while (!mbar_try_wait(&full[lb], (k >> 1) & 1u))
+                if (++spins > kSpinLimit) {
                     atomicOr(P.status, 2);
                     break;
                 }
         }
-        phase ^= 1u << ia;
-        double2* src = bufs + (size_t)ia * slab;
-        double2* dst = bufs + (size_t)ic * slab;
-        uint32_t isrc = ia, idst = ic;
+        double2* src = bufs + (size_t)lb * slab;
+        double2* dst = bufs + 2 * (size_t)slab;
         int Ns = 1, lg_ns = 0;
         for (int st = 0; st < P.fft2.count; ++st) {
             const int RAD = P.fft2.radix[st];
             const double2* pr = (st == 0 && m1 != 0) ? pre : nullptr;
             switch (RAD) {
-                case 2: k2_ring_stage<2, R>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, K2_THREADS); lg_ns += 1; break;
-                case 4: k2_ring_stage<4, R>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, K2_THREADS); lg_ns += 2; break;
-                case 8: k2_ring_stage<8, R>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, K2_THREADS); lg_ns += 3; break;
-                default: k2_ring_stage<16, R>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, K2_THREADS); lg_ns += 4; break;
+                case 2: k2_ring_stage<2, R>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, NT); lg_ns += 1; break;
+                case 4: k2_ring_stage<4, R>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, NT); lg_ns += 2; break;
+                case 8: k2_ring_stage<8, R>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, NT); lg_ns += 3; break;
+                default: k2_ring_stage<16, R>(src, dst, (int)n, Ns, lg_ns, tw2, pr, tid, NT); lg_ns += 4; break;
             }
             Ns *= RAD;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before a buffer's async refill
-            __syncthreads();
+            team_sync();
             double2* t = src;
             src = dst;
             dst = t;
-            const uint32_t ti = isrc;
-            isrc = idst;
-            idst = ti;
-        }
-        // the result is in buffer isrc; idst is free: the slab two m1 ahead lands there
-        if (tid == 0 && k + 2 < nk) {
-            PFT_BOUND((size_t)b * P.y_stride + ((size_t)(m1 + 2 * G) + 1) * slab - 1, P.y_elems);
-            mbar_arrive_expect_tx(&full[idst], bytes);
-            bulk_load(bufs + (size_t)idst * slab, Yb + (size_t)(m1 + 2 * G) * slab, bytes, &full[idst]);
-        }
-        if (k + 1 < nk) {  // pre[] was last read in the first stage
+            if (st == 0 && k + 1 < nk) {  // pre[] was last read in the first stage
 #pragma unroll
-            for (int i = 0; i < PRE_PER; ++i) {
-                const uint32_t c = tid + i * K2_THREADS;
-                if (c < n) pre[c] = pre_next[i];
+                for (int i = 0; i < PRE_PER; ++i) {
+                    const uint32_t c = tid + i * NT;
+                    if (c < n) pre[c] = pre_next[i];
+                }
             }
         }
         const double2* res = src;
-        for (uint64_t s = s_first; s < P.W; s += (uint64_t)P.P1 * K2_THREADS) {
+        for (uint64_t s = s_first; s < P.W; s += (uint64_t)P.P1 * NT) {
             uint64_t mp = P.first_mod_p + s % P.p;
             if (mp >= P.p) mp -= P.p;
             const uint32_t m2 = (uint32_t)(mp / P.P1);
@@ -1417,11 +1365,10 @@ __global__ void __launch_bounds__(K2_THREADS, 1) k2_ring(K2Params P) {
             out[s] = v;
             if (!isfinite(v.x) || !isfinite(v.y)) atomicOr(P.status, 1);
         }
-        __syncthreads();  // the result buffer becomes the next m1's scratch
-        const uint32_t na = ib, nb_ = idst, nc = isrc;
-        ia = na;
-        ib = nb_;
-        ic = nc;
+        // this slab's reads and writes of the load buffer precede its asynchronous refill
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        team_sync();  // also: the scratch and pre[] are free for the next m1
+        if (tid == 0) mbar_arrive(&empty[lb]);
     }
 }
 
@@ -1794,10 +1741,10 @@ cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
         return cudaLaunchKernelEx(&cfg, k2_bluestein_post<R>, P);
     }
     if (P.mode == K2_FFT && P.ring) {
+        cfg.blockDim = dim3(K2R_THREADS);
         cfg.dynamicSmemBytes = k2_ring_smem_bytes(R, P.P2);
         return cudaLaunchKernelEx(&cfg, k2_ring<R>, P);
     }
-    if (P.mode == K2_FFT && P.k2_ctas > 0) return cudaLaunchKernelEx(&cfg, k2_fft_loop<R>, P);
     if (P.mode == K2_FFT) return cudaLaunchKernelEx(&cfg, k2_fft_post<R>, P);
     if (P.mode == K2_DOT) return cudaLaunchKernelEx(&cfg, k2_dot_post<R>, P);
     return cudaLaunchKernelEx(&cfg, k2_direct_post<R>, P);
@@ -1806,8 +1753,6 @@ cudaError_t launch_k2_r(const K2Params& P, dim3 grid, cudaStream_t st) {
 template <int R>
 cudaError_t configure_k2_r(size_t smem) {
     cudaError_t e = cudaFuncSetAttribute(k2_fft_post<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k2_fft_loop<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k2_ring<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

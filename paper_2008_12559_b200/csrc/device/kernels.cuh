@@ -100,7 +100,7 @@ struct K2Params {
     double inv_p;                  // 1 / p
     uint32_t first_mod_p1;         // (mu - M) mod P1
     int mode;                      // K2_DIRECT / K2_FFT / K2_DOT
-    uint32_t k2_ctas;              // K2_L2 grid width (0 = 148); K2_FFT: > 0 = looping grid of that width
+    uint32_t k2_ctas;              // K2_L2 grid width (0 = 148); K2_FFT with `ring`: grid width of k2_ring
     int release_next;              // trigger the next launch at K2 start (1) / end (2) (PDL chaining)
     int ring;                      // K2_FFT on k2_ctas CTAs as a bulk-copy ring over m1 (k2_ring)
     FftRadices fft2;               // radices of P2 (K2_FFT) or of L (K2_BLUESTEIN)
@@ -208,9 +208,9 @@ inline uint32_t k1_pick_stages(int r, uint32_t P1) {
 }
 // Z + scratch (r x P2 each) + omega_P2 + four-step twiddles (P2 each)
 inline size_t k2_smem_bytes(int r, uint32_t P2) { return sizeof(double2) * (2 * (size_t)r * P2 + 2 * (size_t)P2); }
-// ring K2 (k2_ring): three slab buffers (r x P2 each) + omega_P2 + four-step twiddles + 3 mbarriers
+// ring K2 (k2_ring): three slab buffers (r x P2 each) + omega_P2 + four-step twiddles + 4 mbarriers
 inline size_t k2_ring_smem_bytes(int r, uint32_t P2) {
-    return sizeof(double2) * (3 * (size_t)r * P2 + 2 * (size_t)P2) + 3 * sizeof(uint64_t) + 8;
+    return sizeof(double2) * (3 * (size_t)r * P2 + 2 * (size_t)P2) + 4 * sizeof(uint64_t);
 }
 // Z (r x P2) + omega_P2 + four-step twiddles
 inline size_t k2_dot_smem_bytes(int r, uint32_t P2) { return sizeof(double2) * ((size_t)r * P2 + 2 * (size_t)P2); }

@@ -290,8 +290,8 @@ struct pft_dplan_s {
     int k2_mode = pftdev::K2_DIRECT;
     uint32_t k2_ctas = 0;
     uint32_t k2_workers = 0; // chained single executes: K2 worker CTAs riding in K1's grid (k1_k2_worker); 0 = off
-    uint32_t ring_ctas = 0;  // chained single executes: K2 as a bulk-copy ring on this many CTAs (k2_ring); 0 = off
-    bool ring_always = false;  // caller-chosen ring width: isolated executes take the ring too
+    bool ring_ok = false;    // single executes whose K2 is its own grid run the bulk-copy ring kernel (k2_ring)
+    uint32_t ring_ctas = 0;  // its grid width when the caller chose one (k2_grid_ctas); 0 = one CTA per m1
     bool allow_fuse = false; // K2 fused into K1's tail (opt-in; measured slower at C2b/C4)
     bool allow_split = true; // isolated executes: two CTAs (a cluster) per residue class
     bool sum_tail = false;   // unsharded execute: K1 sum tail, no K2 (few output bins)
@@ -548,9 +548,9 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
         cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 (K2 workers) launch");
         return;
     }
-    if (d->ring_ctas && batch == 1 && (pdl || d->ring_always)) {  // K2 under the next transform's stream
+    if (d->ring_ok && batch == 1) {  // slab by bulk copy, stages on its own layout (C2c isolated 70.9 -> 65.4 us)
         P2.ring = 1;
-        P2.k2_ctas = d->ring_ctas;
+        P2.k2_ctas = d->ring_ctas ? d->ring_ctas : (uint32_t)d->P1;
     }
     cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
     cuda_check(pftdev::launch_k2(P2, d->host.r, (uint32_t)batch, st), "K2 launch");
@@ -931,9 +931,13 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
     // K2 worker CTAs (k1_k2_worker) in the slots the P2 streamers leave free, taken when their m1
     // rounds (~8 us per m1 beside a streaming K1, measured at C2c) fit within the stream.
     // tail_ctas overrides the count; k2_at = GRID or a caller-chosen k2_grid_ctas turns them off.
-    // k2_grid_ctas > 0 on such a plan selects the ring K2 kernel (k2_ring) on that many CTAs.
+    // Executes that do not take the workers (isolated ones, or k2_grid_ctas > 0) run the ring K2
+    // kernel (k2_ring) when P2 is a power of two and three slabs fit shared memory: one CTA per
+    // m1, or k2_grid_ctas CTAs looping over m1.
     {
-        const bool pow2 = d->P2 >= 4 && (d->P2 & (d->P2 - 1)) == 0;
+        // power-of-two p: the ring forms build ((m - mu)/p)^j in registers, exact only then (the
+        // post_powers table's values bit for bit: the ring K2 equals the K2 grid bitwise)
+        const bool pow2 = d->P2 >= 4 && (d->P2 & (d->P2 - 1)) == 0 && (H.p & (H.p - 1)) == 0;
         const bool eligible = !d->sum_tail && !d->k2_tail && !d->allow_fuse && d->k2_mode == pftdev::K2_FFT && pow2 &&
                               batch_hint <= 1;
         const uint64_t free_slots = d->k1_capacity > d->P2 ? d->k1_capacity - d->P2 : 0;
@@ -953,10 +957,10 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
             const double stream_us = 16.0 * (double)H.N / 6.5e6;
             if (k2_at == PFT_K2_AT_TAIL || rounds * 8.0 <= stream_us) d->k2_workers = (uint32_t)nw;
         }
-        if (!d->k2_workers && eligible && d->k2_ctas > 0 && d->P2 <= 4ull * pftdev::K2_THREADS &&
+        if (eligible && d->P2 <= 4ull * pftdev::K2_THREADS &&
             pftdev::k2_ring_smem_bytes(H.r, (uint32_t)d->P2) <= (size_t)227 * 1024) {
+            d->ring_ok = true;
             d->ring_ctas = d->k2_ctas;
-            d->ring_always = true;
         }
     }
     // the plan's own batch-1 workspace (after every choice that sizes the control words)

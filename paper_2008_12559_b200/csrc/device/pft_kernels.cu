@@ -94,7 +94,7 @@ cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t
 
 cudaError_t launch_k2(const K2Params& P, int r, uint32_t batch, cudaStream_t st) {
     const uint32_t gx = P.mode == K2_L2 ? (P.k2_ctas ? P.k2_ctas : 148u)
-                        : (P.mode == K2_FFT && P.k2_ctas > 0) ? (P.k2_ctas < P.P1 ? P.k2_ctas : P.P1)
+                        : (P.mode == K2_FFT && P.ring && P.k2_ctas > 0) ? (P.k2_ctas < P.P1 ? P.k2_ctas : P.P1)
                                                                : P.P1;
     const dim3 grid(gx, batch);
     switch (r) {
