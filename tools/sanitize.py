@@ -28,6 +28,10 @@ FORMS = [
     ("K2 L2 form", 2 ** 18, 2 ** 6, 7, 2 ** 12, 1, dict(second_pass="k2-l2")),
     ("K2 tail (last arrivals)", 2 ** 18, 2 ** 9, -5, 2 ** 12, 1, dict(second_pass="k2-fft", k2_at="tail")),
     ("fused K2 (grid barrier)", 2 ** 16, 128, 77, 2 ** 12, 2, dict(second_pass="k2-fft", k2_at="fused")),
+    ("K2 workers inside K1's grid (chained)", 2 ** 20, 2 ** 11, -7, 2 ** 13, 1, dict(second_pass="k2-fft", k2_at="tail")),
+    ("K2 workers, 3 workers, odd r", 2 ** 20, 1500, 0, 2 ** 13, 1, dict(second_pass="k2-fft", k2_at="tail", tail_ctas=3)),
+    ("ring K2 kernel, 6 CTAs looping over m1", 2 ** 20, 2 ** 11, -7, 2 ** 13, 1, dict(second_pass="k2-fft", k2_grid_ctas=6)),
+    ("ring K2 kernel, one CTA per m1", 2 ** 20, 2 ** 11, -7, 2 ** 13, 1, dict(second_pass="k2-fft", k2_at="grid")),
 ]
 
 
@@ -43,6 +47,8 @@ def run_form(label, N, M, mu, p, batch, kw) -> float:
         d.execute_ptr(x.data_ptr(), outs[i].data_ptr(), batch=batch, in_stride=N, d_ws=ws.data_ptr(), stream=s,
                       overlap=True)
     torch.cuda.synchronize()
+    if d.status(d_ws=ws.data_ptr()) != 0:
+        return float("inf")
     worst = 0.0
     for i in range(3):
         got = outs[i].cpu().numpy().reshape(batch, 2 * M + 1)
