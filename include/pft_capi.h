@@ -208,7 +208,11 @@ pft_status pft_partial_bytes(pft_dplan_t d, size_t batch, size_t* bytes);
  * transforms (execute i+1 streams while execute i reduces its last bins).  The caller
  * guarantees that d_in is NOT written by the preceding kernel on the stream (for example the
  * previous execute's d_out, or a kernel that triggers its dependents early, such as a PDL-enabled
- * GEMM).  Without the flag K1 starts only after the preceding work on the stream completed. */
+ * GEMM).  Executes that share a workspace must still complete in order: the preceding kernel on
+ * the stream has to be one that completes only after ITS predecessor completed -- another execute
+ * of this library (every K1 waits for its predecessor before it writes its workspace) or any
+ * kernel launched without programmatic stream serialization.  Without the flag K1 starts only
+ * after the preceding work on the stream completed. */
 #define PFT_EXEC_OVERLAP_PREVIOUS 1u
 
 /* execute: d_in holds `batch` signals of N complex128, signal b at d_in + b*in_stride;

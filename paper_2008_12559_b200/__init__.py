@@ -538,9 +538,11 @@ class DevicePlan:
     pointers (e.g. torch.Tensor.data_ptr() of complex128 CUDA tensors).
 
     second_pass: "auto" | "sum" (sum tail in K1) | "k2-fft" | "k2-dot" | "k2-direct" | "k2-l2"
-    k2_at: where the k2-fft form runs: "auto" | "grid" (own launch) | "tail" (K1's last
-    arrivals) | "fused" (K1 behind a grid barrier).  tail_ctas: sum-tail reducers / K2-tail
-    workers per signal (0 = plan).  batch_hint: typical batch per execute.  split: isolated
+    k2_at: where the k2-fft form runs: "auto" | "grid" (own launch) | "tail" (inside K1: its last
+    arrivals for r = 4..7, K2 worker CTAs riding in K1's grid for r = 8..18 on overlapped
+    executes) | "fused" (K1 behind a grid barrier).  tail_ctas: sum-tail reducers / K2-tail or
+    K2 workers per signal (0 = plan).  k2_grid_ctas: width of the ring K2 kernel's grid (0 = one
+    CTA per m1).  batch_hint: typical batch per execute.  split: isolated
     executes may run two K1 CTAs (a cluster) per residue class (PFT_EXEC_OVERLAP_PREVIOUS
     executes never do)."""
 
@@ -595,7 +597,8 @@ class DevicePlan:
 
     def tail_kind(self) -> str:
         """How execute finishes after K1: "K2 grid", "sum tail", "K2 tail" (K2's work by K1's
-        last arrivals) or "fused K2" (grid barrier, opt-in)."""
+        last arrivals), "fused K2" (grid barrier, opt-in) or "K2 workers in K1 (chained) / K2 grid"
+        (overlapped executes: K2 worker CTAs inside K1's grid; isolated ones: K1 + K2 grid)."""
         n = C.c_int()
         _check(lib().pft_dplan_tail_kind(self._h, C.byref(n)))
         return self.TAIL_KINDS[n.value]

@@ -1257,8 +1257,10 @@ pft_status pft_execute_host(pft_dplan_t dh, const pft_c128* h_in, size_t batch, 
     cuda_check(cudaMemcpyAsync(din, h_in, n_in * sizeof(pft_c128), cudaMemcpyHostToDevice, st), "H2D input");
     run_execute(d, din, batch, d->host.N, dout, sg->ws, st, false);
     cuda_check(cudaMemcpyAsync(h_out, dout, n_out * sizeof(pft_c128), cudaMemcpyDeviceToHost, st), "D2H output");
-    if (read_status(d->ws_view(sg->ws).status, true, st))
+    if (const int f = read_status(d->ws_view(sg->ws).status, true, st)) {
+        if (f & 2) fail(PFT_ERR_INTERNAL, "execute: a device-side wait of the second pass reached its bound");
         fail(PFT_ERR_NON_FINITE, "execute: non-finite input entries (non-finite output detected)");
+    }
     PFT_API_END
 }
 
