@@ -58,7 +58,8 @@ bool factor_radices(uint32_t n, pftdev::FftRadices& out) {
         return true;
     };
     // powers of two: radix 16 first (P1 = 128: 16 x 8, two block barriers instead of three
-    // for 8 x 8 x 2), then one 8, 4 or 2 for the rest
+    // for 8 x 8 x 2), then one 8, 4 or 2 for the rest (capping the radix at 8 / 4 measured C3
+    // 765 -> 781 / 812 us per batch, C2b and C4 unchanged: profiles/r02/ab_fft_radix_cap.log)
     while (m % 16 == 0) { if (!push(16)) return false; m /= 16; }
     while (m % 8 == 0) { if (!push(8)) return false; m /= 8; }
     while (m % 4 == 0) { if (!push(4)) return false; m /= 4; }

@@ -36,7 +36,7 @@ def parse_opts(text: str) -> dict:
     return out
 
 
-def run(cfg: str, p: int, opts: dict, reps: int, check: bool) -> dict:
+def run(cfg: str, p: int, opts: dict, reps: int, check: bool, streams: int = 1) -> dict:
     N, M, mu, _, kind, _ = bench.CONFIGS[cfg]
     B = bench.BATCH.get(cfg, 1)
     W = 2 * M + 1
@@ -49,18 +49,32 @@ def run(cfg: str, p: int, opts: dict, reps: int, check: bool) -> dict:
     ws = torch.zeros(-(-d.workspace_bytes(B) // 16), dtype=torch.complex128, device="cuda")
     out = torch.empty(W * B, dtype=torch.complex128, device="cuda")
     st = torch.cuda.Stream()
+    # streams > 1: free-running PDL chains, one per stream, each with its own workspace and output
+    # (forked once at the start of the graph, joined once at its end); execute i runs on chain i % streams
+    sts = [st] + [torch.cuda.Stream() for _ in range(streams - 1)]
+    wss = [ws] + [torch.zeros_like(ws) for _ in range(streams - 1)]
+    outs = [out] + [torch.empty_like(out) for _ in range(streams - 1)]
 
-    def ex(i, overlap=True):
-        d.execute_ptr(bufs[i % nbuf].data_ptr(), out.data_ptr(), batch=B, in_stride=N, d_ws=ws.data_ptr(),
-                      stream=st.cuda_stream, overlap=overlap)
+    def ex(i, overlap=True, k=0):
+        d.execute_ptr(bufs[i % nbuf].data_ptr(), outs[k].data_ptr(), batch=B, in_stride=N, d_ws=wss[k].data_ptr(),
+                      stream=sts[k].cuda_stream, overlap=overlap)
 
     with torch.cuda.stream(st):
         for i in range(3):
             ex(i)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=st):
+            if streams > 1:
+                fork = torch.cuda.Event()
+                fork.record(st)
+                for s2 in sts[1:]:
+                    s2.wait_event(fork)
             for i in range(reps):
-                ex(i)
+                ex(i, k=i % streams)
+            for s2 in sts[1:]:
+                j = torch.cuda.Event()
+                j.record(s2)
+                st.wait_event(j)
         g.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -69,7 +83,7 @@ def run(cfg: str, p: int, opts: dict, reps: int, check: bool) -> dict:
         e1.record(st)
     torch.cuda.synchronize()
     chained = e0.elapsed_time(e1) / reps * 1e3
-    out_chained = out[:W * min(B, 4)].clone()  # the chain's last execute (input bufs[(reps - 1) % nbuf])
+    out_chained = outs[(reps - 1) % streams][:W * min(B, 4)].clone()  # the last execute (input bufs[(reps - 1) % nbuf])
     with torch.cuda.stream(st):  # serialized executes (no overlap flag): device time per execute
         g2 = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g2, stream=st):
@@ -83,7 +97,7 @@ def run(cfg: str, p: int, opts: dict, reps: int, check: bool) -> dict:
         a1.record(st)
     torch.cuda.synchronize()
     iso = [a0.elapsed_time(a1) * 1e3 / min(reps, 50)]
-    res = {"cfg": cfg, "p": p, "opts": opts, "P1": d.P1, "P2": d.P2, "tail": d.tail_kind(),
+    res = {"cfg": cfg, "p": p, "opts": opts, "streams": streams, "P1": d.P1, "P2": d.P2, "tail": d.tail_kind(),
            "chained_us": chained, "isolated_us": float(np.median(iso)),
            "frac": 16 * N * B / (chained * 1e-6) / 1e9 / bench.measured_hbm_peak()[0]}
     if check:
@@ -110,12 +124,13 @@ def main():
     ap.add_argument("--variant", action="append", default=None, help="DevicePlan options k=v,k=v")
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--streams", type=int, default=1, help="free-running PDL chains (streams, workspaces, outputs)")
     a = ap.parse_args()
     variants = a.variant or [""]
     for cfg in a.configs:
         for v in variants:
             reps = a.reps if cfg not in ("c3", "c5") else 10
-            r = run(cfg, a.p or PICKS[cfg], parse_opts(v), reps, not a.no_check)
+            r = run(cfg, a.p or PICKS[cfg], parse_opts(v), reps, not a.no_check, a.streams)
             print(json.dumps(r), flush=True)
 
 
