@@ -18,7 +18,10 @@ GATE = 1e-11
 
 
 @pytest.mark.parametrize("N,M,mu,p", [(2 ** 20, 64, 0, 2 ** 14), (2 ** 22, 2 ** 9, 2 ** 20, 2 ** 13),
-                                     (3 * 5 * 7 * 64, 20, 11, 3 * 5 * 64)])
+                                     (3 * 5 * 7 * 64, 20, 11, 3 * 5 * 64),
+                                     # a plan whose chained executes take the K2 workers (r = 12): the sharded
+                                     # steps keep the plain slab layout and the K2 finalize
+                                     (2 ** 20, 2 ** 11, -7, 2 ** 13)])
 def test_execute_sharded_one_rank(pft, oracle, N, M, mu, p):
     import torch
     from paper_2008_12559_b200.sharded import NcclComm, ShardedTransform, nccl_available, nccl_unique_id
