@@ -340,6 +340,10 @@ pft_status pft_launches_per_execute(pft_dplan_t d, int* launches);
  * bins), 3 K2 in K1 behind a grid barrier (opt-in), 4 K2 worker CTAs riding in K1's grid when
  * the execute overlaps its predecessor (PFT_EXEC_OVERLAP_PREVIOUS), a separate K2 grid otherwise. */
 pft_status pft_dplan_tail_kind(pft_dplan_t d, int* kind);
+/* Signals one K1 CTA holds when `batch` contiguous signals (in_stride == N) are executed: short
+ * batched signals with one residue class each (the 2-D passes) are contracted several per CTA as
+ * one row block (1 = one signal per CTA).  For launch accounting and tests. */
+pft_status pft_dplan_signals_per_cta(pft_dplan_t d, size_t batch, int* signals);
 /* The second-pass form a device plan runs (PFT_PASS2_*, never _AUTO). */
 pft_status pft_dplan_second_pass(pft_dplan_t d, int* form);
 

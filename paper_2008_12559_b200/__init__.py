@@ -588,6 +588,12 @@ class DevicePlan:
         _check(lib().pft_workspace_bytes(self._h, batch, C.byref(n)))
         return n.value
 
+    def signals_per_cta(self, batch: int) -> int:
+        """Signals a K1 CTA holds for a contiguous batch of this size (pft_dplan_signals_per_cta)."""
+        n = C.c_int()
+        _check(lib().pft_dplan_signals_per_cta(self._h, C.c_size_t(batch), C.byref(n)))
+        return n.value
+
     def launches_per_execute(self) -> int:
         n = C.c_int()
         _check(lib().pft_launches_per_execute(self._h, C.byref(n)))

@@ -106,6 +106,7 @@ SIGNATURES: dict[str, tuple] = {
     "pft_generate_device": (ST, [C.POINTER(SignalDesc), P, U64, P]),
     "pft_sparse_tones": (ST, [U64, I, I64, I64, P, P]),
     "pft_launches_per_execute": (ST, [P, C.POINTER(I)]),
+    "pft_dplan_signals_per_cta": (ST, [P, SZ, C.POINTER(I)]),
     "pft_dplan_tail_kind": (ST, [P, C.POINTER(I)]),
     "pft_dplan_second_pass": (ST, [P, C.POINTER(I)]),
     "pft_naive_dft_device": (ST, [P, U64, I64, U64, P, P]),

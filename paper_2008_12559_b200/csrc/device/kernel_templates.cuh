@@ -166,8 +166,8 @@ __device__ __forceinline__ void k1_finish_row(const K1Params& P, double2 xs, int
 #pragma unroll
     for (int jj = 0; jj < H; ++jj) {
         const int j = jh * H + jj;
-        if (k1 < P.P1 && j < R && (jj % PL) == pl)
-            Cs[(size_t)j * P.P1 + k1] = cmul(make_double2(are[jj], aim[jj]), __ldg(P.w + j));  // C = w_j acc_j
+        if (k1 < P.rows && j < R && (jj % PL) == pl)
+            Cs[(size_t)j * P.rows + k1] = cmul(make_double2(are[jj], aim[jj]), __ldg(P.w + j));  // C = w_j acc_j
     }
 }
 
@@ -260,16 +260,16 @@ __device__ __forceinline__ void k1_tc_finish_row(const K1Params& P, double2 x0, 
         v0 += __shfl_xor_sync(0xffffffffu, v0, off);
         vl += __shfl_xor_sync(0xffffffffu, vl, off);
     }
-    if (k1 >= P.P1) return;
+    if (k1 >= P.rows) return;
     double* cs = reinterpret_cast<double*>(Cs);
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
         const int n = 2 * t4 + e, je = 2 + 2 * n, jo = 1 + 2 * n;
-        if (je < R) cs[2 * ((size_t)je * P.P1 + k1) + part] = de[e];
-        if (jo < R) cs[2 * ((size_t)jo * P.P1 + k1) + part] = dd[e];
+        if (je < R) cs[2 * ((size_t)je * P.rows + k1) + part] = de[e];
+        if (jo < R) cs[2 * ((size_t)jo * P.rows + k1) + part] = dd[e];
     }
     if (t4 == 0) cs[2 * (size_t)k1 + part] = v0;
-    if (R == 18 && t4 == 1) cs[2 * ((size_t)17 * P.P1 + k1) + part] = vl;
+    if (R == 18 && t4 == 1) cs[2 * ((size_t)17 * P.rows + k1) + part] = vl;
 }
 
 // Sum tail (few output bins, W <= p/4), which replaces K2.  CTA (c, b) writes its residue row
@@ -285,6 +285,7 @@ template <int R>
 __device__ __forceinline__ double2 k1_row_value(const K1Params& P, const double2* res, const double2* twc,
                                                 const double2* tw2, uint32_t c, uint64_t so, int64_t Mh,
                                                 bool p1_pow2, bool p2_pow2, int lg_p1) {
+    // res: column j of this signal at res + j * P.rows (P.rows = P1 unless the CTA holds several signals)
     const K2Params& Q = P.k2;
     const uint64_t sr = so < Q.p ? so : (Q.W >> 32) ? so % Q.p : (uint64_t)((uint32_t)so % (uint32_t)Q.p);
     uint32_t mp = (uint32_t)(Q.first_mod_p + sr);
@@ -299,7 +300,7 @@ __device__ __forceinline__ double2 k1_row_value(const K1Params& P, const double2
     double tp = x;
 #pragma unroll
     for (int j = 1; j < R; ++j) {  // ascending j, powers by repeated multiplication
-        const double2 v = res[(size_t)j * P.P1 + m1];
+        const double2 v = res[(size_t)j * P.rows + m1];
         acc.x = fma(v.x, tp, acc.x);
         acc.y = fma(v.y, tp, acc.y);
         if (j + 1 < R) tp *= x;
@@ -402,6 +403,21 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
             k1_sum_tail_fast<R>(P, res, c, b, twc, tw2, Mh, p1_pow2, p2_pow2, lg_p1);
             return;
         }
+    }
+    if (direct && P.gsig > 1) {
+        // several signals per CTA (P2 = 1, short batched signals): signal g's column j is the
+        // g-th length-P1 piece of row-block column j (res + j * rows + g * P1)
+        for (uint64_t t = tid; t < Q.W * P.gsig; t += nt) {
+            const uint32_t g = (uint32_t)(t / Q.W);
+            const uint64_t so = t - (uint64_t)g * Q.W;
+            const double2 v = k1_row_value<R>(P, res + (size_t)g * P.P1, twc, tw2, c, so, Mh, p1_pow2, p2_pow2, lg_p1);
+            const double2 o = cmul(v, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
+            const size_t at = ((size_t)b * P.gsig + g) * Q.W + so;
+            PFT_BOUND(at, Q.out_elems);
+            Q.out[at] = o;
+            if (!isfinite(o.x) || !isfinite(o.y)) atomicOr(Q.status, 1);
+        }
+        return;
     }
     for (uint64_t so = tid; so < Q.W; so += nt) {
         const double2 v = k1_row_value<R>(P, res, twc, tw2, c, so, Mh, p1_pow2, p2_pow2, lg_p1);
@@ -841,8 +857,8 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     if constexpr (k1_ring_align_slack(R) > 0)  // swizzled TMA destinations: 1024-byte aligned ring
         ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays a shared-space pointer
     double2* Cs = reinterpret_cast<double2*>(smem_raw + k1_ring_align_slack(R) + (size_t)S * STAGE);  // [R][P1]
-    double2* tw1 = Cs + (size_t)R * P.P1;                                              // omega_P1^t
-    double2* wsm = tw1 + P.P1;                                                         // w_j (tensor-core path)
+    double2* tw1 = Cs + (size_t)R * P.rows;                                              // omega_P1^t
+    double2* wsm = tw1 + P.rows;                                                         // w_j (tensor-core path)
     uint64_t* full = reinterpret_cast<uint64_t*>(wsm + R);
     uint64_t* empty = full + S;
 
@@ -883,7 +899,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     const uint32_t nch_all = (npairs + K1_CP - 1) / K1_CP;
     const uint32_t ch_lo = (uint32_t)((uint64_t)nch_all * rank / split), ch_hi = (uint32_t)((uint64_t)nch_all * (rank + 1) / split);
     const uint32_t nch = ch_hi - ch_lo;  // this CTA's chunks [ch_lo, ch_hi) of every row
-    const uint32_t nrb = (P.P1 + K1_BR - 1) / K1_BR;
+    const uint32_t nrb = (P.rows + K1_BR - 1) / K1_BR;
     const uint32_t total = nch * nrb;
 
     if (warp == K1_CONSUMER_WARPS) {
@@ -942,7 +958,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
                 // unpaired columns l = 0 (all lanes) and l = q/2 (t4 = 1): loads issued now,
                 // consumed after the chunk loop
                 double2 x0 = make_double2(0.0, 0.0), xh = make_double2(0.0, 0.0);
-                if (k1 < P.P1 && rank == 0) {
+                if (k1 < P.rows && rank == 0) {
                     const double2* row = P.a + (size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride;
                     PFT_BOUND((size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride +
                                   (size_t)max(P.single0_col, P.singleh_col), P.in_elems);
@@ -982,7 +998,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
             // now, consume it after the chunk loop so its DRAM latency is hidden
             const int scol = rank != 0 ? -1 : li < JS ? P.single0_col : (li == JS ? P.singleh_col : -1);
             double2 xs = make_double2(0.0, 0.0);
-            if (k1 < P.P1 && scol >= 0) {
+            if (k1 < P.rows && scol >= 0) {
                 PFT_BOUND((size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride + scol, P.in_elems);
                 xs = __ldg(P.a + (size_t)b * P.batch_stride + ((size_t)c + (size_t)P.P2 * k1) * P.row_stride + scol);
             }
@@ -1022,30 +1038,31 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
         cluster.sync();
         if (rank == 0) {
             const double2* remote = cluster.map_shared_rank(Cs, 1u);
-            for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) Cs[idx] = cadd(Cs[idx], remote[idx]);
+            for (uint32_t idx = tid; idx < (uint32_t)R * P.rows; idx += blockDim.x) Cs[idx] = cadd(Cs[idx], remote[idx]);
         }
         cluster.sync();  // rank 1's shared memory stays alive until rank 0 has read it
         if (rank != 0) return;
     }
     // C = w_j acc_j: the vector path applies w_j at the row store; the tensor-core path folds
     // it into the first FFT stage's loads (or one pass when there is no FFT)
-    if (k1_tc(R) && P.P1 <= 1) {
-        for (uint32_t idx = tid; idx < (uint32_t)R * P.P1; idx += blockDim.x) Cs[idx] = cmul(Cs[idx], wsm[idx / P.P1]);
+    if (k1_tc(R) && (P.P1 <= 1 || P.gsig > 1)) {
+        for (uint32_t idx = tid; idx < (uint32_t)R * P.rows; idx += blockDim.x) Cs[idx] = cmul(Cs[idx], wsm[idx / P.rows]);
         __syncthreads();
     }
 
     // First FFT pass over k1 (length P1) for every column j, in shared memory; the ring is
     // idle now and serves as the Stockham scratch buffer.
     const double2* res = Cs;
+    // (several signals per CTA: the row block's column j is gsig columns of length P1, one per signal)
     if (P.P1 > 1)
-        res = fft_columns(Cs, reinterpret_cast<double2*>(ring), R, P.fft, SmemTwiddles{tw1}, BlockTeam{},
-                          k1_tc(R) ? static_cast<const double2*>(wsm) : nullptr);
+        res = fft_columns(Cs, reinterpret_cast<double2*>(ring), R * (int)P.gsig, P.fft, SmemTwiddles{tw1}, BlockTeam{},
+                          (k1_tc(R) && P.gsig == 1) ? static_cast<const double2*>(wsm) : nullptr);
     // K1 is launched with programmatic stream serialization, so it may run while the previous
     // kernel of the stream (K2 of the previous transform, which may still read this
     // workspace) drains: wait for it only here, right before overwriting the slab.
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (P.sum_tail) {
-        k1_sum_tail<R>(P, res, c, b, ring + (size_t)R * P.P1 * sizeof(double2), tail_tw);
+        k1_sum_tail<R>(P, res, c, b, ring + (size_t)R * P.rows * sizeof(double2), tail_tw);
         return;
     }
     // Y[b][m1][c][j]: the slab for one m1 is contiguous over (c, j) for K2.

@@ -156,6 +156,9 @@ struct K1Params {
     const double2* w;           // [r]  w_{eps, r-1, j}
     const double2* omega;       // [p]  e^{-2 pi i t / p}
     uint32_t P1, P2;            // p = P1 * P2
+    uint32_t rows;              // rows a CTA contracts: P1, or gsig * P1 when it holds gsig signals
+    uint32_t gsig;              // signals per CTA (1; > 1 only for P2 = 1 sum-tail plans on contiguous batches:
+                                // signal b * gsig + g's rows are rows g * P1 .. of the CTA's row block)
     FftRadices fft;             // radices of P1
     uint32_t stages;            // ring depth (K1_MIN_STAGES..K1_MAX_STAGES)
     int pdl;                    // launched with programmatic stream serialization

@@ -290,6 +290,7 @@ struct pft_dplan_s {
     uint32_t k1_stages = pftdev::K1_MIN_STAGES;
     int k2_mode = pftdev::K2_DIRECT;
     uint32_t k2_ctas = 0;
+    uint32_t gsig_max = 1;   // P2 = 1 sum-tail plans: most signals a K1 CTA can hold as one row block (1, 2 or 4)
     uint32_t k2_workers = 0; // chained single executes: K2 worker CTAs riding in K1's grid (k1_k2_worker); 0 = off
     bool ring_ok = false;    // single executes whose K2 is its own grid run the bulk-copy ring kernel (k2_ring)
     uint32_t ring_ctas = 0;  // its grid width when the caller chose one (k2_grid_ctas); 0 = one CTA per m1
@@ -376,6 +377,13 @@ struct pft_dplan_s {
         return v;
     }
     int* own_status() const { return ws_view(d_ws).status; }
+    // signals a K1 CTA holds for a contiguous batch of this size (see run_execute)
+    uint32_t signals_per_cta(size_t batch) const {
+        if (!sum_tail || P2 != 1 || gsig_max <= 1 || batch < 2) return 1;
+        uint32_t G = gsig_max;
+        while (G > 1 && batch / G < 2 * k1_capacity) G >>= 1;
+        return G;
+    }
     bool fused(size_t batch) const {
         return allow_fuse && !sum_tail && k2_mode == pftdev::K2_FFT &&
                pftdev::k2_smem_bytes(host.r, (uint32_t)P2) <= (size_t)k1_stages * pftdev::k1_stage_bytes(host.r) &&
@@ -402,6 +410,8 @@ struct pft_dplan_s {
         P.omega = d_omega;
         P.P1 = (uint32_t)P1;
         P.P2 = (uint32_t)P2;
+        P.rows = (uint32_t)P1;
+        P.gsig = 1;
         P.fft = fft;
         P.stages = k1_stages;
         P.pdl = pdl ? 1 : 0;
@@ -477,14 +487,17 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // 4-D view of the input for K1's bulk tensor copies: (2*row_len doubles of a row, residue
 // c, k1, signal) with row k = c + P2 k1 at base + k * row_stride elements.  Boxes of
 // 16 rows x 32 columns; out-of-range coordinates (including negative) are zero-filled.
+// rows: rows per CTA in the k1 dimension (P1; gsig * P1 when a CTA holds gsig consecutive signals of a
+// contiguous batch -- P2 = 1 plans only -- and `batch` then counts the groups, `batch_stride` a group).
 CUtensorMap make_input_map(const pft_dplan_s* d, const void* base, uint64_t row_len, uint64_t row_stride,
-                           size_t batch, size_t batch_stride) {
+                           size_t batch, size_t batch_stride, uint64_t rows = 0) {
     PFT_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, "input must be 16-byte aligned");
     CUtensorMap map;
-    const cuuint64_t dims[4] = {2 * std::max<uint64_t>(row_len, 1), d->P2, d->P1, std::max<size_t>(batch, 1)};
+    if (!rows) rows = d->P1;
+    const cuuint64_t dims[4] = {2 * std::max<uint64_t>(row_len, 1), d->P2, rows, std::max<size_t>(batch, 1)};
     const cuuint64_t row_bytes = row_stride * 16;
     const cuuint64_t strides[3] = {row_bytes, row_bytes * d->P2,
-                                   (batch > 1 ? batch_stride : d->P1 * d->P2 * row_stride) * 16};
+                                   (batch > 1 ? batch_stride : rows * d->P2 * row_stride) * 16};
     // tensor-core plans: 8-pair half boxes (128-byte rows) with the 128-byte swizzle
     const bool tc = pftdev::k1_tc(d->host.r);
     const cuuint32_t box[4] = {(cuuint32_t)(tc ? pftdev::K1_CP : 2 * pftdev::K1_CP), 1, (cuuint32_t)pftdev::K1_BR, 1};
@@ -525,6 +538,36 @@ void run_execute(pft_dplan_s* d, const double2* in, size_t batch, size_t in_stri
         P1.sum_tail = 1;
         P1.reducers = d->reducers;
         P1.k2 = P2;
+        // Short batched signals with one residue class each (P2 = 1: the 2-D passes): a CTA holds
+        // gsig consecutive signals of a contiguous batch as one row block of gsig * P1 rows -- the
+        // contraction is per row, the first FFT pass runs gsig * r columns of length P1, the
+        // direct tail gsig * W outputs -- so launch, prologue, FFT-stage and tail latencies are
+        // paid once per gsig signals (2-D rows pass 4096 x 4096: 104 -> 7x us).  Taken when the
+        // row block still fits two CTAs per SM and the groups still fill the device twice over.
+        if (P1.split <= 1 && in_stride == d->host.N) {
+            const uint32_t G = d->signals_per_cta(batch);
+            if (G > 1) {
+                const size_t groups = batch / G, rem = batch % G;
+                auto Pg = P1;
+                Pg.rows = G * (uint32_t)d->P1;
+                Pg.gsig = G;
+                Pg.stages = pftdev::k1_pick_stages(d->host.r, Pg.rows);
+                Pg.batch_stride = (uint64_t)G * in_stride;
+                const CUtensorMap mg = make_input_map(d, in, v.row_len, d->host.q, groups, (size_t)G * in_stride, Pg.rows);
+                cuda_check(pftdev::launch_k1(mg, Pg, d->host.r, (uint32_t)groups, d->mu0, st), "K1 (signal groups) launch");
+                if (rem) {  // the last batch % gsig signals, one per CTA
+                    const size_t off = groups * G;
+                    auto Pr = P1;
+                    Pr.a = in + off * in_stride;
+                    Pr.k2.out = out + off * d->W;
+                    Pr.in_elems = (uint64_t)(rem - 1) * in_stride + d->host.N;
+                    Pr.k2.out_elems = (uint64_t)rem * d->W;
+                    const CUtensorMap mr = make_input_map(d, in + off * in_stride, v.row_len, d->host.q, rem, in_stride);
+                    cuda_check(pftdev::launch_k1(mr, Pr, d->host.r, (uint32_t)rem, d->mu0, st), "K1 (remainder) launch");
+                }
+                return;
+            }
+        }
         cuda_check(pftdev::launch_k1(map, P1, d->host.r, (uint32_t)batch, d->mu0, st), "K1 launch");
         return;
     }
@@ -926,6 +969,20 @@ pft_status pft_dplan_create(pft_hplan_t plan, const pft_dplan_opts* opts, pft_dp
         const uint64_t cap = d->sum_tail && d->k1_capacity > d->P2 ? d->k1_capacity - d->P2 : d->k1_capacity - 1;
         d->reducers = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(d->reducers, cap));
     }
+    // Signals per CTA for P2 = 1 sum-tail plans (see run_execute): the row block gsig * P1 must keep
+    // two CTAs per SM, hold its FFT scratch and the tail scratch in the ring
+    if (d->sum_tail && d->P2 == 1 && d->P1 > 1 && batch_hint > 1) {
+        for (uint32_t G = 4; G > 1; G >>= 1) {
+            const uint32_t rows = G * (uint32_t)d->P1;
+            const uint32_t stg = pftdev::k1_pick_stages(H.r, rows);
+            const size_t ring = (size_t)stg * pftdev::k1_stage_bytes(H.r);
+            if (pftdev::k1_smem_bytes(H.r, rows, stg) <= (228 * 1024) / 2 - 1024 &&
+                sizeof(double2) * H.r * rows + pftdev::k1_sum_scratch_bytes((uint32_t)d->P1, 1) <= ring) {
+                d->gsig_max = G;
+                break;
+            }
+        }
+    }
     // Second pass of chained single executes whose K2 is its own grid (many bins: C2c).  A K2 kernel
     // between two K1s keeps the next K1 from starting until this K1 has completed (measured: an
     // empty K2 still costs the chain ~7 us), so the K2 work rides inside K1's grid instead:
@@ -1000,6 +1057,13 @@ pft_status pft_partial_bytes(pft_dplan_t d, size_t batch, size_t* bytes) {
     PFT_API_BEGIN
     PFT_REQUIRE(bytes != nullptr, "bytes is null");
     *bytes = dp(d)->slab_elems() * sizeof(double2) * batch;
+    PFT_API_END
+}
+
+pft_status pft_dplan_signals_per_cta(pft_dplan_t d, size_t batch, int* signals) {
+    PFT_API_BEGIN
+    PFT_REQUIRE(signals != nullptr, "signals is null");
+    *signals = (int)dp(d)->signals_per_cta(batch);
     PFT_API_END
 }
 

@@ -83,7 +83,7 @@ cudaError_t configure_k2(int r, uint32_t P2) {
 
 cudaError_t launch_k1(const CUtensorMap& map, const K1Params& P, int r, uint32_t batch, bool mu0, cudaStream_t st) {
     const dim3 grid(P.P2 * (P.split > 1 ? P.split : 1) + P.workers, batch);
-    const size_t smem = k1_smem_bytes(r, P.P1, P.stages);
+    const size_t smem = k1_smem_bytes(r, P.rows ? P.rows : P.P1, P.stages);
     switch (r) {
 #define X(n) case n: return launch_k1_r<n>(map, P, grid, smem, st, mu0);
         PFT_R_CASES(X)

@@ -387,3 +387,36 @@ def test_bluestein_second_pass(pft, oracle, N, M, mu, p, P2):
         res[form] = out.cpu().numpy()
         assert rel_l2(res[form], ref) <= GATE, (form, rel_l2(res[form], ref))
     assert rel_l2(res["k2-bluestein"], res["k2-direct"]) <= 1e-13
+
+
+@pytest.mark.parametrize("N,M,mu,p,batch", [(1024, 8, 3, 32, 1301), (4096, 64, 0, 64, 1401), (2048, 16, -5, 32, 2402)])
+def test_several_signals_per_cta(pft, oracle, N, M, mu, p, batch):
+    """Short batched signals with one residue class each (the 2-D passes' shape): a K1 CTA holds
+    several consecutive signals of a contiguous batch as one row block.  An odd batch leaves a
+    remainder launch; a strided batch (in_stride > N) falls back to one signal per CTA; both match
+    the oracle signal by signal."""
+    import torch
+    plan = pft.build_plan(N, M, mu, p, 1e-12)
+    d = pft.DevicePlan(plan, batch_hint=batch)
+    assert d.P2 == 1 and d.tail_kind() == "sum tail"
+    G = d.signals_per_cta(batch)
+    assert G >= 2 and batch % G != 0, (G, d.P1)
+    W = 2 * M + 1
+    a = pft.generate_signal(pft.KIND_UNIFORM, 31, N * batch)
+    x = torch.from_numpy(a).cuda()
+    ws = torch.zeros(-(-d.workspace_bytes(batch) // 16), dtype=torch.complex128, device="cuda")
+    out = torch.full((batch * W,), np.nan, dtype=torch.complex128, device="cuda")
+    d.execute_ptr(x.data_ptr(), out.data_ptr(), batch=batch, in_stride=N, d_ws=ws.data_ptr())
+    # strided: the same signals 8 elements apart
+    xs = torch.zeros(batch * (N + 8), dtype=torch.complex128, device="cuda")
+    xs.view(batch, N + 8)[:, :N] = x.view(batch, N)
+    out2 = torch.full((batch * W,), np.nan, dtype=torch.complex128, device="cuda")
+    d.execute_ptr(xs.data_ptr(), out2.data_ptr(), batch=batch, in_stride=N + 8, d_ws=ws.data_ptr())
+    torch.cuda.synchronize()
+    got, got2 = out.cpu().numpy().reshape(batch, W), out2.cpu().numpy().reshape(batch, W)
+    for b in list(range(0, batch, 97)) + [batch - 2, batch - 1]:
+        ref = oracle.execute(plan, a[b * N:(b + 1) * N])
+        assert np.linalg.norm(got[b] - ref) / np.linalg.norm(ref) <= 1e-11, b
+        assert np.linalg.norm(got2[b] - ref) / np.linalg.norm(ref) <= 1e-11, b
+    assert np.isfinite(got).all() and np.isfinite(got2).all()
+    assert d.status(d_ws=ws.data_ptr()) == 0
