@@ -17,7 +17,13 @@
 //      e^{-2 pi i m1 c / p}, runs the length-P2 FFT over c in shared memory, and evaluates
 //      Eq. (7) only at the 2M+1 requested bins (m' = m mod p, m' = m1 + P1 m2):
 //      out[m] = e^{-pi i m/p} sum_j Chat[m'][j] ((m - mu)/p)^j.
-//      k2_direct_post<R> is the any-P2 fallback (direct sum over c).
+//      k2_direct_post<R> is the any-P2 fallback (direct sum over c); k2_ring<R> the same pass as
+//      a bulk-copy ring on the slab's own layout (isolated single executes, power-of-two p).
+//  Inside K1, after the first pass: the sum tail (few bins: K1 finishes the transform itself),
+//      the K2 tail (K2's work by the last-arriving CTAs, r = 4..7), or -- k1_contract_fft<R, MU0, 2>,
+//      r = 8..18, chained executes -- K2 worker CTAs riding at the end of the grid
+//      (k1_k2_worker: the second pass of transform i under the stream of transform i + 1).
+//      Short batched signals with one residue class each share a CTA (K1Params.gsig).
 //  K0  k0_generate              BASELINE.json synthetic inputs (bench only).
 //
 // Summation orders are fixed (lane-strided partial sums + xor-butterfly), so results
