@@ -144,7 +144,8 @@ __device__ __forceinline__ int fft_swz(int i) { return i ^ ((i >> 3) & 7); }
 template <int R, bool POW2, class TW>
 __device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__ src, double2* __restrict__ dst,
                                                      int ncols, int n, int Ns, int lg_nb, int lg_ns, const TW& tw,
-                                                     int t0, int nt, int sw = 0, const double2* colw = nullptr) {
+                                                     int t0, int nt, int sw = 0, const double2* colw = nullptr,
+                                                     int colw_div = 1) {
     const int nb = n / R;
     const uint32_t tstride = (uint32_t)(n / (Ns * R));
     for (int idx = t0; idx < ncols * nb; idx += nt) {
@@ -170,7 +171,7 @@ __device__ __forceinline__ void stockham_stage_fixed(const double2* __restrict__
             for (int r = 0; r < R; ++r) v[r] = s[j + r * nb];
         }
         if (colw) {
-            const double2 wc = colw[col];
+            const double2 wc = colw[colw_div == 1 ? col : col / colw_div];
 #pragma unroll
             for (int r = 0; r < R; ++r) v[r] = cmul(v[r], wc);
         }
@@ -220,11 +221,12 @@ __device__ __forceinline__ void stockham_stage_generic(const double2* __restrict
 
 // Full transform of ncols columns; returns the buffer holding the result (x or y).
 // Caller must team.sync() before (inputs written); the last stage ends with a team.sync().
-// colw: optional per-column factor folded into the first stage's loads (null = none).
+// colw: optional per-column factor folded into the first stage's loads (null = none); column
+// col takes colw[col / colw_div] (several columns per factor: several signals per CTA).
 template <class TW, class Team = BlockTeam>
 __device__ __forceinline__ double2* fft_columns(double2* x, double2* y, int ncols, const FftRadices& plan,
                                                 const TW& tw, const Team team = Team{},
-                                                const double2* colw = nullptr) {
+                                                const double2* colw = nullptr, int colw_div = 1) {
     const int t0 = team.tid(), nt = team.size();
     double2* src = x;
     double2* dst = y;
@@ -241,22 +243,22 @@ __device__ __forceinline__ double2* fft_columns(double2* x, double2* y, int ncol
             // swizzle the buffer between stages 0 and 1 (n >= 64 keeps every 8-block in a column)
             const int sw = (n >= 64 && plan.count >= 2) ? (st == 0 ? 1 : st == 1 ? 2 : 0) : 0;
             switch (R) {
-                case 2: stockham_stage_fixed<2, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw); break;
-                case 4: stockham_stage_fixed<4, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw); break;
-                case 8: stockham_stage_fixed<8, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw); break;
-                default: stockham_stage_fixed<16, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw); break;
+                case 2: stockham_stage_fixed<2, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw, colw_div); break;
+                case 4: stockham_stage_fixed<4, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw, colw_div); break;
+                case 8: stockham_stage_fixed<8, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw, colw_div); break;
+                default: stockham_stage_fixed<16, true>(src, dst, ncols, n, Ns, lg_nb, lg_ns, tw, t0, nt, sw, cw, colw_div); break;
             }
             lg_ns += lg_r;
         } else {
             switch (R) {
-                case 2: stockham_stage_fixed<2, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
-                case 3: stockham_stage_fixed<3, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
-                case 4: stockham_stage_fixed<4, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
-                case 8: stockham_stage_fixed<8, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
-                case 16: stockham_stage_fixed<16, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw); break;
+                case 2: stockham_stage_fixed<2, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw, colw_div); break;
+                case 3: stockham_stage_fixed<3, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw, colw_div); break;
+                case 4: stockham_stage_fixed<4, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw, colw_div); break;
+                case 8: stockham_stage_fixed<8, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw, colw_div); break;
+                case 16: stockham_stage_fixed<16, false>(src, dst, ncols, n, Ns, 0, 0, tw, t0, nt, 0, cw, colw_div); break;
                 default:
                     if (cw) {  // generic radix: apply the column factor in place first
-                        for (int i = t0; i < ncols * n; i += nt) src[i] = cmul(src[i], cw[i / n]);
+                        for (int i = t0; i < ncols * n; i += nt) src[i] = cmul(src[i], cw[i / n / colw_div]);
                         team.sync();
                     }
                     stockham_stage_generic(src, dst, ncols, n, Ns, R, tw, t0, nt);

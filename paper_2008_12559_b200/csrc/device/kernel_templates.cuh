@@ -290,8 +290,9 @@ __device__ __forceinline__ void k1_tc_finish_row(const K1Params& P, double2 x0, 
 template <int R>
 __device__ __forceinline__ double2 k1_row_value(const K1Params& P, const double2* res, const double2* twc,
                                                 const double2* tw2, uint32_t c, uint64_t so, int64_t Mh,
-                                                bool p1_pow2, bool p2_pow2, int lg_p1) {
+                                                bool p1_pow2, bool p2_pow2, int lg_p1, bool unit_tw = false) {
     // res: column j of this signal at res + j * P.rows (P.rows = P1 unless the CTA holds several signals)
+    // unit_tw: one residue class per signal (c = 0): both twiddles are exactly 1, the tables are not read
     const K2Params& Q = P.k2;
     const uint64_t sr = so < Q.p ? so : (Q.W >> 32) ? so % Q.p : (uint64_t)((uint32_t)so % (uint32_t)Q.p);
     uint32_t mp = (uint32_t)(Q.first_mod_p + sr);
@@ -311,6 +312,7 @@ __device__ __forceinline__ double2 k1_row_value(const K1Params& P, const double2
         acc.y = fma(v.y, tp, acc.y);
         if (j + 1 < R) tp *= x;
     }
+    if (unit_tw) return acc;  // cmul(., (1, 0)) is the identity on finite values
     return cmul(cmul(acc, twc[m1]), tw2[e2]);
 }
 
@@ -385,17 +387,19 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
     // omega_p^{(m mod p) c} = omega_p^{m1 c} omega_P2^{m2 c}: both factors from tables in the idle ring
     double2* twc = reinterpret_cast<double2*>(scratch);  // [P1] omega_p^{m1 c}
     double2* tw2 = twc + P.P1;                            // [P2] omega_P2^t
-    // entries t < blockDim.x were prefetched during the stream (tail_tw); the rest load now
-    for (uint32_t t = tid; t < P.P1 + P.P2; t += nt) {
-        double2 v = tail_tw;
-        if (t >= (uint32_t)nt) v = __ldg(P.omega + (t < P.P1 ? (size_t)t * c : (size_t)(t - P.P1) * P.P1));  // m1 c < p
-        twc[t] = v;  // twc[P1 + t'] is tw2[t']
-    }
-    __syncthreads();
     // One residue class per signal (P2 = 1: short batched signals, e.g. the 2-D passes): the
     // row is the output; no row store, ready flag, ticket or read-back (same arithmetic as a
-    // one-row reduction: cadd(0, v) = v).
+    // one-row reduction: cadd(0, v) = v), and no twiddle tables (c = 0: every entry is 1).
     const bool direct = P.P2 == 1;
+    // entries t < blockDim.x were prefetched during the stream (tail_tw); the rest load now
+    if (!direct) {
+        for (uint32_t t = tid; t < P.P1 + P.P2; t += nt) {
+            double2 v = tail_tw;
+            if (t >= (uint32_t)nt) v = __ldg(P.omega + (t < P.P1 ? (size_t)t * c : (size_t)(t - P.P1) * P.P1));  // m1 c < p
+            twc[t] = v;  // twc[P1 + t'] is tw2[t']
+        }
+        __syncthreads();
+    }
     // Few residue classes and few outputs (batched short signals, e.g. C3: P2 = 2, W = 513):
     // only the last CTA of the signal to arrive reduces, each thread summing the P2 rows of its
     // own outputs with all loads in flight at once and its own row's values from registers;
@@ -416,7 +420,7 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
         for (uint64_t t = tid; t < Q.W * P.gsig; t += nt) {
             const uint32_t g = (uint32_t)(t / Q.W);
             const uint64_t so = t - (uint64_t)g * Q.W;
-            const double2 v = k1_row_value<R>(P, res + (size_t)g * P.P1, twc, tw2, c, so, Mh, p1_pow2, p2_pow2, lg_p1);
+            const double2 v = k1_row_value<R>(P, res + (size_t)g * P.P1, twc, tw2, c, so, Mh, p1_pow2, p2_pow2, lg_p1, true);
             const double2 o = cmul(v, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
             const size_t at = ((size_t)b * P.gsig + g) * Q.W + so;
             PFT_BOUND(at, Q.out_elems);
@@ -426,7 +430,7 @@ __device__ __forceinline__ void k1_sum_tail(const K1Params& P, const double2* re
         return;
     }
     for (uint64_t so = tid; so < Q.W; so += nt) {
-        const double2 v = k1_row_value<R>(P, res, twc, tw2, c, so, Mh, p1_pow2, p2_pow2, lg_p1);
+        const double2 v = k1_row_value<R>(P, res, twc, tw2, c, so, Mh, p1_pow2, p2_pow2, lg_p1, direct);
         if (direct) {
             const double2 o = cmul(v, __ldg(Q.post_twiddles + so));  // e^{-pi i m / p}
             PFT_BOUND((size_t)b * Q.W + so, Q.out_elems);
@@ -1051,7 +1055,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     }
     // C = w_j acc_j: the vector path applies w_j at the row store; the tensor-core path folds
     // it into the first FFT stage's loads (or one pass when there is no FFT)
-    if (k1_tc(R) && (P.P1 <= 1 || P.gsig > 1)) {
+    if (k1_tc(R) && P.P1 <= 1) {
         for (uint32_t idx = tid; idx < (uint32_t)R * P.rows; idx += blockDim.x) Cs[idx] = cmul(Cs[idx], wsm[idx / P.rows]);
         __syncthreads();
     }
@@ -1062,7 +1066,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_contract_fft(const __grid_co
     // (several signals per CTA: the row block's column j is gsig columns of length P1, one per signal)
     if (P.P1 > 1)
         res = fft_columns(Cs, reinterpret_cast<double2*>(ring), R * (int)P.gsig, P.fft, SmemTwiddles{tw1}, BlockTeam{},
-                          (k1_tc(R) && P.gsig == 1) ? static_cast<const double2*>(wsm) : nullptr);
+                          k1_tc(R) ? static_cast<const double2*>(wsm) : nullptr, (int)P.gsig);
     // K1 is launched with programmatic stream serialization, so it may run while the previous
     // kernel of the stream (K2 of the previous transform, which may still read this
     // workspace) drains: wait for it only here, right before overwriting the slab.

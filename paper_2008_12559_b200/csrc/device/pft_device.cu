@@ -60,6 +60,9 @@ bool factor_radices(uint32_t n, pftdev::FftRadices& out) {
     // powers of two: radix 16 first (P1 = 128: 16 x 8, two block barriers instead of three
     // for 8 x 8 x 2), then one 8, 4 or 2 for the rest (capping the radix at 8 / 4 measured C3
     // 765 -> 781 / 812 us per batch, C2b and C4 unchanged: profiles/r02/ab_fft_radix_cap.log)
+    // (n = 64 as 8 x 8: twice the butterflies of 16 x 4's first stage at a third of its dependent chain --
+    // the 2-D rows pass, 36 columns of 64 per CTA: 84.3 -> 79.8 us)
+    if (m == 64) { push(8); push(8); m = 1; }
     while (m % 16 == 0) { if (!push(16)) return false; m /= 16; }
     while (m % 8 == 0) { if (!push(8)) return false; m /= 8; }
     while (m % 4 == 0) { if (!push(4)) return false; m /= 4; }
